@@ -1,0 +1,417 @@
+"""ctypes front-end to the parity checkers.  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU legs may import
+this module; the product package (``paper_2605_06534_b200``) never does.
+
+Two checkers are exposed, both as numpy-in / numpy-out functions:
+
+* ``Restatement`` -- oracle/_build/liboracle.so, the C restatement in
+  wsync_oracle.c (F32/I32/BF16, cross-dim extension, synthetic generator).
+* ``Reference``   -- oracle/_ref/libref_capi.so, the UNMODIFIED reference
+  transfer engine (/root/reference/proj/src/transfer) behind ref_capi.cpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+F32, I32, BF16 = 0, 1, 2
+NP_DTYPE = {F32: np.float32, I32: np.int32, BF16: np.uint16}
+ESZ = {F32: 4, I32: 4, BF16: 2}
+
+STATUS = {0: "OK", 1: "ShapeMismatch", 2: "PayloadFormatError", 3: "IndexOutOfShard",
+          4: "IndivisibleShape", 5: "UnknownModuleKind", 6: "IncompleteCoverage",
+          7: "RelayTimeout", 8: "IntegrityError", 10: "TransferError", 22: "Capacity",
+          23: "InvalidArgument", 99: "Exception"}
+
+_p = np.ctypeslib.ndpointer
+_u64p = C.POINTER(C.c_uint64)
+_i64p = C.POINTER(C.c_int64)
+
+
+def build():
+    """Compile the restatement (and the reference wrapper when /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _shape(shape):
+    return (C.c_int64 * max(1, len(shape)))(*shape)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = STATUS.get(code, str(code))
+
+
+class Restatement:
+    """The C restatement (wsync_oracle.c)."""
+
+    def __init__(self, path=None):
+        path = path or os.path.join(HERE, "_build", "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = self.lib = C.CDLL(path)
+        L.wso_diff_shards.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                      C.c_void_p, C.c_void_p, _u64p]
+        L.wso_apply_delta.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_void_p,
+                                      C.c_void_p, C.c_uint64]
+        L.wso_reslice_delta.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                        C.c_void_p, _u64p]
+        L.wso_extract_shard.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_void_p, C.c_void_p]
+        L.wso_copy_overlap_box.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_int64,
+                                           C.c_int64, C.c_void_p, C.c_int, C.c_int64,
+                                           C.c_int64, C.c_void_p]
+        L.wso_copy_overlap_box.restype = C.c_int64
+        L.wso_is_sparse.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
+        L.wso_param_key.argtypes = [C.c_uint64, C.c_char_p]
+        L.wso_param_key.restype = C.c_uint64
+        L.wso_gen_pair_bf16.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p]
+        L.wso_sparse_payload_size.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64]
+        L.wso_sparse_payload_size.restype = C.c_uint64
+        L.wso_encode_sparse.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_void_p,
+                                        C.c_void_p, C.c_uint64, C.c_void_p, _u64p]
+
+    def diff_shards(self, dtype, prev, next_):
+        prev = np.ascontiguousarray(prev, NP_DTYPE[dtype]).ravel()
+        next_ = np.ascontiguousarray(next_, NP_DTYPE[dtype]).ravel()
+        if prev.shape != next_.shape:
+            raise OracleError(1, "diff_shards shape mismatch")
+        idx = np.empty(prev.size, np.uint64)
+        val = np.empty(prev.size, NP_DTYPE[dtype])
+        nnz = C.c_uint64()
+        rc = self.lib.wso_diff_shards(dtype, _ptr(prev), _ptr(next_), prev.size,
+                                      _ptr(idx), _ptr(val), C.byref(nnz))
+        if rc:
+            raise OracleError(rc)
+        return idx[:nnz.value].copy(), val[:nnz.value].copy()
+
+    def apply_delta(self, dtype, target, idx, val):
+        """In-place on a copy; returns (result, status)."""
+        t = np.ascontiguousarray(target, NP_DTYPE[dtype]).ravel().copy()
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        rc = self.lib.wso_apply_delta(dtype, _ptr(t), t.size, _ptr(idx), _ptr(val), idx.size)
+        return t, rc
+
+    def reslice_delta(self, dtype, full_shape, src, dst, idx, val, allow_cross_dim=True):
+        """src/dst are (slice_dim, start, end) with slice_dim < 0 for full."""
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        oi = np.empty(max(1, idx.size), np.uint64)
+        ov = np.empty(max(1, idx.size), NP_DTYPE[dtype])
+        n = C.c_uint64()
+        rc = self.lib.wso_reslice_delta(dtype, _shape(full_shape), len(full_shape),
+                                        src[0], src[1], src[2], dst[0], dst[1], dst[2],
+                                        int(allow_cross_dim), _ptr(idx), _ptr(val), idx.size,
+                                        _ptr(oi), _ptr(ov), C.byref(n))
+        if rc:
+            raise OracleError(rc)
+        return oi[:n.value].copy(), ov[:n.value].copy()
+
+    def extract_shard(self, dtype, full, full_shape, desc):
+        out = np.empty(shard_elems(full_shape, desc), NP_DTYPE[dtype])
+        full = np.ascontiguousarray(full, NP_DTYPE[dtype])
+        rc = self.lib.wso_extract_shard(dtype, _shape(full_shape), len(full_shape), desc[0],
+                                        desc[1], desc[2], _ptr(full), _ptr(out))
+        if rc:
+            raise OracleError(rc)
+        return out
+
+    def copy_overlap_box(self, dtype, full_shape, dst_desc, dst, src_desc, src):
+        dst = np.ascontiguousarray(dst, NP_DTYPE[dtype]).copy()
+        src = np.ascontiguousarray(src, NP_DTYPE[dtype])
+        n = self.lib.wso_copy_overlap_box(dtype, _shape(full_shape), len(full_shape),
+                                          dst_desc[0], dst_desc[1], dst_desc[2], _ptr(dst),
+                                          src_desc[0], src_desc[1], src_desc[2], _ptr(src))
+        if n < 0:
+            raise OracleError(-n)
+        return dst, n
+
+    def is_sparse(self, nnz, n, threshold):
+        return bool(self.lib.wso_is_sparse(nnz, n, threshold))
+
+    def param_key(self, seed, name):
+        return self.lib.wso_param_key(seed, name.encode())
+
+    def gen_pair_bf16(self, seed, name, full_shape, desc, density):
+        n = shard_elems(full_shape, desc)
+        prev = np.empty(n, np.uint16)
+        nxt = np.empty(n, np.uint16)
+        self.lib.wso_gen_pair_bf16(self.param_key(seed, name), _shape(full_shape),
+                                   len(full_shape), desc[0], desc[1], desc[2],
+                                   change_threshold(density), _ptr(prev), _ptr(nxt))
+        return prev, nxt
+
+    def encode_sparse(self, dtype, shape, idx, val, index_width=4):
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        size = self.lib.wso_sparse_payload_size(dtype, len(shape), index_width, idx.size)
+        out = np.empty(size, np.uint8)
+        n = C.c_uint64()
+        rc = self.lib.wso_encode_sparse(dtype, _shape(shape), len(shape), index_width,
+                                        _ptr(idx), _ptr(val), idx.size, _ptr(out), C.byref(n))
+        if rc:
+            raise OracleError(rc)
+        return out[:n.value].tobytes()
+
+
+def change_threshold(density):
+    """Bernoulli threshold on the top 32 bits of a draw: floor(d * 2^32), clamped."""
+    return int(min(max(density, 0.0), 1.0) * 4294967296.0)
+
+
+def shard_shape(full_shape, desc):
+    s = list(full_shape)
+    if desc[0] >= 0:
+        s[desc[0]] = desc[2] - desc[1]
+    return s
+
+
+def shard_elems(full_shape, desc):
+    return int(np.prod(shard_shape(full_shape, desc), dtype=np.int64))
+
+
+class RefParam(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("kind", C.c_int), ("ndims", C.c_int),
+                ("shape", C.c_int64 * 4), ("layer", C.c_int)]
+
+
+def ref_params(manifest):
+    """manifest: list of (name, kind, shape, layer) -> ctypes array (keeps names alive)."""
+    arr = (RefParam * len(manifest))()
+    keep = []
+    for i, (name, kind, shape, layer) in enumerate(manifest):
+        b = name.encode()
+        keep.append(b)
+        arr[i].name = b
+        arr[i].kind = kind
+        arr[i].ndims = len(shape)
+        for k, d in enumerate(shape):
+            arr[i].shape[k] = d
+        arr[i].layer = layer
+    return arr, keep
+
+
+class Reference:
+    """The compiled, unmodified reference (oracle/_ref/libref_capi.so)."""
+
+    def __init__(self, path=None):
+        path = path or os.path.join(HERE, "_ref", "libref_capi.so")
+        if not os.path.exists(path):
+            build()
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_diff_shards.argtypes = [C.c_int, _i64p, C.c_int, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, _u64p]
+        L.ref_apply_delta.argtypes = [C.c_int, _i64p, C.c_int, C.c_void_p, _i64p, C.c_int,
+                                      C.c_void_p, C.c_void_p, C.c_uint64]
+        L.ref_reslice_delta.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_int, C.c_int64, C.c_int64, _i64p,
+                                        C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                        C.c_void_p, C.c_void_p, _u64p, _i64p]
+        L.ref_extract_shard.argtypes = [C.c_int, _i64p, C.c_int, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_copy_overlap.argtypes = [C.c_int, _i64p, C.c_int, C.c_void_p, C.c_int64,
+                                       _i64p, C.c_void_p, C.c_int64, C.c_int]
+        L.ref_copy_overlap.restype = C.c_int64
+        L.ref_encode_sparse.argtypes = [C.c_int, _i64p, C.c_int, C.c_void_p, C.c_void_p,
+                                        C.c_uint64, C.c_int, C.c_void_p, C.c_uint64, _u64p]
+        L.ref_encode_dense.argtypes = [C.c_int, _i64p, C.c_int, C.c_void_p, C.c_void_p,
+                                       C.c_uint64, _u64p]
+        L.ref_decode_payload.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), _i64p, _u64p, C.c_void_p,
+                                         C.c_void_p]
+        L.ref_peek_payload_size.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_peek_payload_size.restype = C.c_int64
+        L.ref_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.c_int, _i64p, C.POINTER(C.c_int), _i64p,
+                               C.POINTER(C.c_int), C.c_int]
+        L.ref_state_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64]
+        L.ref_state_create.restype = C.c_void_p
+        L.ref_state_create_toy.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                           C.c_uint64]
+        L.ref_state_create_toy.restype = C.c_void_p
+        L.ref_state_destroy.argtypes = [C.c_void_p]
+        L.ref_state_nparams.argtypes = [C.c_void_p]
+        L.ref_state_param.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), _i64p, C.POINTER(C.c_int)]
+        L.ref_state_param.restype = C.c_char_p
+        L.ref_state_weights.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ref_state_weights.restype = C.c_void_p
+        L.ref_state_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
+                                    C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+        L.ref_state_model_bytes.argtypes = [C.c_void_p]
+        L.ref_state_model_bytes.restype = C.c_double
+        L.ref_state_serve.argtypes = [C.c_void_p, C.c_int, C.c_int, _u64p]
+        L.ref_state_serve.restype = C.c_void_p
+        L.ref_state_ncodecs.argtypes = [C.c_void_p]
+        L.ref_state_codec.argtypes = [C.c_void_p, C.c_int, _i64p]
+
+    def _check(self, rc):
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode(errors="replace"))
+
+    def diff_shards(self, dtype, shape, prev, next_):
+        prev = np.ascontiguousarray(prev, NP_DTYPE[dtype])
+        next_ = np.ascontiguousarray(next_, NP_DTYPE[dtype])
+        n = int(np.prod(shape))
+        idx = np.empty(max(1, n), np.uint64)
+        val = np.empty(max(1, n), NP_DTYPE[dtype])
+        nnz = C.c_uint64()
+        self._check(self.lib.ref_diff_shards(dtype, _shape(shape), len(shape), _ptr(prev),
+                                             _ptr(next_), _ptr(idx), _ptr(val), C.byref(nnz)))
+        return idx[:nnz.value].copy(), val[:nnz.value].copy()
+
+    def apply_delta(self, dtype, shape, target, delta_shape, idx, val):
+        """Returns (updated target, status) -- partial on IndexOutOfShard like the ref."""
+        t = np.ascontiguousarray(target, NP_DTYPE[dtype]).copy()
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        rc = self.lib.ref_apply_delta(dtype, _shape(shape), len(shape), _ptr(t),
+                                      _shape(delta_shape), len(delta_shape), _ptr(idx),
+                                      _ptr(val), idx.size)
+        return t, rc
+
+    def reslice_delta(self, dtype, full_shape, src, dst, delta_shape, idx, val):
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        oi = np.empty(max(1, idx.size), np.uint64)
+        ov = np.empty(max(1, idx.size), NP_DTYPE[dtype])
+        n = C.c_uint64()
+        osh = (C.c_int64 * 8)()
+        self._check(self.lib.ref_reslice_delta(
+            dtype, _shape(full_shape), len(full_shape), src[0], src[1], src[2], dst[0],
+            dst[1], dst[2], _shape(delta_shape), len(delta_shape), _ptr(idx), _ptr(val),
+            idx.size, _ptr(oi), _ptr(ov), C.byref(n), osh))
+        return oi[:n.value].copy(), ov[:n.value].copy(), list(osh[:len(full_shape)])
+
+    def extract_shard(self, dtype, full, full_shape, desc):
+        out = np.empty(shard_elems(full_shape, desc), NP_DTYPE[dtype])
+        full = np.ascontiguousarray(full, NP_DTYPE[dtype])
+        self._check(self.lib.ref_extract_shard(dtype, _shape(full_shape), len(full_shape),
+                                               desc[0], desc[1], desc[2], _ptr(full),
+                                               _ptr(out)))
+        return out
+
+    def copy_overlap(self, dtype, dst_shape, dst, dst_start, src_shape, src, src_start, dim):
+        dst = np.ascontiguousarray(dst, NP_DTYPE[dtype]).copy()
+        src = np.ascontiguousarray(src, NP_DTYPE[dtype])
+        n = self.lib.ref_copy_overlap(dtype, _shape(dst_shape), len(dst_shape), _ptr(dst),
+                                      dst_start, _shape(src_shape), _ptr(src), src_start, dim)
+        if n < 0:
+            raise OracleError(-n, self.lib.ref_last_error().decode(errors="replace"))
+        return dst, n
+
+    def encode_sparse(self, dtype, shape, idx, val, index_width=0):
+        idx = np.ascontiguousarray(idx, np.uint64)
+        val = np.ascontiguousarray(val, NP_DTYPE[dtype])
+        cap = 64 + 12 * idx.size
+        out = np.empty(cap, np.uint8)
+        n = C.c_uint64()
+        self._check(self.lib.ref_encode_sparse(dtype, _shape(shape), len(shape), _ptr(idx),
+                                               _ptr(val), idx.size, index_width, _ptr(out),
+                                               cap, C.byref(n)))
+        return out[:n.value].tobytes()
+
+    def plan(self, manifest, train, serve):
+        """train=(tp,pp,dp), serve=(tp,pp) -> (push list, pull list) of descriptor tuples."""
+        arr, keep = ref_params(manifest)
+        cap = 1 << 16
+        push = (C.c_int64 * (7 * cap))()
+        pull = (C.c_int64 * (8 * cap))()
+        npush, npull = C.c_int(), C.c_int()
+        self._check(self.lib.ref_plan(arr, len(manifest), *train, *serve, push,
+                                      C.byref(npush), pull, C.byref(npull), cap))
+        pushes = [tuple(push[7 * i:7 * i + 7]) for i in range(npush.value)]
+        pulls = [tuple(pull[8 * i:8 * i + 8]) for i in range(npull.value)]
+        return pushes, pulls
+
+    def state(self, manifest, dtype, train, serve, density, seed):
+        arr, keep = ref_params(manifest)
+        h = self.lib.ref_state_create(arr, len(manifest), dtype, *train, *serve, density, seed)
+        if not h:
+            raise OracleError(99, self.lib.ref_last_error().decode(errors="replace"))
+        return RefState(self, h)
+
+    def toy_state(self, layers, hidden, vocab, dtype, train, serve, density, seed):
+        h = self.lib.ref_state_create_toy(layers, hidden, vocab, dtype, *train, *serve,
+                                          density, seed)
+        if not h:
+            raise OracleError(99, self.lib.ref_last_error().decode(errors="replace"))
+        return RefState(self, h)
+
+
+REPORT_FIELDS = ("wall_s", "push_s", "pull_s", "encode_s", "apply_s", "pushed_bytes",
+                 "pulled_bytes", "push_buckets", "pull_buckets", "dense_shards",
+                 "sparse_shards")
+
+
+class RefState:
+    """A reference TrainState/ServeState pair (bench.cpp:5-43)."""
+
+    def __init__(self, ref, h):
+        self.ref, self.h, L = ref, h, ref.lib
+        self.params = []
+        for i in range(L.ref_state_nparams(h)):
+            kind, nd, layer = C.c_int(), C.c_int(), C.c_int()
+            shp = (C.c_int64 * 4)()
+            name = L.ref_state_param(h, i, C.byref(kind), C.byref(nd), shp, C.byref(layer))
+            self.params.append((name.decode(), kind.value, list(shp[:nd.value]), layer.value))
+        self.dtype = None
+
+    def __del__(self):
+        try:
+            self.ref.lib.ref_state_destroy(self.h)
+        except Exception:
+            pass
+
+    def weights(self, i, which, dtype):
+        n = int(np.prod(self.params[i][2]))
+        p = self.ref.lib.ref_state_weights(self.h, i, which)
+        buf = (C.c_uint8 * (n * ESZ[dtype])).from_address(p)
+        return np.frombuffer(buf, NP_DTYPE[dtype]).copy()
+
+    def run(self, mode_async=True, shard_aware=True, sparse=True, threshold=0.20,
+            bucket_bytes=64 << 20, force_wide=False):
+        rep = (C.c_double * 11)()
+        self.ref._check(self.ref.lib.ref_state_run(self.h, int(mode_async), int(shard_aware),
+                                                   int(sparse), threshold, bucket_bytes,
+                                                   int(force_wide), rep))
+        return dict(zip(REPORT_FIELDS, rep[:11]))
+
+    def model_bytes(self):
+        return self.ref.lib.ref_state_model_bytes(self.h)
+
+    def serve(self, rank, i, dtype):
+        nb = C.c_uint64()
+        p = self.ref.lib.ref_state_serve(self.h, rank, i, C.byref(nb))
+        if not p:
+            return None
+        buf = (C.c_uint8 * nb.value).from_address(p)
+        return np.frombuffer(buf, NP_DTYPE[dtype]).copy()
+
+    def codecs(self):
+        out = []
+        d = (C.c_int64 * 7)()
+        for k in range(self.ref.lib.ref_state_ncodecs(self.h)):
+            c = self.ref.lib.ref_state_codec(self.h, k, d)
+            out.append((tuple(d[:7]), chr(c)))
+        return out
