@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: dense-equivalent weight-sync GB/s (encode+route+apply) on B200.
+
+Workload (BASELINE.json configs[1], scaled to the GPUs given): a Qwen3-8B-
+shaped bf16 model (8.19 G elements), 1% i.i.d. change density, trainer
+FSDP-N shards (every parameter split along dim 0 over the N ranks) -> serving
+TP2 replicas (TP1 at N=1), one rank per GPU.  A "step" is one full sync of
+the whole model: K1 encode on every trainer shard, route (reslice + NVLink
+exchange at N>1) and in-place apply on every serving shard.  Steps alternate
+direction (prev->next, next->prev) so every step is a genuine sync and the
+serving weights stay verifiable.
+
+    python bench.py [--gpus N --steps K --warmup W]          # our arm
+    python bench.py --impl reference [...]                   # the reference's CPU path
+
+Value = 2 B x model elements / (max over ranks of device time per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dense-equivalent weight-sync GB/s (encode+route+apply) at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="qwen3-8b")
+    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--threshold", type=float, default=0.20)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=1,
+                    help="Qwen layers per CPU thread in the reference sample")
+    ap.add_argument("--verify", action="store_true", help="check serving == snapshot after run")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def layouts(n):
+    """FSDP-N trainer -> TP2 x N/2 serving replicas (TP1 at N=1)."""
+    tp = 1 if n == 1 else 2
+    return tp, n // tp
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# The reference's CPU path (oracle/_ref, the unmodified transfer engine)
+# ---------------------------------------------------------------------------
+
+def cpu_reference(args, threads=None, reps=1):
+    """Times TransferEngine::sync_step of the compiled reference on a bounded
+    sample of the same workload: one Qwen layer (no embedding) per thread, I32
+    weights of identical element counts (the reference has no bf16; I32 is the
+    dtype whose exact wrap rule the bf16 path mirrors), Async + shard-aware +
+    sparse, threshold 0.20, MemoryRelay, unthrottled.  The
+    layout is TP1 -> TP1: FSDP1 -> TP1 is the same tensor set, and the
+    reference cannot express FSDP -> TP2 (no cross-dim reslice)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import I32, Reference
+    import paper_2605_06534_b200.manifest as mf
+    ref = Reference()
+    nproc = os.cpu_count() or 1
+    layer_elems = sum(p.numel() for p in mf.MODELS[args.model](layer_subset=[1]))
+    # 3 copies (prev, next, serving) at 4 B/elem per thread, at most half the free RAM
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0]
+                    .split()[1]) * 1024
+    except Exception:
+        avail = 32 << 30
+    per = layer_elems * args.cpu_sample_layers * 4 * 3 * 1.3
+    t = threads or nproc
+    t = max(1, min(t, nproc, int(avail * 0.5 // per)))
+    states = []
+
+    def make(i):
+        layers = [1 + i * args.cpu_sample_layers + k for k in range(args.cpu_sample_layers)]
+        layers = [1 + (l - 1) % 34 for l in layers]
+        m = [p.as_tuple() for p in mf.MODELS[args.model](layer_subset=layers)]
+        return ref.state(m, I32, (1, 1, 1), (1, 1), args.density, args.seed + i)
+
+    with ThreadPoolExecutor(t) as ex:
+        states = list(ex.map(make, range(t)))
+    elems = sum(st.model_bytes() / 4 for st in states)
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(t) as ex:
+            reps_ = list(ex.map(lambda st: st.run(True, True, True, args.threshold, 64 << 20),
+                                states))
+        walls.append(time.perf_counter() - t0)
+    wall = statistics.median(walls)
+    gbs = elems * 2 / wall / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": t, "kind": "reference",
+            "sample": f"{t} thread(s) x {args.cpu_sample_layers} {args.model} layer(s) "
+                      f"({int(elems):,} elements, I32 weights, {args.density:.2%} density), "
+                      f"reference TransferEngine::sync_step TP1->TP1 Async+shard-aware+sparse; "
+                      f"dense-eq at 2 B/elem ({gbs * 2:.3f} GB/s at 4 B/elem)",
+            "wall_s": wall, "elems": int(elems),
+            "encode_s_sum": sum(r["encode_s"] for r in reps_),
+            "host_cpus": nproc}
+
+
+def run_reference_arm(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    reps = max(1, min(args.steps, 3))
+    cb = cpu_reference(args, reps=reps)
+    tp, rep_ = layouts(args.gpus)
+    line = {"metric": METRIC, "value": round(cb["value"], 4), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": reps, "warmup": 0,
+            "ms_per_step": round(cb["wall_s"] * 1e3 * (8.19e9 / max(cb["elems"], 1)), 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.model} 1% density weight sync, reference CPU path "
+                                   f"on a bounded layer sample (TP1->TP1)",
+                       "model": args.model, "density": args.density},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": round(cb["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_06534_b200 as ws
+    world, rank, local = dist_env()
+    n = world if world > 1 else args.gpus
+    if world == 1 and args.gpus != 1:
+        print(json.dumps({"error": "--gpus > 1 needs torchrun (one process per GPU)"}))
+        return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [ws.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    manifest = ws.MODELS[args.model]()
+    tp, replicas = layouts(n)
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, replicas),
+                   world=n, rank=rank)
+    eng = ws.TransferEngine(plan, device=local, unique_id=uid)
+    eng.generate(seed=args.seed, density=args.density)
+    torch.cuda.synchronize()
+    model_elems = plan.info.model_elems
+    dense_eq_bytes = 2 * model_elems
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---- warm-up (also sizes the record buffers) ----
+    rev = False
+    for _ in range(max(3, args.warmup)):
+        eng.sync_step(sparse=True, density_threshold=args.threshold, reverse=rev, report=False)
+        rev = not rev
+    torch.cuda.synchronize()
+    probe = eng.sync_step(sparse=True, density_threshold=args.threshold, reverse=rev, report=True)
+    rev = not rev
+    eng.timing(reset=True)
+
+    # ---- timed region: K syncs, no host synchronisation inside ----
+    barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            eng.sync_step(sparse=True, density_threshold=args.threshold, reverse=rev,
+                          report=False)
+            rev = not rev
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end) / args.steps
+    tim = eng.timing(reset=True)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = dense_eq_bytes / (ms_max * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (K1 encode) ----
+    enc_s = tim["encode_s"] / max(1, tim["steps"])
+    train_elems = plan.info.train_elems
+    nnz = probe["nnz"]
+    alg_bytes = 4 * train_elems + 6 * nnz  # read prev+next (2 B each), write idx u32 + val u16
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / enc_s / 1e9 if enc_s > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "encode_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("model") == args.model and tr.get("n_gpus") == n:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- end-to-end through the C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e, rev = run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev)
+
+    verified = None
+    if args.verify:
+        verified = verify_serving(eng, plan, rev)
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference(args)
+            cpu = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in cb.items()
+                   if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the reference build is test infrastructure; report why
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic",
+            "config": {"workload": f"{args.model} bf16 weight sync, {args.density:.2%} i.i.d. "
+                                   f"change density, trainer FSDP{n} -> serving TP{tp} x "
+                                   f"{replicas} replica(s)",
+                       "model": args.model, "density": args.density,
+                       "density_threshold": args.threshold, "train": f"fsdp{n}",
+                       "serve": f"tp{tp}x{replicas}", "model_elems": model_elems,
+                       "l2": "inputs larger than L2 (prev+next %.1f GB per GPU per step)"
+                             % (4 * train_elems / 1e9)},
+            "per_gpu_value": round(value / n, 2),
+            "stages_ms": {"encode": round(enc_s * 1e3, 4),
+                          "apply": round(tim["apply_s"] / max(1, tim["steps"]) * 1e3, 4),
+                          "route": round(tim["route_s"] / max(1, tim["steps"]) * 1e3, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None,
+                         "traffic": traffic, "kernel": "encode_kernel<bf16> (K1)",
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": int(tim["kernel_launches"]),
+            "clocks": clocks.summary(), "nnz_per_step": nnz,
+        }
+        if verified is not None:
+            line["verified"] = verified
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev):
+    """Same metric through the C-ABI's host-buffer entry point: every step
+    copies the new snapshot (this rank's trainer arena) from pinned host
+    memory and reads the per-shard change counts back."""
+    import torch
+    arena_bytes = eng.arena[0].numel() * eng.arena[0].element_size()
+    try:
+        host = [torch.empty(eng.arena[i].shape, dtype=eng.arena[i].dtype, pin_memory=True)
+                for i in range(2)]
+        pinned = True
+    except RuntimeError:
+        host = [torch.empty(eng.arena[i].shape, dtype=eng.arena[i].dtype) for i in range(2)]
+        pinned = False
+    for i in range(2):
+        host[i].copy_(eng.arena[i])
+    steps = max(1, args.e2e_steps)
+    # warm-up step in the current direction; reverse=True reads the new
+    # snapshot into arena 0, reverse=False into arena 1
+    eng.sync_step_host(host[0] if rev else host[1], density_threshold=args.threshold,
+                       reverse=rev, report=False)
+    rev = not rev
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        # reverse=True reads the new snapshot into arena 0 (the old "prev")
+        eng.sync_step_host(host[0] if rev else host[1], density_threshold=args.threshold,
+                           reverse=rev, report=False)
+        rev = not rev
+    torch.cuda.synchronize()
+    barrier()
+    wall = (time.perf_counter() - t0) / steps
+    t = torch.tensor([wall], device=eng.device, dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    wall = float(t.item())
+    del host
+    return {"value": round(dense_eq_bytes / wall / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": arena_bytes, "d2h_bytes_per_step": 8 * len(plan.segments),
+            "steps": steps, "ms_per_step": round(wall * 1e3, 2), "pinned": pinned,
+            "path": "ws_engine_sync_step_host (C-ABI), host timer around H2D+sync+D2H"}, rev
+
+
+def verify_serving(eng, plan, rev):
+    """After an even number of syncs the serving shards equal arena[rev]."""
+    import torch
+    torch.cuda.synchronize()
+    ok = True
+    if plan.world == 1:
+        for i in range(len(plan.segments)):
+            a = eng.segment_view(i, 1 if rev else 0)
+            ok &= bool(torch.equal(eng.serve_view(i).view(torch.int16), a.view(torch.int16)))
+    return ok
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

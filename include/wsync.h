@@ -1,0 +1,310 @@
+/*
+ * wsync.h -- C-ABI of the B200-native sparse weight-sync data plane
+ * (libwsync.so, sm_100a).
+ *
+ * This is the drop-in boundary for the hot path of the reference's
+ * cross-cluster weight-transfer engine (/root/reference/proj/include/
+ * coserve/transfer).  Every entry point names the reference interface it
+ * replaces; INTEGRATION.md shows the C++ shim that re-exposes the reference's
+ * own signatures (HostTensor / SparseDelta) on top of these calls.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "dev" pointers are CUDA device
+ *     pointers; "host" pointers are host memory.  No exception crosses the
+ *     ABI: every call returns a ws_status whose numbering maps 1:1 onto the
+ *     reference's TransferError hierarchy (tensor.hpp:16-24, codec.hpp:9-11,
+ *     shard.hpp:9-14, plan.hpp:7-9, relay.hpp:17-22, key.hpp:10-12).
+ *     ws_last_error() returns the message of the calling thread's last error.
+ *   - Kernel entry points are asynchronous on the given stream.  Errors found
+ *     on the device (an index outside the shard) are reported through a
+ *     device word `err_dev` (bit flags WS_ERRBIT_*); the caller reads it
+ *     after synchronising.  Unlike the reference (codec.cpp:73-79, which
+ *     applies a prefix of the records before throwing) a device-detected
+ *     error leaves the target untouched.
+ *   - dtype codes 0/1 are the reference's DType (tensor.hpp:26); code 2 is
+ *     the bf16 extension (16-bit words compared by bit pattern, u16
+ *     wrap-around delta and apply -- the reference's I32 rule on 16-bit
+ *     words, codec.cpp:52-61 / :80-91).
+ *   - Delta streams (the reference's SparseDelta, codec.hpp:16-32) are SoA:
+ *     ascending, unique u32 local flat indices + raw values of the dtype
+ *     width.  (pick_index_width, codec.cpp:140-143, picks 4 bytes for every
+ *     shard below 2^32 elements; shards beyond that are rejected with
+ *     WS_INVALID_ARGUMENT.)
+ *   - Threading: one stream per call; handles are not shared across threads
+ *     without external synchronisation (engine.hpp:70-92's TransferEngine is
+ *     likewise used by one caller at a time).
+ */
+#ifndef WSYNC_H
+#define WSYNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ws_stream_t; /* == cudaStream_t */
+
+typedef enum ws_status {
+  WS_OK = 0,
+  WS_SHAPE_MISMATCH = 1,       /* ShapeMismatch        tensor.hpp:19-21 */
+  WS_PAYLOAD_FORMAT = 2,       /* PayloadFormatError   tensor.hpp:22-24 */
+  WS_INDEX_OUT_OF_SHARD = 3,   /* IndexOutOfShard      codec.hpp:9-11   */
+  WS_INDIVISIBLE_SHAPE = 4,    /* IndivisibleShape     shard.hpp:9-11   */
+  WS_UNKNOWN_MODULE_KIND = 5,  /* UnknownModuleKind    shard.hpp:12-14  */
+  WS_INCOMPLETE_COVERAGE = 6,  /* IncompleteCoverage   plan.hpp:7-9     */
+  WS_RELAY_TIMEOUT = 7,        /* RelayTimeout         relay.hpp:17-19  */
+  WS_INTEGRITY = 8,            /* IntegrityError       relay.hpp:20-22  */
+  WS_KEY_FORMAT = 9,           /* KeyFormatError       key.hpp:10-12    */
+  WS_TRANSFER_ERROR = 10,      /* TransferError        tensor.hpp:16-18 */
+  WS_CUDA = 20,
+  WS_NCCL = 21,
+  WS_CAPACITY = 22,
+  WS_INVALID_ARGUMENT = 23
+} ws_status;
+
+typedef enum ws_dtype { WS_F32 = 0, WS_I32 = 1, WS_BF16 = 2 } ws_dtype;
+
+/* ModuleKind (manifest.hpp:13-19) + WS_EXPERT: a stacked expert tensor
+ * [E, ...] that is split along dim 0 (EP) by every layout. */
+typedef enum ws_module_kind {
+  WS_COLUMN_LINEAR = 0,
+  WS_ROW_LINEAR = 1,
+  WS_EMBEDDING = 2,
+  WS_NORM = 3,
+  WS_REPLICATED = 4,
+  WS_EXPERT = 5
+} ws_module_kind;
+
+/* Device-side error bits written to err_dev. */
+#define WS_ERRBIT_INDEX_OUT_OF_SHARD 0x1u
+#define WS_ERRBIT_CAPACITY 0x2u
+
+#define WS_MAX_DIMS 4
+
+const char* ws_status_name(ws_status s);
+const char* ws_last_error(void);
+int ws_abi_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Codec kernels on one shard (raw device pointers)                          */
+/* ------------------------------------------------------------------------ */
+
+/* Workspace bytes needed by ws_diff_shards / ws_reslice_delta for n
+ * elements (resp. nnz records). */
+size_t ws_diff_workspace_bytes(uint64_t n);
+
+/* K1, replaces diff_shards (codec.hpp:37, codec.cpp:34-63): every position
+ * whose value changed between prev and next, ascending.  Records beyond
+ * `cap` are counted but not written (nnz_dev still receives the full
+ * count), so cap = threshold * n implements the density fallback of
+ * engine.cpp:118-127 without a second pass. */
+ws_status ws_diff_shards(ws_dtype dtype, const void* prev_dev,
+                         const void* next_dev, uint64_t n, uint32_t* idx_dev,
+                         void* val_dev, uint64_t cap, uint64_t* nnz_dev,
+                         void* workspace_dev, size_t workspace_bytes,
+                         ws_stream_t stream);
+
+/* K4, replaces apply_delta (codec.hpp:41, codec.cpp:65-92): target[idx[k]]
+ * += val[k] (F32 IEEE add; I32/BF16 wrap-around add).  The record count is
+ * read from nnz_dev when non-null, else nnz.  All indices are validated
+ * before any write; an index >= n sets WS_ERRBIT_INDEX_OUT_OF_SHARD in
+ * err_dev and leaves target unchanged. */
+ws_status ws_apply_delta(ws_dtype dtype, void* target_dev, uint64_t n,
+                         const uint32_t* idx_dev, const void* val_dev,
+                         uint64_t nnz, const uint64_t* nnz_dev, uint32_t* err_dev,
+                         ws_stream_t stream);
+
+/* One rank's slice of one parameter (ShardDescriptor, shard.hpp:32-45):
+ * slice_dim < 0 means the full tensor. */
+typedef struct ws_shard {
+  int32_t slice_dim;
+  int64_t start;
+  int64_t end;
+} ws_shard;
+
+/* K3 (re-index part), replaces reslice_delta (codec.hpp:46-48,
+ * codec.cpp:94-138): re-expresses a delta local to `src` as a delta local to
+ * `dst`, dropping records outside dst, order preserving.  Extension: when
+ * src and dst are sliced along different dims the box intersection is used
+ * (the reference throws ShapeMismatch, codec.cpp:101-102); pass
+ * allow_cross_dim = 0 for the reference's behaviour.  An index outside the
+ * source shard sets WS_ERRBIT_INDEX_OUT_OF_SHARD and writes no output. */
+ws_status ws_reslice_delta(ws_dtype dtype, const int64_t* full_shape, int ndims,
+                           ws_shard src, ws_shard dst, int allow_cross_dim,
+                           const uint32_t* idx_dev, const void* val_dev,
+                           uint64_t nnz, const uint64_t* nnz_dev,
+                           uint32_t* out_idx_dev, void* out_val_dev,
+                           uint64_t* out_nnz_dev, uint32_t* err_dev,
+                           void* workspace_dev, size_t workspace_bytes,
+                           ws_stream_t stream);
+
+/* Dense fallback apply, replaces copy_overlap (shard.hpp:62-63,
+ * shard.cpp:136-170) generalised to two shards of one tensor (same-dim or
+ * cross-dim): copies src's overlap with dst into dst.  *copied receives the
+ * element count (host). */
+ws_status ws_copy_overlap(ws_dtype dtype, const int64_t* full_shape, int ndims,
+                          ws_shard dst, void* dst_dev, ws_shard src,
+                          const void* src_dev, int64_t* copied,
+                          ws_stream_t stream);
+
+/* Replaces extract_shard (shard.hpp:57, shard.cpp:111-134) on the device. */
+ws_status ws_extract_shard(ws_dtype dtype, const int64_t* full_shape, int ndims,
+                           ws_shard desc, const void* full_dev, void* out_dev,
+                           ws_stream_t stream);
+
+/* Synthetic bf16 weight pair for one shard;
+ * the device twin of random_weights/perturb_weights (manifest.cpp:47-89).
+ * change_thr = floor(density * 2^32) (<= 2^32). */
+ws_status ws_gen_pair_bf16(uint64_t seed, const char* param_name,
+                           const int64_t* full_shape, int ndims, ws_shard desc,
+                           uint64_t change_thr, uint16_t* prev_dev,
+                           uint16_t* next_dev, ws_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Planner (host, plan.hpp / shard.hpp)                                      */
+/* ------------------------------------------------------------------------ */
+
+typedef struct ws_param {
+  const char* name;
+  int32_t kind;  /* ws_module_kind */
+  int32_t ndims;
+  int64_t shape[WS_MAX_DIMS];
+  int32_t layer; /* owning pipeline layer (manifest.hpp:28) */
+} ws_param;
+
+typedef enum ws_train_scheme {
+  WS_TRAIN_TP = 0,  /* TrainConfig{tp,pp,dp} dealt by plan_pushes (plan.cpp:8-21) */
+  WS_TRAIN_FSDP = 1 /* every parameter split along dim 0 over all ranks */
+} ws_train_scheme;
+
+typedef struct ws_train_layout {
+  int32_t scheme;
+  int32_t tp, pp, dp;
+} ws_train_layout;
+
+/* ServeConfig{tp,pp} (plan.hpp:17-21) times `replicas` identical copies.
+ * Serving rank of (replica r, stage s, tp rank k) is r*tp*pp + s*tp + k.
+ * WS_EXPERT parameters are split along dim 0 over the tp ranks (EP = TP
+ * for experts, e.g. tp 8 gives EP8). */
+typedef struct ws_serve_layout {
+  int32_t tp, pp, replicas;
+} ws_serve_layout;
+
+typedef struct ws_plan ws_plan;
+
+/* Builds the static plan of rank `rank` of `world` GPUs: which trainer
+ * shards it encodes (plan_pushes), which serving shards it holds
+ * (ServeState::init, engine.cpp:34-49), and the route from every trainer
+ * shard to every serving shard that intersects it (plan_pulls,
+ * plan.cpp:89-121, extended with box intersection across dims).  Errors:
+ * WS_INDIVISIBLE_SHAPE, WS_UNKNOWN_MODULE_KIND, WS_INCOMPLETE_COVERAGE,
+ * WS_INVALID_ARGUMENT (world != layout sizes). */
+ws_status ws_plan_create(const ws_param* params, int nparams, ws_dtype dtype,
+                         const ws_train_layout* train,
+                         const ws_serve_layout* serve, int world, int rank,
+                         ws_plan** out);
+void ws_plan_destroy(ws_plan* plan);
+
+typedef struct ws_plan_info {
+  int32_t num_segments;       /* trainer shards encoded on this rank */
+  int32_t num_serve_shards;   /* serving shards resident on this rank */
+  int32_t num_routes;         /* (segment, serving coordinate) pairs */
+  int32_t serve_coord;        /* this rank's serving coordinate, -1 if none */
+  uint64_t train_arena_elems; /* prev/next arena sizes (elements) */
+  uint64_t serve_arena_elems;
+  uint64_t train_elems;       /* sum of segment sizes (dense-equivalent) */
+  uint64_t model_elems;       /* whole model */
+} ws_plan_info;
+ws_status ws_plan_get_info(const ws_plan* plan, ws_plan_info* info);
+
+/* Segment i of this rank: parameter index, shard descriptor, offset in the
+ * trainer arena, element count. */
+ws_status ws_plan_segment(const ws_plan* plan, int i, int32_t* param,
+                          ws_shard* desc, uint64_t* offset, uint64_t* n);
+/* Serving shard i of this rank. */
+ws_status ws_plan_serve_shard(const ws_plan* plan, int i, int32_t* param,
+                              ws_shard* desc, uint64_t* offset, uint64_t* n);
+/* Route i: source segment, destination serving coordinate, number of
+ * destination ranks (replicas of that coordinate) and the elements of the
+ * box intersection. */
+ws_status ws_plan_route(const ws_plan* plan, int i, int32_t* segment,
+                        int32_t* coord, int32_t* num_dst_ranks,
+                        uint64_t* overlap_elems);
+
+/* ------------------------------------------------------------------------ */
+/* Engine: one weight sync (TransferEngine::sync_step, engine.cpp:66-254)     */
+/* ------------------------------------------------------------------------ */
+
+typedef struct ws_engine ws_engine;
+
+typedef struct ws_sync_options { /* SyncOptions, engine.hpp:18-32 */
+  int32_t sparse;           /* sparse deltas with dense fallback (default 1) */
+  double density_threshold; /* inclusive, default 0.20 (engine.cpp:121) */
+  int32_t reverse;          /* 1: sync next -> prev (swap snapshot roles) */
+} ws_sync_options;
+
+typedef struct ws_report { /* TransferReport, engine.hpp:34-42 */
+  double wall_s;    /* device time from encode launch to last apply */
+  double encode_s;  /* K1 */
+  double route_s;   /* pack + exchange */
+  double apply_s;   /* K4 (sparse scatter + dense copies) */
+  uint64_t pushed_bytes;  /* record/dense bytes leaving this rank */
+  uint64_t pulled_bytes;  /* record/dense bytes arriving at this rank */
+  uint64_t nnz;           /* changed elements found on this rank */
+  int32_t dense_shards, sparse_shards;
+  uint32_t kernel_launches; /* kernels launched by this sync */
+} ws_report;
+
+/* unique_id: 128-byte NCCL unique id (ws_nccl_unique_id on rank 0, then
+ * broadcast by the caller), NULL when world == 1. */
+ws_status ws_nccl_unique_id(uint8_t out[128]);
+ws_status ws_engine_create(const ws_plan* plan, int device,
+                           const uint8_t* unique_id, ws_engine** out);
+void ws_engine_destroy(ws_engine* eng);
+
+/* Binds the caller-owned device arenas (sizes from ws_plan_info). */
+ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev,
+                         void* train_next_dev, void* serve_dev);
+
+/* Fills this rank's bound trainer arenas with the synthetic pair and its
+ * serving arena with the matching `prev` values (ServeState::init). */
+ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density,
+                             ws_stream_t stream);
+
+/* One sync on `stream`.  When report is non-null the call synchronises and
+ * fills it; otherwise it only enqueues (graph-capturable when world == 1). */
+ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts,
+                              ws_stream_t stream, ws_report* report);
+
+/* Same, with the new snapshot read from HOST memory (pinned for full
+ * speed): copies it into the trainer arena that becomes `next` for this
+ * step, syncs, and copies the per-segment change counts back to the host
+ * (nnz_host, num_segments entries, may be NULL). */
+ws_status ws_engine_sync_step_host(ws_engine* eng, const void* next_host,
+                                   const ws_sync_options* opts,
+                                   ws_stream_t stream, uint64_t* nnz_host,
+                                   ws_report* report);
+
+/* Device-time totals of the syncs since the last reset (the most recent 256
+ * at most), summed from CUDA events recorded on each sync's stream -- so a
+ * timed loop needs no per-step synchronisation.  Synchronises the engine's
+ * last stream.  reset != 0 clears the totals after reading. */
+typedef struct ws_timing {
+  uint32_t steps;
+  uint32_t kernel_launches; /* libwsync kernels launched by those syncs */
+  double wall_s, encode_s, route_s, apply_s;
+} ws_timing;
+ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out);
+
+/* Segment i's delta stream from the last sync: device pointers into the
+ * engine's record buffer, its record count (host, needs a synchronised
+ * stream) and the codec chosen ('S' sparse, 'D' dense). */
+ws_status ws_engine_segment_delta(ws_engine* eng, int i, const uint32_t** idx,
+                                  const void** val, uint64_t* nnz, char* codec);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSYNC_H */

@@ -1,0 +1,210 @@
+// common.cuh -- shared device helpers of libwsync (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "wsync.h"
+
+namespace wsync {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// ---- dtype traits ---------------------------------------------------------
+// BF16 and I32 compare bit patterns and use wrap-around arithmetic (the
+// reference's exact-dtype rule, codec.cpp:52-61 / :80-91); F32 compares by
+// value and uses IEEE round-to-nearest add/sub (codec.cpp:44-50 / :78).
+template <int DT>
+struct Traits;
+
+template <>
+struct Traits<WS_BF16> {
+  using T = uint16_t;
+  static constexpr int kVE = 8;  // elements per 16-byte vector
+  __device__ __forceinline__ static bool changed(T a, T b) { return a != b; }
+  __device__ __forceinline__ static T delta(T a, T b) { return (T)(b - a); }
+  __device__ __forceinline__ static T add(T t, T v) { return (T)(t + v); }
+  __device__ __forceinline__ static T get(const uint4& q, int e) {
+    const uint32_t w = e < 2 ? q.x : e < 4 ? q.y : e < 6 ? q.z : q.w;
+    return (T)((e & 1) ? (w >> 16) : (w & 0xffffu));
+  }
+};
+
+template <>
+struct Traits<WS_I32> {
+  using T = uint32_t;
+  static constexpr int kVE = 4;
+  __device__ __forceinline__ static bool changed(T a, T b) { return a != b; }
+  __device__ __forceinline__ static T delta(T a, T b) { return b - a; }
+  __device__ __forceinline__ static T add(T t, T v) { return t + v; }
+  __device__ __forceinline__ static T get(const uint4& q, int e) {
+    return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
+  }
+};
+
+template <>
+struct Traits<WS_F32> {
+  using T = uint32_t;  // carried as raw bits
+  static constexpr int kVE = 4;
+  __device__ __forceinline__ static bool changed(T a, T b) {
+    return !(__uint_as_float(a) == __uint_as_float(b));
+  }
+  __device__ __forceinline__ static T delta(T a, T b) {
+    return __float_as_uint(__fsub_rn(__uint_as_float(b), __uint_as_float(a)));
+  }
+  __device__ __forceinline__ static T add(T t, T v) {
+    return __float_as_uint(__fadd_rn(__uint_as_float(t), __uint_as_float(v)));
+  }
+  __device__ __forceinline__ static T get(const uint4& q, int e) {
+    return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
+  }
+};
+
+// Change mask of the VE elements of one 16-byte vector pair.
+template <int DT>
+__device__ __forceinline__ uint32_t change_mask(const uint4& a, const uint4& b) {
+  if constexpr (DT == WS_BF16) {
+    const uint32_t x0 = a.x ^ b.x, x1 = a.y ^ b.y, x2 = a.z ^ b.z, x3 = a.w ^ b.w;
+    return ((x0 & 0xffffu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) |
+           ((x1 & 0xffffu) ? 4u : 0u) | ((x1 >> 16) ? 8u : 0u) |
+           ((x2 & 0xffffu) ? 16u : 0u) | ((x2 >> 16) ? 32u : 0u) |
+           ((x3 & 0xffffu) ? 64u : 0u) | ((x3 >> 16) ? 128u : 0u);
+  } else {
+    using Tr = Traits<DT>;
+    return (Tr::changed(a.x, b.x) ? 1u : 0u) | (Tr::changed(a.y, b.y) ? 2u : 0u) |
+           (Tr::changed(a.z, b.z) ? 4u : 0u) | (Tr::changed(a.w, b.w) ? 8u : 0u);
+  }
+}
+
+// ---- memory helpers -------------------------------------------------------
+// Streaming 128-bit load: read-once data, do not pollute L1.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- decoupled look-back status words ---------------------------------------
+// status = epoch(30b) << 34 | flag(2b) << 32 | value(32b).  A word whose epoch
+// differs from the launch's epoch is "not yet written"; the epoch advances
+// per launch so the status array never needs clearing.
+constexpr uint32_t kFlagAggregate = 1, kFlagPrefix = 2;
+
+__device__ __forceinline__ unsigned long long make_status(uint32_t epoch, uint32_t flag,
+                                                          uint32_t value) {
+  return ((unsigned long long)(epoch & 0x3fffffffu) << 34) |
+         ((unsigned long long)flag << 32) | value;
+}
+
+// Exclusive prefix of `tile` within its chain [first_tile, tile): executed by
+// one full warp.  Every tile of the chain publishes its aggregate before
+// looking back, and the chain head publishes an inclusive prefix, so the walk
+// terminates.
+__device__ __forceinline__ uint32_t warp_lookback(const unsigned long long* status,
+                                                  int64_t tile, int64_t first_tile,
+                                                  uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long want = (unsigned long long)(epoch & 0x3fffffffu);
+  uint32_t excl = 0;
+  int64_t pos = tile - 1;
+  while (true) {
+    const int64_t my = pos - lane;
+    uint32_t flag = 0, val = 0;
+    if (my >= first_tile) {
+      unsigned long long st;
+      do {
+        st = ld_relaxed_u64(status + my);
+      } while ((st >> 34) != want);
+      flag = (uint32_t)(st >> 32) & 3u;
+      val = (uint32_t)st;
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, flag == kFlagPrefix);
+    const int stop = pmask ? __ffs(pmask) - 1 : 31;
+    uint32_t c = lane <= stop ? val : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFullMask, c, o);
+    excl += c;
+    if (pmask) break;
+    pos -= 32;
+  }
+  return excl;
+}
+
+// ---- geometry: shard boxes -------------------------------------------------
+struct Box {
+  int32_t nd;
+  uint32_t lo[WS_MAX_DIMS];
+  uint32_t ext[WS_MAX_DIMS];
+};
+
+// Source-local flat index -> destination-local flat index, or ~0ull when the
+// element lies outside the destination box (codec.cpp:125-131 generalised).
+struct Remap {
+  int32_t nd;
+  uint32_t src_ext[WS_MAX_DIMS];
+  int64_t shift[WS_MAX_DIMS];   // src.lo - dst.lo
+  uint32_t dst_ext[WS_MAX_DIMS];
+};
+
+__device__ __forceinline__ unsigned long long remap_index(const Remap& m, uint32_t i) {
+  uint32_t c[WS_MAX_DIMS];
+  uint32_t rem = i;
+#pragma unroll
+  for (int d = WS_MAX_DIMS - 1; d >= 0; --d) {
+    if (d < m.nd) {
+      c[d] = rem % m.src_ext[d];
+      rem /= m.src_ext[d];
+    }
+  }
+  unsigned long long di = 0;
+#pragma unroll
+  for (int d = 0; d < WS_MAX_DIMS; ++d) {
+    if (d < m.nd) {
+      const int64_t g = (int64_t)c[d] + m.shift[d];
+      if (g < 0 || g >= (int64_t)m.dst_ext[d]) return ~0ull;
+      di = di * m.dst_ext[d] + (unsigned long long)g;
+    }
+  }
+  return di;
+}
+
+// ---- synthetic generator (oracle/wsync_oracle.c gen_elem) ------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ void gen_elem_bf16(uint64_t key, uint64_t g, uint64_t change_thr,
+                                              uint16_t& p, uint16_t& n) {
+  const uint64_t r0 = splitmix64(key + (2 * g) * 0x9e3779b97f4a7c15ull);
+  const uint64_t r1 = splitmix64(key + (2 * g + 1) * 0x9e3779b97f4a7c15ull);
+  const int32_t s = (int32_t)(r0 & 0xffff) + (int32_t)((r0 >> 16) & 0xffff) +
+                    (int32_t)((r0 >> 32) & 0xffff) + (int32_t)(r0 >> 48) - 131070;
+  const float v = __fmul_rn((float)s, 5.2858e-7f);
+  uint32_t u = __float_as_uint(v);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  const uint16_t pb = (uint16_t)(u >> 16);
+  uint16_t nb = pb;
+  if ((r1 >> 32) < change_thr) {
+    const uint16_t m = (uint16_t)(1 + (r1 & 0xf));
+    nb = ((r1 >> 4) & 1) ? (uint16_t)(pb - m) : (uint16_t)(pb + m);
+  }
+  p = pb;
+  n = nb;
+}
+
+}  // namespace wsync

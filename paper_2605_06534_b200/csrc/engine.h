@@ -1,0 +1,80 @@
+// engine.h -- the per-GPU weight-sync engine behind ws_engine_*.
+#pragma once
+
+#include <functional>
+#include <vector>
+
+#include "plan.h"
+#include "route.h"
+
+struct ws_engine {
+  ws_engine(const wsync::Plan& plan, int device);
+  ~ws_engine();
+
+  ws_status init(const uint8_t* unique_id);
+  ws_status generate(uint64_t seed, double density, cudaStream_t s);
+  ws_status sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
+                      uint64_t* nnz_host, ws_report* report);
+  ws_status segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
+                          char* codec);
+  ws_status timing(int reset, ws_timing* out);
+
+  // caller-owned arenas (ws_engine_bind)
+  void* arena[2] = {nullptr, nullptr};
+  void* serve = nullptr;
+
+ private:
+  ws_status ensure_records(double threshold, int sparse);
+  ws_status init_comm(const uint8_t* unique_id);  // exchange.cu
+  void destroy_comm();
+  ws_status exchange(const ws_sync_options& o, int next_arena, cudaStream_t s, uint32_t* launches);
+  uint32_t next_epoch();
+
+  wsync::Plan plan_;
+  int device_;
+  int dtype_;
+  int nseg_;
+  uint32_t ntiles_ = 0;
+  uint32_t epoch_ = 0;
+  int route_grid_ = 0;
+
+  // encode tables (device)
+  wsync::SegDev* d_segs_ = nullptr;
+  uint32_t* d_tile0_ = nullptr;
+  unsigned long long* d_status_ = nullptr;
+  unsigned int* d_ticket_ = nullptr;
+  uint64_t* d_nnz_ = nullptr;
+  uint64_t* d_cap_ = nullptr;
+  uint64_t* d_rec_ = nullptr;
+  uint64_t* d_base_ = nullptr;
+  std::vector<wsync::SegDev> segs_;
+  double cur_threshold_ = -1.0;
+  int cur_sparse_ = -1;
+
+  // record buffers
+  uint32_t* d_idx_ = nullptr;
+  void* d_val_ = nullptr;
+  uint64_t rec_alloc_ = 0;
+
+  // local routes
+  wsync::LocalEntry* d_local_ = nullptr;
+  int nlocal_ = 0;
+  uint64_t* d_unit_off_ = nullptr;
+
+  // per-step stage events: [start, after H2D, after encode, after local
+  // apply, after exchange, end]; a ring so timed loops need no sync.
+  static constexpr int kRing = 256;
+  cudaEvent_t (*ring_)[6] = nullptr;
+  uint32_t ring_steps_ = 0;    // steps recorded since reset
+  uint32_t ring_head_ = 0;     // next slot
+  uint32_t launch_total_ = 0;
+  cudaStream_t last_stream_ = nullptr;
+  bool last_sparse_ = true;
+  std::vector<uint64_t> h_nnz_;
+  uint64_t* h_nnz_pinned_ = nullptr;
+
+  // multi-GPU state (exchange.cu)
+  struct Comm;
+  Comm* comm_ = nullptr;
+  uint64_t pulled_bytes_ = 0;
+};

@@ -1,0 +1,318 @@
+// engine_impl.cu -- ws_engine: device tables, K1 launch, local route/apply.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "capi_util.h"
+#include "engine.h"
+
+using namespace wsync;
+
+#define WS_CUDA_TRY(expr, what)                        \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_status(_e, what); \
+  } while (0)
+
+ws_engine::ws_engine(const Plan& plan, int device)
+    : plan_(plan), device_(device), dtype_(plan.dtype()),
+      nseg_((int)plan.segments().size()) {}
+
+ws_engine::~ws_engine() {
+  cudaSetDevice(device_);
+  cudaFree(d_segs_);
+  cudaFree(d_tile0_);
+  cudaFree(d_status_);
+  cudaFree(d_ticket_);
+  cudaFree(d_nnz_);
+  cudaFree(d_cap_);
+  cudaFree(d_rec_);
+  cudaFree(d_base_);
+  cudaFree(d_idx_);
+  cudaFree(d_val_);
+  cudaFree(d_local_);
+  cudaFree(d_unit_off_);
+  if (h_nnz_pinned_) cudaFreeHost(h_nnz_pinned_);
+  if (ring_) {
+    for (int i = 0; i < kRing; ++i)
+      for (auto& e : ring_[i])
+        if (e) cudaEventDestroy(e);
+    delete[] ring_;
+  }
+  destroy_comm();
+}
+
+uint32_t ws_engine::next_epoch() {
+  epoch_ = (epoch_ + 1) & 0x3fffffffu;
+  if (epoch_ == 0) epoch_ = 1;
+  return epoch_;
+}
+
+ws_status ws_engine::init(const uint8_t* unique_id) {
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  const auto& segs = plan_.segments();
+  // Encode tiles: one look-back chain per segment.
+  std::vector<uint32_t> tile0(nseg_ + 1, 0);
+  const uint32_t tile = encode_tile_elems(dtype_);
+  uint64_t t = 0;
+  for (int i = 0; i < nseg_; ++i) {
+    tile0[i] = (uint32_t)t;
+    t += (segs[i].n + tile - 1) / tile;
+  }
+  tile0[nseg_] = (uint32_t)t;
+  if (t >= (1ull << 31)) return set_error(WS_CAPACITY, "too many encode tiles");
+  ntiles_ = (uint32_t)t;
+  segs_.resize(nseg_);
+  std::vector<uint64_t> base(nseg_);
+  for (int i = 0; i < nseg_; ++i) {
+    segs_[i] = SegDev{segs[i].offset, segs[i].n, 0, 0};
+    base[i] = segs[i].offset;
+  }
+  const size_t ns = std::max(1, nseg_);
+  WS_CUDA_TRY(cudaMalloc(&d_segs_, ns * sizeof(SegDev)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_tile0_, (ns + 1) * sizeof(uint32_t)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_status_, std::max<size_t>(1, ntiles_) * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemset(d_status_, 0, std::max<size_t>(1, ntiles_) * 8), "cudaMemset");
+  WS_CUDA_TRY(cudaMalloc(&d_ticket_, 256), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_nnz_, ns * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemset(d_nnz_, 0, ns * 8), "cudaMemset");
+  WS_CUDA_TRY(cudaMalloc(&d_cap_, ns * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_rec_, ns * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_base_, ns * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(d_tile0_, tile0.data(), (nseg_ + 1) * 4, cudaMemcpyHostToDevice), "H2D");
+  if (nseg_)
+    WS_CUDA_TRY(cudaMemcpy(d_base_, base.data(), nseg_ * 8, cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMallocHost(&h_nnz_pinned_, ns * 8), "cudaMallocHost");
+  h_nnz_.assign(nseg_, 0);
+
+  // Local routes: destinations on this GPU's serving coordinate.
+  std::vector<LocalEntry> local;
+  const int me = plan_.my_coord();
+  for (const Route& r : plan_.routes()) {
+    if (r.coord != me) continue;
+    const ParamMeta& p = plan_.manifest()[r.dst.param];
+    local.push_back(make_local_entry(dtype_, p.shape.data(), (int)p.shape.size(), r.seg,
+                                     segs[r.seg].shard.d, r.dst.d, r.dst_offset));
+  }
+  nlocal_ = (int)local.size();
+  WS_CUDA_TRY(cudaMalloc(&d_local_, std::max<size_t>(1, local.size()) * sizeof(LocalEntry)),
+              "cudaMalloc");
+  if (nlocal_)
+    WS_CUDA_TRY(cudaMemcpy(d_local_, local.data(), local.size() * sizeof(LocalEntry),
+                           cudaMemcpyHostToDevice),
+                "H2D");
+  WS_CUDA_TRY(cudaMalloc(&d_unit_off_, (local.size() + 1) * 8), "cudaMalloc");
+  route_grid_ = sm_count() * 8;
+  ring_ = new cudaEvent_t[kRing][6]();
+  for (int i = 0; i < kRing; ++i)
+    for (auto& e : ring_[i]) WS_CUDA_TRY(cudaEventCreate(&e), "cudaEventCreate");
+  return init_comm(unique_id);
+}
+
+ws_status ws_engine::ensure_records(double threshold, int sparse) {
+  if (threshold == cur_threshold_ && sparse == cur_sparse_) return WS_OK;
+  if (!(threshold >= 0.0)) return set_error(WS_INVALID_ARGUMENT, "density_threshold must be >= 0");
+  // The largest record count k with k/n <= threshold (engine.cpp:121) is
+  // the capacity of a segment: one more change makes it dense.
+  uint64_t total = 0;
+  std::vector<uint64_t> cap(nseg_), rec(nseg_);
+  for (int i = 0; i < nseg_; ++i) {
+    const uint64_t n = segs_[i].n;
+    uint64_t c = 0;
+    if (sparse && n) {
+      c = (uint64_t)std::floor(threshold * (double)n);
+      if (c > n) c = n;
+      while (c < n && (double)(c + 1) / (double)n <= threshold) ++c;
+      while (c > 0 && (double)c / (double)n > threshold) --c;
+    }
+    cap[i] = c;
+    rec[i] = total;
+    total += (c + 63) / 64 * 64;
+    segs_[i].cap = c;
+    segs_[i].rec = rec[i];
+  }
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync before record realloc");
+  if (total > rec_alloc_) {
+    cudaFree(d_idx_);
+    cudaFree(d_val_);
+    d_idx_ = nullptr;
+    d_val_ = nullptr;
+    WS_CUDA_TRY(cudaMalloc(&d_idx_, total * 4), "cudaMalloc records");
+    WS_CUDA_TRY(cudaMalloc(&d_val_, total * dtype_size(dtype_)), "cudaMalloc records");
+    rec_alloc_ = total;
+  }
+  if (nseg_) {
+    WS_CUDA_TRY(cudaMemcpy(d_segs_, segs_.data(), nseg_ * sizeof(SegDev), cudaMemcpyHostToDevice),
+                "H2D");
+    WS_CUDA_TRY(cudaMemcpy(d_cap_, cap.data(), nseg_ * 8, cudaMemcpyHostToDevice), "H2D");
+    WS_CUDA_TRY(cudaMemcpy(d_rec_, rec.data(), nseg_ * 8, cudaMemcpyHostToDevice), "H2D");
+  }
+  cur_threshold_ = threshold;
+  cur_sparse_ = sparse;
+  return WS_OK;
+}
+
+ws_status ws_engine::generate(uint64_t seed, double density, cudaStream_t s) {
+  if (dtype_ != WS_BF16) return set_error(WS_INVALID_ARGUMENT, "generate: bf16 engines only");
+  if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "generate: unbound");
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  const double d = std::min(std::max(density, 0.0), 1.0);
+  const uint64_t thr = (uint64_t)(d * 4294967296.0);
+  for (const Segment& sg : plan_.segments()) {
+    const ParamMeta& p = plan_.manifest()[sg.shard.param];
+    WS_CUDA_TRY(launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
+                                (int)p.shape.size(), sg.shard.d, thr,
+                                (uint16_t*)arena[0] + sg.offset, (uint16_t*)arena[1] + sg.offset, s),
+                "generate");
+  }
+  for (const ServeShard& ss : plan_.serve_shards()) {
+    const ParamMeta& p = plan_.manifest()[ss.shard.param];
+    WS_CUDA_TRY(launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
+                                (int)p.shape.size(), ss.shard.d, thr,
+                                (uint16_t*)serve + ss.offset, nullptr, s),
+                "generate");
+  }
+  return WS_OK;
+}
+
+ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
+                               uint64_t* nnz_host, ws_report* report) {
+  if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "sync: unbound");
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  ws_status st = ensure_records(o.density_threshold, o.sparse ? 1 : 0);
+  if (st != WS_OK) return st;
+  const int pa = o.reverse ? 1 : 0, na = 1 - pa;
+  const int esz = dtype_size(dtype_);
+  uint32_t launches = 0;
+  cudaEvent_t* ev_ = ring_[ring_head_];
+  ring_head_ = (ring_head_ + 1) % kRing;
+  ring_steps_ = std::min<uint32_t>(ring_steps_ + 1, kRing);
+  last_stream_ = s;
+
+  WS_CUDA_TRY(cudaEventRecord(ev_[0], s), "event");
+  if (next_host) {
+    WS_CUDA_TRY(cudaMemcpyAsync(arena[na], next_host, plan_.train_arena_elems() * esz,
+                                cudaMemcpyHostToDevice, s),
+                "H2D next snapshot");
+  }
+  WS_CUDA_TRY(cudaEventRecord(ev_[1], s), "event");
+  last_sparse_ = o.sparse != 0;
+  if (o.sparse && ntiles_) {
+    EncodeArgs a{};
+    a.prev = arena[pa];
+    a.next = arena[na];
+    a.segs = d_segs_;
+    a.tile0 = d_tile0_;
+    a.nseg = nseg_;
+    a.ntiles = ntiles_;
+    a.out_idx = d_idx_;
+    a.out_val = d_val_;
+    a.seg_nnz = d_nnz_;
+    a.status = d_status_;
+    a.epoch = next_epoch();
+    a.ticket = d_ticket_;
+    WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
+    ++launches;
+  }
+  WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
+  RouteSideArgs r{};
+  r.entries = d_local_;
+  r.nentries = nlocal_;
+  r.sparse = o.sparse ? 1 : 0;
+  r.seg_nnz = d_nnz_;
+  r.seg_cap = d_cap_;
+  r.seg_rec = d_rec_;
+  r.seg_base = d_base_;
+  r.rec_idx = d_idx_;
+  r.rec_val = d_val_;
+  r.train_next = arena[na];
+  r.serve = serve;
+  r.unit_off = d_unit_off_;
+  WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
+  if (nlocal_) launches += 2;
+  WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
+  if (plan_.world() > 1) {
+    st = exchange(o, na, s, &launches);
+    if (st != WS_OK) return st;
+  }
+  WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
+  if ((nnz_host || report) && nseg_)
+    WS_CUDA_TRY(cudaMemcpyAsync(h_nnz_pinned_, d_nnz_, nseg_ * 8, cudaMemcpyDeviceToHost, s),
+                "D2H counts");
+  WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
+  launch_total_ += launches;
+  if (!nnz_host && !report) return WS_OK;
+  WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  std::memcpy(h_nnz_.data(), h_nnz_pinned_, nseg_ * 8);
+  if (nnz_host) std::memcpy(nnz_host, h_nnz_.data(), nseg_ * 8);
+  if (report) {
+    std::memset(report, 0, sizeof(*report));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_[0], ev_[5]);
+    report->wall_s = ms * 1e-3;
+    cudaEventElapsedTime(&ms, ev_[1], ev_[2]);
+    report->encode_s = ms * 1e-3;
+    cudaEventElapsedTime(&ms, ev_[2], ev_[3]);
+    report->apply_s = ms * 1e-3;
+    cudaEventElapsedTime(&ms, ev_[3], ev_[4]);
+    report->route_s = ms * 1e-3;
+    // Wire accounting of the reference payloads (transfer_cases.hpp:187-194),
+    // with the dtype's value width.
+    for (int i = 0; i < nseg_; ++i) {
+      const auto& sg = plan_.segments()[i];
+      const uint64_t nd = plan_.manifest()[sg.shard.param].shape.size();
+      const bool sparse = o.sparse && (!ntiles_ || h_nnz_[i] <= segs_[i].cap);
+      if (sparse) {
+        report->sparse_shards++;
+        report->pushed_bytes += 8 + 8 * nd + 8 + h_nnz_[i] * (4 + esz);
+      } else {
+        report->dense_shards++;
+        report->pushed_bytes += 8 + 8 * nd + sg.n * esz;
+      }
+      report->nnz += o.sparse ? h_nnz_[i] : 0;
+    }
+    report->pulled_bytes = pulled_bytes_;
+    report->kernel_launches = launches;
+  }
+  return WS_OK;
+}
+
+ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
+                                   char* codec) {
+  if (i < 0 || i >= nseg_) return set_error(WS_INVALID_ARGUMENT, "segment index out of range");
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  uint64_t n = 0;
+  WS_CUDA_TRY(cudaMemcpy(&n, d_nnz_ + i, 8, cudaMemcpyDeviceToHost), "D2H nnz");
+  if (idx) *idx = d_idx_ ? d_idx_ + segs_[i].rec : nullptr;
+  if (val) *val = d_val_ ? (const char*)d_val_ + segs_[i].rec * dtype_size(dtype_) : nullptr;
+  if (nnz) *nnz = n;
+  if (codec) *codec = (last_sparse_ && n <= segs_[i].cap) ? 'S' : 'D';
+  return WS_OK;
+}
+
+ws_status ws_engine::timing(int reset, ws_timing* out) {
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  if (last_stream_) WS_CUDA_TRY(cudaStreamSynchronize(last_stream_), "sync");
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  ws_timing t{};
+  t.steps = ring_steps_;
+  t.kernel_launches = launch_total_;
+  for (uint32_t k = 0; k < ring_steps_; ++k) {
+    const cudaEvent_t* e = ring_[(ring_head_ + kRing - 1 - k) % kRing];
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e[0], e[5]);
+    t.wall_s += ms * 1e-3;
+    cudaEventElapsedTime(&ms, e[1], e[2]);
+    t.encode_s += ms * 1e-3;
+    cudaEventElapsedTime(&ms, e[2], e[3]);
+    t.apply_s += ms * 1e-3;
+    cudaEventElapsedTime(&ms, e[3], e[4]);
+    t.route_s += ms * 1e-3;
+  }
+  if (out) *out = t;
+  if (reset) {
+    ring_steps_ = 0;
+    launch_total_ = 0;
+  }
+  return WS_OK;
+}

@@ -1,0 +1,105 @@
+// kernels.h -- host-side launch interface of the libwsync device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace wsync {
+
+constexpr int kEncodeThreads = 256;
+constexpr int kEncodeVPT = 4;  // 16-byte vectors per thread per array per tile
+
+// Elements per encode tile: 8192 for bf16, 4096 for 4-byte dtypes (16 KB of
+// prev plus 16 KB of next per tile).
+inline uint32_t encode_tile_elems(int dtype) {
+  return kEncodeThreads * kEncodeVPT * (dtype == WS_BF16 ? 8 : 4);
+}
+inline uint32_t elems_per_vec(int dtype) { return dtype == WS_BF16 ? 8 : 4; }
+inline int dtype_size(int dtype) { return dtype == WS_BF16 ? 2 : 4; }
+
+// One encode segment: a trainer shard at `base` (elements, multiple of the
+// vector width) in the prev/next arenas, its records written at
+// [rec, rec + min(nnz, cap)) of the record arrays.
+struct SegDev {
+  uint64_t base, n, rec, cap;
+};
+
+struct EncodeArgs {
+  const void* prev;
+  const void* next;
+  const SegDev* segs;     // null: the single segment seg0
+  SegDev seg0;
+  const uint32_t* tile0;  // nseg + 1 prefix of per-segment tile counts (null with seg0)
+  int32_t nseg;
+  uint32_t ntiles;
+  uint32_t* out_idx;
+  void* out_val;
+  uint64_t* seg_nnz;
+  unsigned long long* status;  // >= ntiles words
+  uint32_t epoch;
+  unsigned int* ticket;        // zeroed before launch
+};
+
+// K1: fused compare + ballot/popc + block scan + decoupled look-back
+// compaction over all segments.  Returns the persistent grid used.
+cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out = nullptr);
+
+// Record validation + in-place apply (ws_apply_delta).
+cudaError_t launch_apply(int dtype, void* target, uint64_t n, const uint32_t* idx,
+                         const void* val, uint64_t nnz, const uint64_t* nnz_dev,
+                         uint32_t* err, cudaStream_t s);
+
+// Order-preserving filter + re-index of one record stream (ws_reslice_delta).
+struct ResliceArgs {
+  Remap map;
+  uint64_t src_elems;
+  const uint32_t* idx;
+  const void* val;
+  uint64_t cap_in;            // upper bound on the record count
+  const uint64_t* nnz_dev;    // actual count (device) or null
+  uint64_t nnz;               // actual count when nnz_dev is null
+  uint32_t* out_idx;
+  void* out_val;
+  uint64_t* out_nnz;
+  uint32_t* err;
+  unsigned long long* status;
+  uint32_t epoch;
+  unsigned int* ticket;
+};
+constexpr uint32_t kResliceTile = 256 * 4;
+cudaError_t launch_reslice(int dtype, const ResliceArgs& a, cudaStream_t s);
+
+// Dense box copy: the overlap of two shards of one tensor (copy_overlap).
+struct BoxCopyArgs {
+  void* dst;
+  const void* src;
+  uint64_t rows;          // rows of the overlap (product of outer dims)
+  uint64_t run;           // contiguous elements per row
+  int32_t nd_outer;       // dims enumerated by `rows`
+  uint32_t outer_ext[WS_MAX_DIMS];
+  uint64_t src_stride[WS_MAX_DIMS], dst_stride[WS_MAX_DIMS];  // elements
+  uint64_t src_base, dst_base;                                // elements
+  int vec;                // 1: 16-byte vectors are legal for every row
+};
+cudaError_t launch_box_copy(int dtype, const BoxCopyArgs& a, cudaStream_t s);
+
+// Builds BoxCopyArgs for copying the overlap of `src` into `dst` (both
+// shards of full_shape).  Returns the overlap element count (0: none).
+uint64_t make_box_copy(int dtype, const int64_t* full, int nd, const ws_shard& dst,
+                       const ws_shard& src, BoxCopyArgs* out);
+
+// Synthetic bf16 pair for one shard; also used to initialise serving shards
+// (prev only when next == nullptr).
+cudaError_t launch_gen_bf16(uint64_t key, const int64_t* full, int nd, const ws_shard& desc,
+                            uint64_t change_thr, uint16_t* prev, uint16_t* next,
+                            cudaStream_t s);
+
+// Host helpers.
+uint64_t param_key(uint64_t seed, const char* name);
+Box shard_box(const int64_t* full, int nd, const ws_shard& d);
+Remap make_remap(const int64_t* full, int nd, const ws_shard& src, const ws_shard& dst);
+int sm_count();
+
+}  // namespace wsync

@@ -1,0 +1,162 @@
+// kernels_route.cu -- K3/K4 on the serving side of the engine.
+//
+// After K1 every trainer segment's delta stream (or, above the density
+// threshold, its dense `next` snapshot) must land in each serving shard it
+// intersects.  For destinations on the same GPU this is done here without
+// materialising resliced streams: a tiny single-block kernel turns the
+// per-segment record counts into a work list (records in chunks for sparse
+// segments, row runs for dense ones), and one persistent kernel walks it,
+// re-indexing each record into the destination shard (codec.cpp:125-131,
+// box-generalised) and applying it in place (codec.cpp:80-91), or copying
+// the dense overlap (shard.cpp:161-168).
+#include <algorithm>
+
+#include "route.h"
+
+namespace wsync {
+
+namespace {
+
+constexpr int kWlThreads = 1024;
+
+__device__ __forceinline__ bool seg_dense(const RouteSideArgs& a, int seg) {
+  return !a.sparse || a.seg_nnz[seg] > a.seg_cap[seg];
+}
+
+// Units of one entry: record chunks (sparse) or row-run chunks (dense).
+__device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const LocalEntry& e) {
+  if (seg_dense(a, e.seg)) {
+    const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
+    return e.box.rows * per_row;
+  }
+  const uint64_t nnz = a.seg_nnz[e.seg];
+  return (nnz + kApplyChunk - 1) / kApplyChunk;
+}
+
+__global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
+  __shared__ uint64_t s_carry;
+  __shared__ uint64_t s_warp[kWlThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < a.nentries; base += kWlThreads) {
+    const int e = base + tid;
+    const uint64_t u = e < a.nentries ? entry_units(a, a.entries[e]) : 0;
+    uint64_t inc = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = s_warp[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFullMask, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint64_t excl = s_carry + s_warp[warp] + inc - u;
+    if (e < a.nentries) a.unit_off[e] = excl;
+    __syncthreads();
+    if (tid == kWlThreads - 1) s_carry = excl + u;
+    __syncthreads();
+  }
+  if (tid == 0) a.unit_off[a.nentries] = s_carry;
+}
+
+__device__ __forceinline__ int find_entry(const uint64_t* off, int n, uint64_t u) {
+  int lo = 0, hi = n;  // off[lo] <= u < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  __shared__ int s_entry;
+  __shared__ uint64_t s_u0;
+  const uint64_t total = a.unit_off[a.nentries];
+  T* serve = reinterpret_cast<T*>(a.serve);
+  const T* val = reinterpret_cast<const T*>(a.rec_val);
+  const T* next = reinterpret_cast<const T*>(a.train_next);
+  for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const int e = find_entry(a.unit_off, a.nentries, u);
+      s_entry = e;
+      s_u0 = a.unit_off[e];
+    }
+    __syncthreads();
+    const LocalEntry& E = a.entries[s_entry];
+    const uint64_t lu = u - s_u0;
+    __syncthreads();
+    if (!seg_dense(a, E.seg)) {
+      const uint64_t nnz = a.seg_nnz[E.seg];
+      const uint64_t k0 = lu * kApplyChunk;
+      const uint64_t k1 = min(nnz, k0 + kApplyChunk);
+      const uint64_t rec = a.seg_rec[E.seg];
+      T* dst = serve + E.dst_base;
+      if (E.identity) {
+        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+          const uint32_t i = __ldg(a.rec_idx + rec + k);
+          if (i < E.keep_lo || i >= E.keep_hi) continue;
+          const uint64_t d = (uint64_t)((int64_t)i + E.shift);
+          dst[d] = Tr::add(dst[d], __ldg(val + rec + k));
+        }
+      } else {
+        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+          const uint64_t d = remap_index(E.map, __ldg(a.rec_idx + rec + k));
+          if (d == ~0ull) continue;
+          dst[d] = Tr::add(dst[d], __ldg(val + rec + k));
+        }
+      }
+    } else {
+      // dense fallback: copy one chunk of one row of the overlap
+      const BoxCopyArgs& B = E.box;
+      const uint64_t per_row = (B.run + kCopyChunk - 1) / kCopyChunk;
+      const uint64_t row = lu / per_row, c0 = (lu % per_row) * kCopyChunk;
+      const uint64_t c1 = min(B.run, c0 + kCopyChunk);
+      uint64_t so = B.src_base, dso = B.dst_base, rem = row;
+      for (int d = B.nd_outer - 1; d >= 0; --d) {
+        const uint64_t c = rem % B.outer_ext[d];
+        rem /= B.outer_ext[d];
+        so += c * B.src_stride[d];
+        dso += c * B.dst_stride[d];
+      }
+      const T* src = next + a.seg_base[E.seg] + so;
+      T* dst = serve + E.dst_base + dso;
+      if (B.vec) {
+        constexpr int VE = Tr::kVE;
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + c0);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+        for (uint64_t j = threadIdx.x; j < (c1 - c0) / VE; j += blockDim.x) d4[j] = ld_stream(s4 + j);
+      } else {
+        for (uint64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) dst[j] = src[j];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_local_route(int dtype, const RouteSideArgs& a, int grid, cudaStream_t s) {
+  if (a.nentries == 0) return cudaSuccess;
+  worklist_kernel<<<1, kWlThreads, 0, s>>>(a);
+  switch (dtype) {
+    case WS_BF16: local_apply_kernel<WS_BF16><<<grid, 256, 0, s>>>(a); break;
+    case WS_I32: local_apply_kernel<WS_I32><<<grid, 256, 0, s>>>(a); break;
+    case WS_F32: local_apply_kernel<WS_F32><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace wsync

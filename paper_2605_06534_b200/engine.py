@@ -1,0 +1,209 @@
+"""The weight-sync engine (TransferEngine::sync_step, engine.hpp:70-92) on one
+GPU of a box, backed by libwsync.
+
+One process per GPU.  ``Plan`` is the static part (plan_pushes / plan_pulls,
+plan.cpp:8-121, extended with FSDP and cross-dim routes); ``TransferEngine``
+owns this rank's device arenas (torch tensors: trainer ``prev``/``next``
+snapshots and the resident serving shards) and runs one sync per call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import BF16, F32, I32, check, lib
+from .codec import SparseDelta, shard_shape
+from .manifest import ParamMeta
+
+TORCH_DTYPE = {BF16: torch.bfloat16, I32: torch.int32, F32: torch.float32}
+VAL_DTYPE = {BF16: torch.int16, I32: torch.int32, F32: torch.float32}
+
+
+@dataclass
+class TrainConfig:
+    """Trainer layout: ``scheme="tp"`` is the reference's TrainConfig{tp,pp,dp}
+    (plan.hpp:11-15); ``scheme="fsdp"`` splits every parameter along dim 0
+    over all ranks."""
+    scheme: str = "fsdp"
+    tp: int = 1
+    pp: int = 1
+    dp: int = 1
+
+    def c(self):
+        return _lib.TrainLayout(1 if self.scheme == "fsdp" else 0, self.tp, self.pp, self.dp)
+
+
+@dataclass
+class ServeConfig:
+    """ServeConfig{tp,pp} (plan.hpp:17-21) x ``replicas``."""
+    tp: int = 1
+    pp: int = 1
+    replicas: int = 1
+
+    def c(self):
+        return _lib.ServeLayout(self.tp, self.pp, self.replicas)
+
+
+class Plan:
+    def __init__(self, manifest, dtype, train: TrainConfig, serve: ServeConfig, world=1, rank=0):
+        self.manifest = [p if isinstance(p, ParamMeta) else ParamMeta(*p) for p in manifest]
+        self.dtype = dtype
+        self.world, self.rank = world, rank
+        arr = (_lib.Param * len(self.manifest))()
+        self._names = []
+        for i, p in enumerate(self.manifest):
+            b = p.name.encode()
+            self._names.append(b)
+            arr[i].name = b
+            arr[i].kind = p.kind
+            arr[i].ndims = len(p.shape)
+            for k, d in enumerate(p.shape):
+                arr[i].shape[k] = d
+            arr[i].layer = p.layer
+        h = C.c_void_p()
+        check(lib.ws_plan_create(arr, len(self.manifest), dtype, C.byref(train.c()),
+                                 C.byref(serve.c()), world, rank, C.byref(h)))
+        self.h = h
+        info = _lib.PlanInfo()
+        check(lib.ws_plan_get_info(h, C.byref(info)))
+        self.info = info
+        self.segments = []
+        for i in range(info.num_segments):
+            p, d, off, n = C.c_int32(), _lib.Shard(), C.c_uint64(), C.c_uint64()
+            check(lib.ws_plan_segment(h, i, C.byref(p), C.byref(d), C.byref(off), C.byref(n)))
+            self.segments.append((p.value, (d.slice_dim, d.start, d.end), off.value, n.value))
+        self.serve_shards = []
+        for i in range(info.num_serve_shards):
+            p, d, off, n = C.c_int32(), _lib.Shard(), C.c_uint64(), C.c_uint64()
+            check(lib.ws_plan_serve_shard(h, i, C.byref(p), C.byref(d), C.byref(off),
+                                          C.byref(n)))
+            self.serve_shards.append((p.value, (d.slice_dim, d.start, d.end), off.value, n.value))
+        self.routes = []
+        for i in range(info.num_routes):
+            s, c, r, ov = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
+            check(lib.ws_plan_route(h, i, C.byref(s), C.byref(c), C.byref(r), C.byref(ov)))
+            self.routes.append((s.value, c.value, r.value, ov.value))
+
+    def __del__(self):
+        try:
+            lib.ws_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib.ws_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class TransferEngine:
+    """One rank's engine.  Arenas are torch CUDA tensors owned here."""
+
+    def __init__(self, plan: Plan, device=None, unique_id: bytes | None = None):
+        self.plan = plan
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else device)
+        td = TORCH_DTYPE[plan.dtype]
+        info = plan.info
+        with torch.cuda.device(self.device):
+            self.arena = [torch.zeros(max(1, info.train_arena_elems), dtype=td,
+                                      device=self.device) for _ in range(2)]
+            self.serve = torch.zeros(max(1, info.serve_arena_elems), dtype=td, device=self.device)
+        uid = None
+        if unique_id is not None:
+            uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib.ws_engine_create(plan.h, self.device.index, uid, C.byref(h)))
+        self.h = h
+        check(lib.ws_engine_bind(h, self.arena[0].data_ptr(), self.arena[1].data_ptr(),
+                                 self.serve.data_ptr()))
+
+    def __del__(self):
+        try:
+            lib.ws_engine_destroy(self.h)
+        except Exception:
+            pass
+
+    # ---- data access -------------------------------------------------------
+    def segment_view(self, i, which=0):
+        """Trainer shard i in arena ``which`` (0 = prev, 1 = next), shaped."""
+        p, desc, off, n = self.plan.segments[i]
+        shp = shard_shape(self.plan.manifest[p].shape, desc)
+        return self.arena[which][off:off + n].view(shp)
+
+    def serve_view(self, i):
+        p, desc, off, n = self.plan.serve_shards[i]
+        shp = shard_shape(self.plan.manifest[p].shape, desc)
+        return self.serve[off:off + n].view(shp)
+
+    # ---- sync ----------------------------------------------------------------
+    def generate(self, seed=1, density=0.01):
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_generate(self.h, seed, density, _stream()))
+
+    def sync_step(self, sparse=True, density_threshold=0.20, reverse=False, report=True,
+                  stream=None):
+        o = _lib.SyncOptions(int(sparse), density_threshold, int(reverse))
+        rep = _lib.Report() if report else None
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_sync_step(self.h, C.byref(o), _stream(stream),
+                                          C.byref(rep) if rep is not None else None))
+        return rep.as_dict() if rep is not None else None
+
+    def sync_step_host(self, next_host: torch.Tensor, sparse=True, density_threshold=0.20,
+                       reverse=False, report=True, stream=None):
+        """Reads the new snapshot from host memory (pinned for full speed)."""
+        if next_host.device.type != "cpu" or next_host.numel() < self.plan.info.train_arena_elems:
+            raise _lib.InvalidArgument("sync_step_host: host snapshot of the trainer arena needed")
+        o = _lib.SyncOptions(int(sparse), density_threshold, int(reverse))
+        rep = _lib.Report() if report else None
+        nnz = (C.c_uint64 * max(1, len(self.plan.segments)))()
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_sync_step_host(self.h, next_host.data_ptr(), C.byref(o),
+                                               _stream(stream), nnz,
+                                               C.byref(rep) if rep is not None else None))
+        return (rep.as_dict() if rep is not None else None), list(nnz)
+
+    def timing(self, reset=True):
+        """Per-stage device-time totals of the syncs since the last reset."""
+        t = _lib.Timing()
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_timing(self.h, int(reset), C.byref(t)))
+        return t.as_dict()
+
+    def segment_delta(self, i) -> tuple:
+        """(SparseDelta of segment i from the last sync, codec 'S'/'D')."""
+        idx, val, nnz, codec = C.c_void_p(), C.c_void_p(), C.c_uint64(), C.create_string_buffer(1)
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            check(lib.ws_engine_segment_delta(self.h, i, C.byref(idx), C.byref(val),
+                                              C.byref(nnz), codec))
+        p, desc, off, n = self.plan.segments[i]
+        shp = shard_shape(self.plan.manifest[p].shape, desc)
+        c = codec.raw[:1].decode()
+        k = nnz.value if c == "S" else 0
+        return SparseDelta(self.plan.dtype, shp, _wrap(idx.value, k, torch.int32, self.device),
+                           _wrap(val.value, k, VAL_DTYPE[self.plan.dtype], self.device)), c, nnz.value
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class _CudaArray:
+    def __init__(self, ptr, n, typestr, device):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, True), "version": 3}
+
+
+def _wrap(ptr, n, dtype, device):
+    """Zero-copy torch view of engine-owned device memory (copied for safety)."""
+    if n == 0 or not ptr:
+        return torch.empty(0, dtype=dtype, device=device)
+    typestr = {torch.int32: "<i4", torch.int16: "<i2", torch.float32: "<f4"}[dtype]
+    return torch.as_tensor(_CudaArray(ptr, n, typestr, device), device=device).clone()

@@ -1,0 +1,154 @@
+"""GPU parity of one whole sync (encode -> route -> apply) on one GPU.
+
+bf16: against the C restatement on the synthetic pair (segment delta streams
+and patched serving weights, bit for bit).  F32/I32: against the compiled,
+unmodified reference engine (TransferEngine::sync_step over MemoryRelay) run
+on the same weights -- serving weights and per-shard codecs must agree."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import BF16, F32, I32
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(t):
+    t = t.detach().cpu().contiguous()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16).ravel()
+    return t.numpy().ravel()
+
+
+def _engine(manifest, dtype=None, train=None, serve=None):
+    import paper_2605_06534_b200 as ws
+    plan = ws.Plan(manifest, ws.BF16 if dtype is None else dtype,
+                   train or ws.TrainConfig("fsdp"), serve or ws.ServeConfig(1, 1, 1))
+    return ws, plan, ws.TransferEngine(plan, device=0)
+
+
+@pytest.mark.parametrize("density", [0.0, 0.01, 0.15])
+def test_bf16_sync_matches_oracle(restatement, density):
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.toy_transformer_manifest(layers=3, hidden=64, vocab=384))
+    eng.generate(seed=5, density=density)
+    rep = eng.sync_step(sparse=True, density_threshold=0.20)
+    assert rep["dense_shards"] == 0
+    total = 0
+    for i, (p, desc, off, n) in enumerate(plan.segments):
+        meta = plan.manifest[p]
+        prev, nxt = restatement.gen_pair_bf16(5, meta.name, meta.shape, desc, density)
+        assert bits(eng.segment_view(i, 0)).tobytes() == prev.tobytes()
+        want_i, want_v = restatement.diff_shards(BF16, prev, nxt)
+        delta, codec, nnz = eng.segment_delta(i)
+        assert codec == "S" and nnz == want_i.size
+        assert delta.indices.cpu().numpy().view(np.uint32).tolist() == want_i.tolist()
+        assert delta.values.cpu().numpy().view(np.uint16).tobytes() == want_v.tobytes()
+        assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
+        total += want_i.size
+    assert rep["nnz"] == total
+    # reverse sync restores the previous version exactly
+    eng.sync_step(sparse=True, density_threshold=0.20, reverse=True)
+    for i, (p, desc, off, n) in enumerate(plan.segments):
+        assert bits(eng.serve_view(i)).tobytes() == bits(eng.segment_view(i, 0)).tobytes()
+
+
+def test_bf16_dense_fallback_and_sparse_off(restatement):
+    import paper_2605_06534_b200 as ws
+    ws_, plan, eng = _engine(ws.toy_transformer_manifest(layers=2, hidden=32, vocab=64))
+    eng.generate(seed=9, density=0.45)  # engine.cpp:121 threshold 0.20 -> all dense
+    rep = eng.sync_step(sparse=True, density_threshold=0.20)
+    assert rep["sparse_shards"] == 0 and rep["dense_shards"] == len(plan.segments)
+    for i in range(len(plan.segments)):
+        assert eng.segment_delta(i)[1] == "D"
+        assert bits(eng.serve_view(i)).tobytes() == bits(eng.segment_view(i, 1)).tobytes()
+    eng.sync_step(sparse=False, reverse=True)
+    for i in range(len(plan.segments)):
+        assert bits(eng.serve_view(i)).tobytes() == bits(eng.segment_view(i, 0)).tobytes()
+
+
+def test_threshold_is_inclusive():
+    """Exactly threshold*n changes stay sparse, one more goes dense (engine.cpp:121)."""
+    import paper_2605_06534_b200 as ws
+    K = ws.ModuleKind
+    _, plan, eng = _engine([ws.ParamMeta("w", K.NORM, (1000,), 0),
+                            ws.ParamMeta("v", K.NORM, (1000,), 0)])
+    a0, a1 = eng.segment_view(0, 0), eng.segment_view(1, 0)
+    a0.zero_(), a1.zero_()
+    eng.segment_view(0, 1).zero_()
+    eng.segment_view(1, 1).zero_()
+    eng.segment_view(0, 1).view(torch.int16)[:200] = 1
+    eng.segment_view(1, 1).view(torch.int16)[:201] = 1
+    rep = eng.sync_step(sparse=True, density_threshold=0.20)
+    assert eng.segment_delta(0)[1] == "S" and eng.segment_delta(1)[1] == "D"
+    assert rep["sparse_shards"] == 1 and rep["dense_shards"] == 1
+
+
+def test_qwen_subset_bf16(restatement):
+    import paper_2605_06534_b200 as ws
+    m = ws.MODELS["qwen2.5-0.5b"](layer_subset=[0, 23])
+    _, plan, eng = _engine(m)
+    eng.generate(seed=1, density=0.01)
+    rep = eng.sync_step()
+    assert rep["dense_shards"] == 0
+    for i, (p, desc, off, n) in enumerate(plan.segments):
+        meta = plan.manifest[p]
+        prev, nxt = restatement.gen_pair_bf16(1, meta.name, meta.shape, desc, 0.01)
+        assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
+
+
+def test_sync_step_host_e2e(restatement):
+    """The new snapshot comes from pinned host memory (the e2e path)."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.toy_transformer_manifest(layers=2, hidden=64, vocab=128))
+    eng.generate(seed=3, density=0.02)
+    host = eng.arena[1].cpu().pin_memory()
+    eng.arena[1].zero_()
+    rep, nnz = eng.sync_step_host(host)
+    for i, (p, desc, off, n) in enumerate(plan.segments):
+        meta = plan.manifest[p]
+        prev, nxt = restatement.gen_pair_bf16(3, meta.name, meta.shape, desc, 0.02)
+        assert nnz[i] == int((prev != nxt).sum())
+        assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes()
+
+
+def _load_reference_state(eng, plan, st, dtype):
+    """Upload the reference's prev/next into our trainer arenas and its prev
+    slices into our serving arena (ServeState::init, engine.cpp:34-49)."""
+    import paper_2605_06534_b200 as ws
+    td = {I32: torch.int32, F32: torch.float32}[dtype]
+    full = {}
+    for i in range(len(plan.manifest)):
+        full[i] = (torch.from_numpy(st.weights(i, 0, dtype)).cuda(),
+                   torch.from_numpy(st.weights(i, 1, dtype)).cuda())
+    for s, (p, desc, off, n) in enumerate(plan.segments):
+        shp = plan.manifest[p].shape
+        eng.segment_view(s, 0).copy_(ws.extract_shard(full[p][0].view(shp).to(td), desc))
+        eng.segment_view(s, 1).copy_(ws.extract_shard(full[p][1].view(shp).to(td), desc))
+    for s, (p, desc, off, n) in enumerate(plan.serve_shards):
+        shp = plan.manifest[p].shape
+        eng.serve_view(s).copy_(ws.extract_shard(full[p][0].view(shp).to(td), desc))
+
+
+@pytest.mark.parametrize("dtype", [I32, F32])
+@pytest.mark.parametrize("density,sparse", [(0.05, True), (0.45, True), (0.05, False)])
+def test_matches_reference_engine(reference, dtype, density, sparse):
+    """Same weights through the reference's sync_step and ours (TP1 -> TP1)."""
+    import paper_2605_06534_b200 as ws
+    st = reference.toy_state(3, 64, 128, dtype, (1, 1, 1), (1, 1), density, 42)
+    ref_rep = st.run(mode_async=True, shard_aware=True, sparse=sparse, threshold=0.20,
+                     bucket_bytes=8192)
+    plan = ws.Plan([ws.ParamMeta(n, k, tuple(s), l) for (n, k, s, l) in st.params], dtype,
+                   ws.TrainConfig("tp", 1, 1, 1), ws.ServeConfig(1, 1, 1))
+    eng = ws.TransferEngine(plan, device=0)
+    _load_reference_state(eng, plan, st, dtype)
+    rep = eng.sync_step(sparse=sparse, density_threshold=0.20)
+    assert rep["dense_shards"] == ref_rep["dense_shards"]
+    assert rep["sparse_shards"] == ref_rep["sparse_shards"]
+    assert rep["pushed_bytes"] == ref_rep["pushed_bytes"]  # transfer_cases.hpp:187-199
+    codecs = {d[0]: c for d, c in st.codecs()}
+    for s, (p, desc, off, n) in enumerate(plan.segments):
+        assert eng.segment_delta(s)[1] == codecs[p]
+    for s, (p, desc, off, n) in enumerate(plan.serve_shards):
+        want = st.serve(0, p, dtype)
+        assert bits(eng.serve_view(s)).tobytes() == want.tobytes(), plan.manifest[p].name

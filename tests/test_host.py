@@ -1,0 +1,145 @@
+"""Host-side tests (CPU only): the C-ABI library loads and exports every
+symbol include/wsync.h declares, and the planner matches the reference's
+plan_pushes/plan_pulls (plan.cpp:8-121) wherever the reference can express
+the layout, plus its own extensions (FSDP, cross-dim routes)."""
+import os
+import re
+from collections import defaultdict
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+
+    from paper_2605_06534_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "wsync.h")).read()
+    declared = set(re.findall(r"\b(ws_[a-z0-9_]+)\s*\(", hdr))
+    assert len(declared) >= 24
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(_lib.SYMBOLS) <= declared
+
+
+def test_library_has_sm100a_code():
+    import subprocess
+
+    from paper_2605_06534_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_qwen_manifest_sizes():
+    from paper_2605_06534_b200.manifest import MODELS, manifest_numel
+    assert manifest_numel(MODELS["qwen2.5-0.5b"]()) == 494_032_768  # SURVEY §6 probe
+    assert manifest_numel(MODELS["qwen3-8b"]()) == 8_190_735_360
+    assert abs(manifest_numel(MODELS["qwen3-32b"]()) - 32.76e9) < 0.01e9
+    assert abs(manifest_numel(MODELS["qwen3-30b-a3b"]()) - 30.53e9) < 0.01e9
+
+
+def _ref_manifest(m):
+    return [p.as_tuple() for p in m]
+
+
+@pytest.mark.parametrize("train,serve", [((2, 1, 1), (4, 1)), ((2, 1, 2), (2, 1)),
+                                         ((4, 2, 1), (2, 2)), ((1, 1, 3), (1, 1)),
+                                         ((2, 2, 2), (4, 1)), ((8, 1, 1), (4, 1))])
+def test_routes_match_reference_plan_pulls(reference, train, serve):
+    """Every serving coordinate pulls exactly the source shards plan_pulls picks."""
+    import paper_2605_06534_b200 as ws
+    manifest = ws.toy_transformer_manifest(layers=4, hidden=64, vocab=128)
+    _, pulls = reference.plan(_ref_manifest(manifest), train, serve)
+    want = defaultdict(set)
+    for (rank, param, tp_rank, tp_size, stage, dim, start, end) in pulls:
+        want[rank].add((param, dim, start if dim >= 0 else 0, end if dim >= 0 else 0))
+    world = train[0] * train[1] * train[2]
+    # our serving layout: replicas fill the world when it is larger
+    replicas = max(1, world // (serve[0] * serve[1]))
+    if serve[0] * serve[1] * replicas != world:
+        pytest.skip("world does not factor into serve replicas")
+    got = defaultdict(set)
+    for r in range(world):
+        plan = ws.Plan(manifest, ws.I32, ws.TrainConfig("tp", *train), ws.ServeConfig(*serve,
+                       replicas), world=world, rank=r)
+        for (seg, coord, nrep, ov) in plan.routes:
+            p, desc, off, n = plan.segments[seg]
+            got[coord].add((p, desc[0], desc[1] if desc[0] >= 0 else 0,
+                            desc[2] if desc[0] >= 0 else 0))
+    assert got == want
+
+
+def test_pushes_deal_every_shard_once(reference):
+    """plan.cpp:8-21: each distinct shard encoded by exactly one rank."""
+    import paper_2605_06534_b200 as ws
+    manifest = ws.toy_transformer_manifest(layers=4, hidden=256, vocab=1024)
+    pushes, _ = reference.plan(_ref_manifest(manifest), (4, 2, 1), (1, 1))
+    want = sorted((p, d, s, e) for (p, _, _, _, d, s, e) in pushes)
+    got = []
+    for r in range(8):
+        plan = ws.Plan(manifest, ws.I32, ws.TrainConfig("tp", 4, 2, 1),
+                       ws.ServeConfig(1, 1, 8), world=8, rank=r)
+        for (p, desc, off, n) in plan.segments:
+            got.append((p, desc[0], desc[1], desc[2]))
+    norm = lambda x: (x[0], x[1], x[2] if x[1] >= 0 else 0, x[3] if x[1] >= 0 else 0)  # noqa
+    assert sorted(map(norm, got)) == sorted(map(norm, want))
+
+
+def test_fsdp_to_tp_cross_dim_routes():
+    """FSDP dim-0 trainer shards feed RowLinear dim-1 serving shards (the
+    reference reports IncompleteCoverage here, plan.cpp:51-55)."""
+    import paper_2605_06534_b200 as ws
+    m = ws.MODELS["qwen3-8b"]()
+    total_overlap = defaultdict(int)
+    for r in range(8):
+        plan = ws.Plan(m, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, 4), world=8,
+                       rank=r)
+        assert plan.info.serve_coord == r % 2
+        for (seg, coord, nrep, ov) in plan.routes:
+            p = plan.segments[seg][0]
+            total_overlap[(coord, p)] += ov
+            assert nrep == 4
+    for (coord, p), ov in total_overlap.items():
+        meta = m[p]
+        want = meta.numel() // 2 if meta.kind in (0, 1, 2) else meta.numel()
+        assert ov == want, meta.name
+
+
+def test_reference_cannot_express_fsdp_row(reference):
+    """The reference's cover drops cross-dim sources (finding 3)."""
+    from oracle.oracle import OracleError
+    manifest = [("w", 1, [8, 8], 0)]  # RowLinear: serving slices dim 1
+    # a trainer sliced on dim 0 is not expressible as a TrainConfig at all, so
+    # check the codec-level restriction instead
+    import numpy as np
+    with pytest.raises(OracleError) as e:
+        reference.reslice_delta(1, [8, 8], (0, 0, 4), (1, 0, 4), [4, 8],
+                                np.array([1], np.uint64), np.array([1], np.int32))
+    assert e.value.kind == "ShapeMismatch"
+    assert manifest
+
+
+def test_plan_errors():
+    import paper_2605_06534_b200 as ws
+    K = ws.ModuleKind
+    with pytest.raises(ws.IndivisibleShape):
+        ws.Plan([ws.ParamMeta("w", K.COLUMN_LINEAR, (6, 4), 0)], ws.BF16, ws.TrainConfig("fsdp"),
+                ws.ServeConfig(4, 1, 1), world=4, rank=0)
+    with pytest.raises(ws.UnknownModuleKind):
+        ws.Plan([ws.ParamMeta("w", 99, (8, 4), 0)], ws.BF16, ws.TrainConfig("fsdp"),
+                ws.ServeConfig(1, 1, 1))
+    with pytest.raises(ws.InvalidArgument):
+        ws.Plan([ws.ParamMeta("w", K.NORM, (8,), 0)], ws.BF16, ws.TrainConfig("tp", 2, 1, 1),
+                ws.ServeConfig(1, 1, 1), world=1, rank=0)
+
+
+def test_arena_alignment():
+    import paper_2605_06534_b200 as ws
+    plan = ws.Plan(ws.MODELS["qwen2.5-0.5b"](), ws.BF16, ws.TrainConfig("fsdp"),
+                   ws.ServeConfig(1, 1, 1))
+    for (p, desc, off, n) in plan.segments + plan.serve_shards:
+        assert off % 64 == 0
+    assert plan.info.train_elems == 494_032_768
