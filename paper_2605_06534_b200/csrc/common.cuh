@@ -111,33 +111,48 @@ __device__ __forceinline__ unsigned long long make_status(uint32_t epoch, uint32
 // Exclusive prefix of `tile` within its chain [first_tile, tile): executed by
 // one full warp.  Every tile of the chain publishes its aggregate before
 // looking back, and the chain head publishes an inclusive prefix, so the walk
-// terminates.
+// terminates.  Each lane inspects 4 predecessors, so one L2 round trip covers
+// a window of 128 tiles (the walk's throughput bound is window / latency).
 __device__ __forceinline__ uint32_t warp_lookback(const unsigned long long* status,
                                                   int64_t tile, int64_t first_tile,
                                                   uint32_t epoch) {
+  constexpr int J = 4;
   const int lane = threadIdx.x & 31;
   const unsigned long long want = (unsigned long long)(epoch & 0x3fffffffu);
   uint32_t excl = 0;
   int64_t pos = tile - 1;
   while (true) {
-    const int64_t my = pos - lane;
-    uint32_t flag = 0, val = 0;
-    if (my >= first_tile) {
-      unsigned long long st;
-      do {
-        st = ld_relaxed_u64(status + my);
-      } while ((st >> 34) != want);
-      flag = (uint32_t)(st >> 32) & 3u;
-      val = (uint32_t)st;
+    uint32_t flag[J], val[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t my = pos - (int64_t)(lane * J + j);
+      flag[j] = 0;
+      val[j] = 0;
+      if (my >= first_tile) {
+        unsigned long long st = ld_relaxed_u64(status + my);
+        while ((st >> 34) != want) {
+          __nanosleep(32);
+          st = ld_relaxed_u64(status + my);
+        }
+        flag[j] = (uint32_t)(st >> 32) & 3u;
+        val[j] = (uint32_t)st;
+      }
     }
-    const unsigned pmask = __ballot_sync(kFullMask, flag == kFlagPrefix);
-    const int stop = pmask ? __ffs(pmask) - 1 : 31;
-    uint32_t c = lane <= stop ? val : 0u;
+    int jp = J;  // nearest predecessor of this lane holding an inclusive prefix
+#pragma unroll
+    for (int j = J - 1; j >= 0; --j)
+      if (flag[j] == kFlagPrefix) jp = j;
+    const unsigned pmask = __ballot_sync(kFullMask, jp < J);
+    const int stop = pmask ? __ffs(pmask) - 1 : 32;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (lane < stop || (lane == stop && j <= jp)) c += val[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFullMask, c, o);
     excl += c;
     if (pmask) break;
-    pos -= 32;
+    pos -= 32 * J;
   }
   return excl;
 }

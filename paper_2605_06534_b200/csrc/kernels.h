@@ -9,12 +9,14 @@
 namespace wsync {
 
 constexpr int kEncodeThreads = 256;
-constexpr int kEncodeVPT = 4;  // 16-byte vectors per thread per array per tile
+constexpr int kEncodeVPT = 4;        // 16-byte vectors per thread per array per sub-tile
+constexpr int kEncodeSubTiles = 8;   // sub-tiles per super-tile (one look-back each)
+constexpr uint32_t kStageCap = 4096; // records staged in shared memory per super-tile
 
-// Elements per encode tile: 8192 for bf16, 4096 for 4-byte dtypes (16 KB of
-// prev plus 16 KB of next per tile).
+// Elements per encode super-tile: 65536 for bf16, 32768 for 4-byte dtypes
+// (128 KB of prev plus 128 KB of next).
 inline uint32_t encode_tile_elems(int dtype) {
-  return kEncodeThreads * kEncodeVPT * (dtype == WS_BF16 ? 8 : 4);
+  return kEncodeThreads * kEncodeVPT * (dtype == WS_BF16 ? 8 : 4) * kEncodeSubTiles;
 }
 inline uint32_t elems_per_vec(int dtype) { return dtype == WS_BF16 ? 8 : 4; }
 inline int dtype_size(int dtype) { return dtype == WS_BF16 ? 2 : 4; }
@@ -40,6 +42,7 @@ struct EncodeArgs {
   unsigned long long* status;  // >= ntiles words
   uint32_t epoch;
   unsigned int* ticket;        // zeroed before launch
+  uint32_t debug;              // perf experiments only (WSYNC_ENCODE_DEBUG): 1 no look-back, 2 no writes
 };
 
 // K1: fused compare + ballot/popc + block scan + decoupled look-back

@@ -9,6 +9,7 @@
 // are written at their final ascending position.  Segments are independent
 // look-back chains so every segment's records start at its own base.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -60,31 +61,102 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
   return inc - x + s_warp[warp];
 }
 
+// One block owns one super-tile (kEncodeSubTiles sub-tiles of kThreads x
+// kVPT 16-byte vectors) at a time; records are ordered by element, i.e. by
+// chunk c = (sub-tile g, vector slot v, warp w) and then lane/element.
+//   phase 1 (warp-local, no block barrier): each warp streams its chunks with
+//     128-bit loads, builds the change masks, ranks records with a shuffle
+//     scan of popc(mask) and stages them in its own shared-memory slice;
+//   phase 2: one block scan over the 256 chunk counts gives every chunk's
+//     super-tile-local offset, and warp 0 resolves the super-tile's offset in
+//     its segment with the decoupled look-back (one per 256 KB of input);
+//   phase 3: each warp flushes its staged records with coalesced stores.
+// A warp whose chunks overflow its staging slice re-derives the overflow
+// records from global memory (warp-local slow path).
 template <int DT>
-__global__ void __launch_bounds__(kThreads) encode_kernel(EncodeArgs a) {
+__device__ __noinline__ void encode_overflow(const EncodeArgs& a, const SegDev& sg, uint64_t e0,
+                                             uint32_t cnt, uint64_t prefix, const uint32_t* s_cnt,
+                                             const uint32_t* s_off, uint32_t wstart_lane) {
   using Tr = Traits<DT>;
   using T = typename Tr::T;
   constexpr int VE = Tr::kVE;
-  constexpr uint32_t TILE = kThreads * kVPT * VE;
+  constexpr uint32_t SUB = kThreads * kVPT * VE;
+  constexpr uint32_t WCAP = kStageCap / kWarps;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const T* prevT = reinterpret_cast<const T*>(a.prev);
+  const T* nextT = reinterpret_cast<const T*>(a.next);
+  T* out_val = reinterpret_cast<T*>(a.out_val);
+  for (int c = 0; c < kEncodeSubTiles * kVPT; ++c) {
+    const uint32_t ccnt = s_cnt[c * kWarps + w];
+    const uint32_t start = __shfl_sync(kFullMask, wstart_lane, c);
+    if (start + ccnt <= WCAP || ccnt == 0) continue;  // fully staged
+    const int g = c / kVPT, v = c % kVPT;
+    const uint32_t off = g * SUB + (uint32_t)(v * kThreads + w * 32 + lane) * VE;
+    uint32_t m = 0;
+    T ta[VE], tb[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      const bool in = off + e < cnt;
+      ta[e] = in ? prevT[sg.base + e0 + off + e] : T(0);
+      tb[e] = in ? nextT[sg.base + e0 + off + e] : T(0);
+      if (in && Tr::changed(ta[e], tb[e])) m |= 1u << e;
+    }
+    uint32_t incl = __popc(m);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t k = incl - __popc(m);
+    const uint64_t goff = prefix + s_off[c * kWarps + w];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) {
+      if (m & (1u << e)) {
+        const uint64_t pos = goff + k;
+        if (start + k >= WCAP && pos < sg.cap) {
+          a.out_idx[sg.rec + pos] = (uint32_t)(e0 + off + e);
+          out_val[sg.rec + pos] = Tr::delta(ta[e], tb[e]);
+        }
+        ++k;
+      }
+    }
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 4) encode_kernel(EncodeArgs a) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  constexpr int VE = Tr::kVE;
+  constexpr uint32_t SUB = kThreads * kVPT * VE;
+  constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
+  constexpr int NCH = kEncodeSubTiles * kVPT;  // chunks per warp per super-tile (32)
+  constexpr uint32_t WCAP = kStageCap / kWarps;
+  static_assert(NCH == 32, "one lane per chunk in the flush");
+  static_assert(NCH * kWarps == kThreads, "one thread per chunk in the block scan");
 
   __shared__ unsigned long long s_warp[kWarps + 1];
   __shared__ uint32_t s_tile[2];
   __shared__ uint32_t s_prefix;
+  __shared__ uint32_t s_cnt[NCH * kWarps];   // chunk counts, index c * kWarps + w
+  __shared__ uint32_t s_off[NCH * kWarps];   // chunk offsets within the super-tile
+  __shared__ uint32_t s_idx[kStageCap];      // warp w stages at [w * WCAP, (w + 1) * WCAP)
+  __shared__ T s_val[kStageCap];
 
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_tile[0] = atomicAdd(a.ticket, 1u);
   __syncthreads();
-
-  // Empty segments have no tile: block 0 publishes their zero counts.
-  if (blockIdx.x == 0 && a.segs) {
+  if (blockIdx.x == 0 && a.segs) {  // empty segments have no tile
     for (int s = tid; s < a.nseg; s += kThreads)
       if (a.segs[s].n == 0) a.seg_nnz[s] = 0;
   }
-
   const uint4* prev4 = reinterpret_cast<const uint4*>(a.prev);
   const uint4* next4 = reinterpret_cast<const uint4*>(a.next);
+  const T* prevT = reinterpret_cast<const T*>(a.prev);
+  const T* nextT = reinterpret_cast<const T*>(a.next);
   T* out_val = reinterpret_cast<T*>(a.out_val);
+  uint32_t* w_idx = s_idx + w * WCAP;
+  T* w_val = s_val + w * WCAP;
 
   for (int it = 0;; ++it) {
     const uint32_t t = s_tile[it & 1];
@@ -94,60 +166,77 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncodeArgs a) {
     const int s = a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0;
     const SegDev sg = a.segs ? a.segs[s] : a.seg0;
     const uint32_t lt = a.tile0 ? t - __ldg(a.tile0 + s) : t;
-    const uint64_t e0 = (uint64_t)lt * TILE;
+    const uint64_t e0 = (uint64_t)lt * SUPER;
     const uint64_t rem_n = sg.n - e0;
-    const uint32_t cnt = rem_n < TILE ? (uint32_t)rem_n : TILE;
+    const uint32_t cnt = rem_n < SUPER ? (uint32_t)rem_n : SUPER;
     const bool last_tile = (a.tile0 ? __ldg(a.tile0 + s + 1) : a.ntiles) == t + 1;
-
-    // ---- load the tile: kVPT coalesced 16-byte vectors per thread per array
-    uint4 pa[kVPT], pb[kVPT];
     const uint64_t vbase = (sg.base + e0) / VE;
+
+    // ---- phase 1: warp-local streaming, ranking and staging
+    uint32_t running = 0;  // records staged by this warp so far (warp-uniform)
+#pragma unroll 1
+    for (int g = 0; g < kEncodeSubTiles; ++g) {
+      const uint32_t g0 = g * SUB;
+      uint4 pa[kVPT], pb[kVPT];
 #pragma unroll
-    for (int v = 0; v < kVPT; ++v) {
-      const uint32_t off = (uint32_t)(v * kThreads + tid) * VE;
-      if (off + VE <= cnt) {
-        pa[v] = ld_stream(prev4 + vbase + off / VE);
-        pb[v] = ld_stream(next4 + vbase + off / VE);
-      } else {
-        pa[v] = make_uint4(0, 0, 0, 0);
-        pb[v] = make_uint4(0, 0, 0, 0);
-        if (off < cnt) {  // ragged tail: element loads, the rest stays equal
-          const T* p = reinterpret_cast<const T*>(a.prev) + sg.base + e0 + off;
-          const T* q = reinterpret_cast<const T*>(a.next) + sg.base + e0 + off;
-          T ta[VE], tb[VE];
+      for (int v = 0; v < kVPT; ++v) {
+        const uint32_t off = g0 + (uint32_t)(v * kThreads + tid) * VE;
+        if (off + VE <= cnt) {
+          pa[v] = ld_stream(prev4 + vbase + off / VE);
+          pb[v] = ld_stream(next4 + vbase + off / VE);
+        } else {
+          pa[v] = make_uint4(0, 0, 0, 0);
+          pb[v] = make_uint4(0, 0, 0, 0);
+          if (off < cnt) {  // ragged tail
+            T ta[VE], tb[VE];
 #pragma unroll
-          for (int e = 0; e < VE; ++e) {
-            ta[e] = off + e < cnt ? p[e] : T(0);
-            tb[e] = off + e < cnt ? q[e] : T(0);
+            for (int e = 0; e < VE; ++e) {
+              ta[e] = off + e < cnt ? prevT[sg.base + e0 + off + e] : T(0);
+              tb[e] = off + e < cnt ? nextT[sg.base + e0 + off + e] : T(0);
+            }
+            memcpy(&pa[v], ta, 16);
+            memcpy(&pb[v], tb, 16);
           }
-          memcpy(&pa[v], ta, 16);
-          memcpy(&pb[v], tb, 16);
         }
       }
-    }
-
-    // ---- change masks and packed per-vector counts
-    uint32_t m[kVPT];
-    unsigned long long packed = 0;
 #pragma unroll
-    for (int v = 0; v < kVPT; ++v) {
-      m[v] = change_mask<DT>(pa[v], pb[v]);
-      packed |= (unsigned long long)__popc(m[v]) << (16 * v);
+      for (int v = 0; v < kVPT; ++v) {
+        const uint32_t m = change_mask<DT>(pa[v], pb[v]);
+        uint32_t incl = __popc(m);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(kFullMask, incl, 31);
+        if (lane == 0) s_cnt[(g * kVPT + v) * kWarps + w] = tot;
+        if (m) {
+          uint32_t k = running + incl - __popc(m);
+          const uint32_t off = g0 + (uint32_t)(v * kThreads + tid) * VE;
+#pragma unroll
+          for (int e = 0; e < VE; ++e) {
+            if (m & (1u << e)) {
+              if (k < WCAP) {
+                w_idx[k] = off + e;
+                w_val[k] = Tr::delta(Tr::get(pa[v], e), Tr::get(pb[v], e));
+              }
+              ++k;
+            }
+          }
+        }
+        running += tot;
+      }
     }
+    __syncthreads();
+
+    // ---- phase 2: chunk offsets (block scan) + look-back for the super-tile
     unsigned long long total;
-    const unsigned long long excl = block_scan_packed(packed, s_warp, &total);
-    uint32_t vstart[kVPT];
-    uint32_t tile_count = 0;
-#pragma unroll
-    for (int v = 0; v < kVPT; ++v) {
-      vstart[v] = tile_count;
-      tile_count += (uint32_t)(total >> (16 * v)) & 0xffffu;
-    }
-
-    // ---- decoupled look-back across the segment's tiles (warp 0)
-    if (warp == 0) {
+    const uint32_t my_cnt = s_cnt[tid];
+    s_off[tid] = (uint32_t)block_scan_packed(my_cnt, s_warp, &total);
+    const uint32_t tile_count = (uint32_t)total;
+    if (w == 0) {
       uint32_t prefix = 0;
-      if (lt == 0) {
+      if (lt == 0 || (a.debug & 1)) {
         if (tid == 0) st_relaxed_u64(a.status + t, make_status(a.epoch, kFlagPrefix, tile_count));
       } else {
         if (tid == 0) st_relaxed_u64(a.status + t, make_status(a.epoch, kFlagAggregate, tile_count));
@@ -161,28 +250,40 @@ __global__ void __launch_bounds__(kThreads) encode_kernel(EncodeArgs a) {
       }
     }
     __syncthreads();
-    const uint32_t prefix = s_prefix;
+    const uint64_t prefix = s_prefix;
 
-    // ---- write records at their final positions (ascending index order)
+    // ---- phase 3: flush this warp's staged records (lane c owns chunk c)
+    const uint32_t ccnt = s_cnt[lane * kWarps + w];
+    uint32_t wincl = ccnt;
 #pragma unroll
-    for (int v = 0; v < kVPT; ++v) {
-      uint32_t mm = m[v];
-      if (!mm) continue;
-      uint64_t pos = (uint64_t)prefix + vstart[v] + ((uint32_t)(excl >> (16 * v)) & 0xffffu);
-      const uint32_t off = (uint32_t)(v * kThreads + tid) * VE;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFullMask, wincl, o);
+      if (lane >= o) wincl += y;
+    }
+    const uint32_t wstart = wincl - ccnt;  // chunk's first slot in the warp's staging
+    const uint32_t staged = min(running, WCAP);
+    if (!(a.debug & 2)) {
+      for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        // owner chunk of staged record k: the largest c with start(c) <= k
+        // (starts are non-decreasing; an empty chunk shares its successor's)
+        int c = 0;
 #pragma unroll
-      for (int e = 0; e < VE; ++e) {
-        if (mm & (1u << e)) {
+        for (int b = 16; b > 0; b >>= 1)
+          if (__shfl_sync(kFullMask, wstart, c + b) <= k) c += b;
+        const uint32_t cstart = __shfl_sync(kFullMask, wstart, c);
+        if (k < staged) {
+          const uint64_t pos = prefix + s_off[c * kWarps + w] + (k - cstart);
           if (pos < sg.cap) {
-            a.out_idx[sg.rec + pos] = (uint32_t)(e0 + off + e);
-            out_val[sg.rec + pos] = Tr::delta(Tr::get(pa[v], e), Tr::get(pb[v], e));
+            a.out_idx[sg.rec + pos] = (uint32_t)(e0 + w_idx[k]);
+            out_val[sg.rec + pos] = w_val[k];
           }
-          ++pos;
         }
       }
     }
-    // s_tile/s_prefix/s_warp are rewritten next iteration only after the
-    // block scan's first barrier, which every thread reaches after this point.
+    if (running > WCAP && !(a.debug & 2))
+      encode_overflow<DT>(a, sg, e0, cnt, prefix, s_cnt, s_off, wstart);
+    __syncthreads();  // staging, s_cnt and s_prefix are reused by the next super-tile
   }
 }
 
@@ -372,13 +473,16 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
     default: return cudaErrorInvalidValue;
   }
   grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)grid, std::max(a.ntiles, 1u)));
+  if (const char* g = getenv("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
+  EncodeArgs a2 = a;
+  if (const char* d = getenv("WSYNC_ENCODE_DEBUG")) a2.debug = (uint32_t)atoi(d);
   if (grid_out) *grid_out = grid;
   cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   switch (dtype) {
-    case WS_BF16: encode_kernel<WS_BF16><<<grid, kThreads, 0, s>>>(a); break;
-    case WS_I32: encode_kernel<WS_I32><<<grid, kThreads, 0, s>>>(a); break;
-    default: encode_kernel<WS_F32><<<grid, kThreads, 0, s>>>(a); break;
+    case WS_BF16: encode_kernel<WS_BF16><<<grid, kThreads, 0, s>>>(a2); break;
+    case WS_I32: encode_kernel<WS_I32><<<grid, kThreads, 0, s>>>(a2); break;
+    default: encode_kernel<WS_F32><<<grid, kThreads, 0, s>>>(a2); break;
   }
   return cudaGetLastError();
 }

@@ -198,7 +198,7 @@ def _stream(stream=None):
 class _CudaArray:
     def __init__(self, ptr, n, typestr, device):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
-                                         "data": (ptr, True), "version": 3}
+                                         "data": (ptr, False), "version": 3}
 
 
 def _wrap(ptr, n, dtype, device):

@@ -33,20 +33,24 @@ def test_bf16_sync_matches_oracle(restatement, density):
     _, plan, eng = _engine(ws.toy_transformer_manifest(layers=3, hidden=64, vocab=384))
     eng.generate(seed=5, density=density)
     rep = eng.sync_step(sparse=True, density_threshold=0.20)
-    assert rep["dense_shards"] == 0
-    total = 0
+    total, dense = 0, 0
     for i, (p, desc, off, n) in enumerate(plan.segments):
         meta = plan.manifest[p]
         prev, nxt = restatement.gen_pair_bf16(5, meta.name, meta.shape, desc, density)
         assert bits(eng.segment_view(i, 0)).tobytes() == prev.tobytes()
         want_i, want_v = restatement.diff_shards(BF16, prev, nxt)
         delta, codec, nnz = eng.segment_delta(i)
-        assert codec == "S" and nnz == want_i.size
-        assert delta.indices.cpu().numpy().view(np.uint32).tolist() == want_i.tolist()
-        assert delta.values.cpu().numpy().view(np.uint16).tobytes() == want_v.tobytes()
+        assert nnz == want_i.size
+        # engine.cpp:121: small shards can exceed the threshold at 15% density
+        assert codec == ("S" if restatement.is_sparse(nnz, n, 0.20) else "D")
+        if codec == "S":
+            assert delta.indices.cpu().numpy().view(np.uint32).tolist() == want_i.tolist()
+            assert delta.values.cpu().numpy().view(np.uint16).tobytes() == want_v.tobytes()
+        else:
+            dense += 1
         assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
         total += want_i.size
-    assert rep["nnz"] == total
+    assert rep["nnz"] == total and rep["dense_shards"] == dense
     # reverse sync restores the previous version exactly
     eng.sync_step(sparse=True, density_threshold=0.20, reverse=True)
     for i, (p, desc, off, n) in enumerate(plan.segments):
