@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libwsync.so")
+LIB_PATH = os.environ.get("WSYNC_LIB") or os.path.join(HERE, "lib", "libwsync.so")
 
 # ---- ws_status -> the reference's TransferError hierarchy (tensor.hpp:16-24,
 # codec.hpp:9-11, shard.hpp:9-14, plan.hpp:7-9, relay.hpp:17-22, key.hpp:10-12)

@@ -8,15 +8,27 @@
 
 namespace wsync {
 
-constexpr int kEncodeThreads = 256;
-constexpr int kEncodeVPT = 4;        // 16-byte vectors per thread per array per sub-tile
-constexpr int kEncodeSubTiles = 8;   // sub-tiles per super-tile (one look-back each)
-constexpr uint32_t kStageCap = 4096; // records staged in shared memory per super-tile
+#ifndef WS_ENC_SUBTILES
+#define WS_ENC_SUBTILES 4
+#endif
+#ifndef WS_ENC_RING
+#define WS_ENC_RING 3
+#endif
+#ifndef WS_ENC_CONSUMERS
+#define WS_ENC_CONSUMERS 512
+#endif
+constexpr int kEncodeThreads = 256;                 // block size of the small codec kernels
+constexpr int kEncodeVPT = 4;                       // their vectors per thread
+constexpr int kEncConsumers = WS_ENC_CONSUMERS;     // K1 consumer threads (16 warps)
+constexpr int kEncodeBlock = kEncConsumers + 3 * 32;  // + TMA producer + 2 resolver warps
+constexpr int kEncodeSubTiles = WS_ENC_SUBTILES;    // sub-tiles (ring stages) per super-tile
+constexpr int kRing = WS_ENC_RING;                  // shared-memory ring stages
+constexpr uint32_t kStageBytes = 16384;             // per array per stage
 
-// Elements per encode super-tile: 65536 for bf16, 32768 for 4-byte dtypes
-// (128 KB of prev plus 128 KB of next).
+// Elements per encode super-tile: 32768 for bf16, 16384 for 4-byte dtypes
+// (64 KB of prev plus 64 KB of next).
 inline uint32_t encode_tile_elems(int dtype) {
-  return kEncodeThreads * kEncodeVPT * (dtype == WS_BF16 ? 8 : 4) * kEncodeSubTiles;
+  return kStageBytes / (dtype == WS_BF16 ? 2 : 4) * kEncodeSubTiles;
 }
 inline uint32_t elems_per_vec(int dtype) { return dtype == WS_BF16 ? 8 : 4; }
 inline int dtype_size(int dtype) { return dtype == WS_BF16 ? 2 : 4; }

@@ -61,230 +61,406 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
   return inc - x + s_warp[warp];
 }
 
-// One block owns one super-tile (kEncodeSubTiles sub-tiles of kThreads x
-// kVPT 16-byte vectors) at a time; records are ordered by element, i.e. by
-// chunk c = (sub-tile g, vector slot v, warp w) and then lane/element.
-//   phase 1 (warp-local, no block barrier): each warp streams its chunks with
-//     128-bit loads, builds the change masks, ranks records with a shuffle
-//     scan of popc(mask) and stages them in its own shared-memory slice;
-//   phase 2: one block scan over the 256 chunk counts gives every chunk's
-//     super-tile-local offset, and warp 0 resolves the super-tile's offset in
-//     its segment with the decoupled look-back (one per 256 KB of input);
-//   phase 3: each warp flushes its staged records with coalesced stores.
-// A warp whose chunks overflow its staging slice re-derives the overflow
-// records from global memory (warp-local slow path).
+// K1 as a warp-specialised pipeline (one persistent block per SM):
+//   warp 16      producer: claims super-tiles in order (one ticket each) and
+//                streams their sub-tiles of prev and next into a kRing-deep
+//                shared-memory ring with 1-D bulk copies (cp.async.bulk)
+//                completing on per-stage mbarriers;
+//   warps 0-15   consumers: per 16-byte vector the change mask (bit compare
+//                for bf16/i32, value compare for f32); per (sub-tile, vector
+//                slot, warp) chunk the record count; records ranked with a
+//                ballot/popc fast path (shuffle scan when a lane holds two or
+//                more) and staged in the warp's slice of a double-buffered
+//                staging area.  Each stage is released as soon as it is
+//                counted, so HBM streams continuously;
+//   warps 17-18  resolvers (one per staging buffer): scan the chunk counts,
+//                publish the super-tile count, resolve its offset in its
+//                segment with the decoupled look-back, and flush the staged
+//                records to their final ascending positions with coalesced
+//                stores.  Look-back latency never stalls the stream.
+// Super-tiles denser than 25% spill: records past a warp slice are
+// re-derived from the kept masks and global memory by the resolver.
+struct StageMeta {
+  SegDev sg;
+  uint32_t t, s, lt, nsub, cnt, last;
+  uint32_t pad[2];
+};
+
 template <int DT>
-__device__ __noinline__ void encode_overflow(const EncodeArgs& a, const SegDev& sg, uint64_t e0,
-                                             uint32_t cnt, uint64_t prefix, const uint32_t* s_cnt,
-                                             const uint32_t* s_off, uint32_t wstart_lane) {
+struct EncCfg {
+  using T = typename Traits<DT>::T;
+  static constexpr int VE = Traits<DT>::kVE;
+  static constexpr int NCW = kEncConsumers / 32;                      // consumer warps
+  static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
+  static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
+  static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
+  static constexpr uint32_t CAP = SUPER / 4;                          // staged records per buffer
+  static constexpr uint32_t WCAP = CAP / NCW;
+  static constexpr int NCH = kEncodeSubTiles * VPT * NCW;             // chunks per super-tile
+  static constexpr int CPW = kEncodeSubTiles * VPT;                   // chunks per consumer warp
+  static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
+  static constexpr size_t kSmem = kRingBytes + 2 * (size_t)CAP * (4 + sizeof(T)) +
+                                  2 * (size_t)kEncodeSubTiles * kEncConsumers * 4 +  // masks
+                                  2 * NCH * 4 * 2 + 2 * NCW * 4 +                    // cnt/off/wrun
+                                  (kRing + 2) * sizeof(StageMeta) + 32 + 16 + (2 * kRing + 4) * 8;
+  static_assert(NCH % 32 == 0, "chunks per lane");
+  static_assert(CPW <= 32 && (CPW & (CPW - 1)) == 0, "chunk search over lanes");
+  static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
+};
+
+// Warp exclusive rank of popc(mv) and the warp total: a ballot fast path
+// when no lane holds two or more records, a shuffle scan otherwise.
+__device__ __forceinline__ uint32_t warp_rank(uint32_t mv, uint32_t* tot) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = __popc(mv);
+  const unsigned b1 = __ballot_sync(kFullMask, c > 0);
+  const unsigned b2 = __ballot_sync(kFullMask, c > 1);
+  if (!b2) {
+    *tot = __popc(b1);
+    return __popc(b1 & ((1u << lane) - 1u));
+  }
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+    if (lane >= o) incl += y;
+  }
+  *tot = __shfl_sync(kFullMask, incl, 31);
+  return incl - c;
+}
+
+// Resolver step for one staged super-tile (one warp): scan the chunk counts
+// into chunk offsets, publish the super-tile's count, resolve its offset in
+// its segment with the decoupled look-back, publish the inclusive prefix.
+template <int DT>
+__device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMeta& ti,
+                                             const uint32_t* s_cnt, uint32_t* s_off,
+                                             unsigned long long* s_prefix) {
+  using C = EncCfg<DT>;
+  constexpr int PER = C::NCH / 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t loc[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = sum;
+    sum += s_cnt[lane * PER + q];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t count = __shfl_sync(kFullMask, incl, 31);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) s_off[lane * PER + q] = incl - sum + loc[q];
+  const bool head = ti.lt == 0 || (a.debug & 1);
+  if (lane == 0)
+    st_relaxed_u64(a.status + ti.t,
+                   make_status(a.epoch, head ? kFlagPrefix : kFlagAggregate, count));
+  uint32_t prefix = 0;
+  if (!head) {
+    prefix = warp_lookback(a.status, ti.t, (int64_t)ti.t - ti.lt, a.epoch);
+    if (lane == 0)
+      st_relaxed_u64(a.status + ti.t, make_status(a.epoch, kFlagPrefix, prefix + count));
+  }
+  if (lane == 0) {
+    if (ti.last) a.seg_nnz[ti.s] = (uint64_t)prefix + count;
+    *s_prefix = prefix;
+  }
+}
+
+// A consumer warp writes its own staged records of a resolved super-tile:
+// its slice holds its chunks (g, v) in order; records past the slice
+// capacity are re-derived from the kept masks and global memory.
+template <int DT>
+__device__ __forceinline__ void flush_slice(const EncodeArgs& a, const StageMeta& ti,
+                                            uint64_t prefix, const uint32_t* widx,
+                                            const typename Traits<DT>::T* wval,
+                                            const uint32_t* s_mask, const uint32_t* s_cnt,
+                                            const uint32_t* s_off, uint32_t run) {
+  using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
-  constexpr int VE = Tr::kVE;
-  constexpr uint32_t SUB = kThreads * kVPT * VE;
-  constexpr uint32_t WCAP = kStageCap / kWarps;
+  constexpr int VE = C::VE, NCW = C::NCW, CPW = C::CPW;
+  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, WCAP = C::WCAP;
+  constexpr uint32_t VMASK = (1u << VE) - 1u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const T* prevT = reinterpret_cast<const T*>(a.prev);
-  const T* nextT = reinterpret_cast<const T*>(a.next);
+  if (run == 0 || (a.debug & 2) || prefix >= ti.sg.cap) return;
+  const uint64_t e0 = (uint64_t)ti.lt * SUPER;
   T* out_val = reinterpret_cast<T*>(a.out_val);
-  for (int c = 0; c < kEncodeSubTiles * kVPT; ++c) {
-    const uint32_t ccnt = s_cnt[c * kWarps + w];
-    const uint32_t start = __shfl_sync(kFullMask, wstart_lane, c);
-    if (start + ccnt <= WCAP || ccnt == 0) continue;  // fully staged
-    const int g = c / kVPT, v = c % kVPT;
-    const uint32_t off = g * SUB + (uint32_t)(v * kThreads + w * 32 + lane) * VE;
-    uint32_t m = 0;
-    T ta[VE], tb[VE];
+  const int cl = lane < CPW ? lane : CPW - 1;
+  const uint32_t ccnt = lane < CPW ? s_cnt[cl * NCW + w] : 0u;
+  const uint32_t coff = s_off[cl * NCW + w];
+  uint32_t ci = ccnt;
 #pragma unroll
-    for (int e = 0; e < VE; ++e) {
-      const bool in = off + e < cnt;
-      ta[e] = in ? prevT[sg.base + e0 + off + e] : T(0);
-      tb[e] = in ? nextT[sg.base + e0 + off + e] : T(0);
-      if (in && Tr::changed(ta[e], tb[e])) m |= 1u << e;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFullMask, ci, o);
+    if (lane >= o) ci += y;
+  }
+  const uint32_t cstart = ci - ccnt;
+  const uint32_t staged = min(run, WCAP);
+  for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    int c = 0;  // owner chunk: the largest c with start(c) <= k
+#pragma unroll
+    for (int b = CPW / 2; b > 0; b >>= 1)
+      if (__shfl_sync(kFullMask, cstart, c + b) <= k) c += b;
+    const uint32_t st = __shfl_sync(kFullMask, cstart, c);
+    const uint32_t of = __shfl_sync(kFullMask, coff, c);
+    if (k < staged) {
+      const uint64_t pos = prefix + of + (k - st);
+      if (pos < ti.sg.cap) {
+        a.out_idx[ti.sg.rec + pos] = (uint32_t)(e0 + widx[k]);
+        out_val[ti.sg.rec + pos] = wval[k];
+      }
     }
-    uint32_t incl = __popc(m);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
-      if (lane >= o) incl += y;
-    }
-    uint32_t k = incl - __popc(m);
-    const uint64_t goff = prefix + s_off[c * kWarps + w];
-#pragma unroll
-    for (int e = 0; e < VE; ++e) {
-      if (m & (1u << e)) {
-        const uint64_t pos = goff + k;
-        if (start + k >= WCAP && pos < sg.cap) {
-          a.out_idx[sg.rec + pos] = (uint32_t)(e0 + off + e);
-          out_val[sg.rec + pos] = Tr::delta(ta[e], tb[e]);
+  }
+  if (run > WCAP) {  // spill (warp-uniform)
+    const T* prevT = reinterpret_cast<const T*>(a.prev);
+    const T* nextT = reinterpret_cast<const T*>(a.next);
+    for (int g = 0; g < (int)ti.nsub; ++g) {
+      const uint32_t m = s_mask[g * kEncConsumers + threadIdx.x];
+      for (int v = 0; v < (int)VPT; ++v) {
+        const int c = g * VPT + v;
+        uint32_t mv = (m >> (v * VE)) & VMASK;
+        uint32_t tot;
+        uint32_t r = warp_rank(mv, &tot);
+        const uint32_t st = __shfl_sync(kFullMask, cstart, c);
+        const uint32_t of = __shfl_sync(kFullMask, coff, c);
+        const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
+        while (mv) {
+          const int e = __ffs(mv) - 1;
+          mv &= mv - 1;
+          const uint64_t pos = prefix + of + r;
+          if (st + r >= WCAP && pos < ti.sg.cap) {
+            const uint64_t gi = ti.sg.base + e0 + li + e;
+            a.out_idx[ti.sg.rec + pos] = (uint32_t)(e0 + li + e);
+            out_val[ti.sg.rec + pos] = Tr::delta(prevT[gi], nextT[gi]);
+          }
+          ++r;
         }
-        ++k;
       }
     }
   }
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 4) encode_kernel(EncodeArgs a) {
+__global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
+  using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
-  constexpr int VE = Tr::kVE;
-  constexpr uint32_t SUB = kThreads * kVPT * VE;
-  constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  constexpr int NCH = kEncodeSubTiles * kVPT;  // chunks per warp per super-tile (32)
-  constexpr uint32_t WCAP = kStageCap / kWarps;
-  static_assert(NCH == 32, "one lane per chunk in the flush");
-  static_assert(NCH * kWarps == kThreads, "one thread per chunk in the block scan");
+  constexpr int VE = C::VE, NCW = C::NCW, NCH = C::NCH;
+  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, CAP = C::CAP, WCAP = C::WCAP;
+  constexpr uint32_t END = 0xffffffffu;
 
-  __shared__ unsigned long long s_warp[kWarps + 1];
-  __shared__ uint32_t s_tile[2];
-  __shared__ uint32_t s_prefix;
-  __shared__ uint32_t s_cnt[NCH * kWarps];   // chunk counts, index c * kWarps + w
-  __shared__ uint32_t s_off[NCH * kWarps];   // chunk offsets within the super-tile
-  __shared__ uint32_t s_idx[kStageCap];      // warp w stages at [w * WCAP, (w + 1) * WCAP)
-  __shared__ T s_val[kStageCap];
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* ring_prev = dsm;
+  uint8_t* ring_next = dsm + kRing * kStageBytes;
+  uint32_t* sb_idx = reinterpret_cast<uint32_t*>(dsm + C::kRingBytes);  // [2][CAP]
+  T* sb_val = reinterpret_cast<T*>(sb_idx + 2 * CAP);                   // [2][CAP]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(sb_val + 2 * CAP);     // [2][SUBT * consumers]
+  uint32_t* s_cnt = s_mask + 2 * kEncodeSubTiles * kEncConsumers;       // [2][NCH]
+  uint32_t* s_off = s_cnt + 2 * NCH;                                    // [2][NCH]
+  uint32_t* s_wrun = s_off + 2 * NCH;                                   // [2][NCW]
+  StageMeta* meta = reinterpret_cast<StageMeta*>(
+      (reinterpret_cast<uintptr_t>(s_wrun + 2 * NCW) + 15) & ~uintptr_t(15));  // [kRing]
+  StageMeta* tinfo = meta + kRing;                                      // [2]
+  unsigned long long* s_prefix = reinterpret_cast<unsigned long long*>(tinfo + 2);  // [2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + 2);           // [kRing]
+  uint64_t* empty = full + kRing;                                       // [kRing]
+  uint64_t* staged = empty + kRing;                                     // [2]
+  uint64_t* resolved = staged + 2;                                      // [2]
 
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) s_tile[0] = atomicAdd(a.ticket, 1u);
-  __syncthreads();
-  if (blockIdx.x == 0 && a.segs) {  // empty segments have no tile
-    for (int s = tid; s < a.nseg; s += kThreads)
-      if (a.segs[s].n == 0) a.seg_nnz[s] = 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int k = 0; k < kRing; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], NCW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&staged[b], NCW);
+      mbar_init(&resolved[b], 1);
+    }
+    mbar_fence_init();
   }
-  const uint4* prev4 = reinterpret_cast<const uint4*>(a.prev);
-  const uint4* next4 = reinterpret_cast<const uint4*>(a.next);
+  __syncthreads();
   const T* prevT = reinterpret_cast<const T*>(a.prev);
   const T* nextT = reinterpret_cast<const T*>(a.next);
-  T* out_val = reinterpret_cast<T*>(a.out_val);
-  uint32_t* w_idx = s_idx + w * WCAP;
-  T* w_val = s_val + w * WCAP;
 
-  for (int it = 0;; ++it) {
-    const uint32_t t = s_tile[it & 1];
-    if (t >= a.ntiles) break;
-    if (tid == 0) s_tile[(it + 1) & 1] = atomicAdd(a.ticket, 1u);
-
-    const int s = a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0;
-    const SegDev sg = a.segs ? a.segs[s] : a.seg0;
-    const uint32_t lt = a.tile0 ? t - __ldg(a.tile0 + s) : t;
-    const uint64_t e0 = (uint64_t)lt * SUPER;
-    const uint64_t rem_n = sg.n - e0;
-    const uint32_t cnt = rem_n < SUPER ? (uint32_t)rem_n : SUPER;
-    const bool last_tile = (a.tile0 ? __ldg(a.tile0 + s + 1) : a.ntiles) == t + 1;
-    const uint64_t vbase = (sg.base + e0) / VE;
-
-    // ---- phase 1: warp-local streaming, ranking and staging
-    uint32_t running = 0;  // records staged by this warp so far (warp-uniform)
-#pragma unroll 1
-    for (int g = 0; g < kEncodeSubTiles; ++g) {
-      const uint32_t g0 = g * SUB;
-      uint4 pa[kVPT], pb[kVPT];
-#pragma unroll
-      for (int v = 0; v < kVPT; ++v) {
-        const uint32_t off = g0 + (uint32_t)(v * kThreads + tid) * VE;
-        if (off + VE <= cnt) {
-          pa[v] = ld_stream(prev4 + vbase + off / VE);
-          pb[v] = ld_stream(next4 + vbase + off / VE);
-        } else {
-          pa[v] = make_uint4(0, 0, 0, 0);
-          pb[v] = make_uint4(0, 0, 0, 0);
-          if (off < cnt) {  // ragged tail
-            T ta[VE], tb[VE];
-#pragma unroll
-            for (int e = 0; e < VE; ++e) {
-              ta[e] = off + e < cnt ? prevT[sg.base + e0 + off + e] : T(0);
-              tb[e] = off + e < cnt ? nextT[sg.base + e0 + off + e] : T(0);
-            }
-            memcpy(&pa[v], ta, 16);
-            memcpy(&pb[v], tb, 16);
+  if (warp == NCW) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      uint32_t ebits = (1u << kRing) - 1u;  // the first wait on each empty barrier passes
+      int k = 0;
+      while (true) {
+        const uint32_t t = atomicAdd(a.ticket, 1u);
+        if (t >= a.ntiles) {
+          mbar_wait(&empty[k], (ebits >> k) & 1u);
+          meta[k].t = END;
+          mbar_arrive(&full[k]);
+          break;
+        }
+        const int s = a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0;
+        const SegDev sg = a.segs ? a.segs[s] : a.seg0;
+        const uint32_t lt = a.tile0 ? t - __ldg(a.tile0 + s) : t;
+        const uint64_t e0 = (uint64_t)lt * SUPER;
+        const uint64_t rem_n = sg.n - e0;
+        const uint32_t cnt = rem_n < SUPER ? (uint32_t)rem_n : SUPER;
+        const uint32_t nsub = (cnt + SUB - 1) / SUB;
+        const uint32_t last = (a.tile0 ? __ldg(a.tile0 + s + 1) : a.ntiles) == t + 1;
+        for (uint32_t g = 0; g < nsub; ++g) {
+          mbar_wait(&empty[k], (ebits >> k) & 1u);
+          ebits ^= 1u << k;
+          StageMeta& m = meta[k];
+          m.sg = sg;
+          m.t = t;
+          m.s = (uint32_t)s;
+          m.lt = lt;
+          m.nsub = nsub;
+          m.cnt = cnt;
+          m.last = last;
+          const uint32_t sub_cnt = min(SUB, cnt - g * SUB);
+          const uint32_t bytes = (sub_cnt / VE) * 16u;
+          mbar_arrive_expect_tx(&full[k], 2 * bytes);
+          if (bytes) {
+            const uint64_t el = sg.base + e0 + (uint64_t)g * SUB;
+            tma_load_1d(ring_prev + k * kStageBytes, prevT + el, bytes, &full[k]);
+            tma_load_1d(ring_next + k * kStageBytes, nextT + el, bytes, &full[k]);
           }
+          k = (k + 1) % kRing;
         }
       }
+    }
+    return;
+  }
+
+  if (warp > NCW) {
+    // ---------------- resolvers: warp NCW+1+b owns staging buffer b ----------------
+    const int b = warp - NCW - 1;
+    uint32_t par = 0;
+    while (true) {
+      mbar_wait(&staged[b], par);
+      par ^= 1u;
+      const StageMeta ti = tinfo[b];
+      if (ti.t == END) break;
+      resolve_tile<DT>(a, ti, s_cnt + b * NCH, s_off + b * NCH, &s_prefix[b]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&resolved[b]);
+    }
+    return;
+  }
+
+  // ---------------- consumers (warps 0..15) ----------------
+  if (blockIdx.x == 0 && a.segs) {  // empty segments have no tile
+    for (int s = tid; s < a.nseg; s += kEncConsumers)
+      if (a.segs[s].n == 0) a.seg_nnz[s] = 0;
+  }
+  uint32_t fbits = 0, rbits = 0;
+  int k = 0;
+  StageMeta prev_ti{};
+  uint32_t prev_run = 0;
+  bool have_prev = false;
+  uint32_t i = 0;
+  for (;; ++i) {
+    const int b = (int)(i & 1u);
+    mbar_wait(&full[k], (fbits >> k) & 1u);
+    if (meta[k].t == END) break;
+    const StageMeta ti = meta[k];
+    const uint64_t e0 = (uint64_t)ti.lt * SUPER;
+    uint32_t* widx = sb_idx + b * CAP + warp * WCAP;
+    T* wval = sb_val + b * CAP + warp * WCAP;
+    uint32_t* cnt_b = s_cnt + b * NCH;
+    uint32_t running = 0;  // records of this warp in this super-tile (warp-uniform)
+#pragma unroll 1
+    for (int g = 0; g < kEncodeSubTiles; ++g) {
+      if ((uint32_t)g >= ti.nsub) {
+        if (lane < (int)VPT) cnt_b[(g * VPT + lane) * NCW + warp] = 0;
+        continue;
+      }
+      const int kk = (k + g) % kRing;
+      if (g > 0) mbar_wait(&full[kk], (fbits >> kk) & 1u);
+      fbits ^= 1u << kk;
+      const uint32_t sub_cnt = min(SUB, ti.cnt - g * SUB);
+      const uint32_t nvec = sub_cnt / VE;
+      const uint4* P = reinterpret_cast<const uint4*>(ring_prev + kk * kStageBytes);
+      const uint4* N = reinterpret_cast<const uint4*>(ring_next + kk * kStageBytes);
+      uint32_t m = 0;
 #pragma unroll
-      for (int v = 0; v < kVPT; ++v) {
-        const uint32_t m = change_mask<DT>(pa[v], pb[v]);
-        uint32_t incl = __popc(m);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t tot = __shfl_sync(kFullMask, incl, 31);
-        if (lane == 0) s_cnt[(g * kVPT + v) * kWarps + w] = tot;
-        if (m) {
-          uint32_t k = running + incl - __popc(m);
-          const uint32_t off = g0 + (uint32_t)(v * kThreads + tid) * VE;
-#pragma unroll
+      for (uint32_t v = 0; v < VPT; ++v) {
+        const uint32_t j = v * kEncConsumers + tid;
+        uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
+        uint32_t mv = 0;
+        if (j < nvec) {
+          pa = P[j];
+          pb = N[j];
+          if ((pa.x ^ pb.x) | (pa.y ^ pb.y) | (pa.z ^ pb.z) | (pa.w ^ pb.w) || DT == WS_F32)
+            mv = change_mask<DT>(pa, pb);
+        } else if (j == nvec && (sub_cnt % VE)) {  // ragged tail from global memory
+          const uint64_t el = ti.sg.base + e0 + (uint64_t)g * SUB + j * VE;
+          T ta[VE], tb[VE];
           for (int e = 0; e < VE; ++e) {
-            if (m & (1u << e)) {
-              if (k < WCAP) {
-                w_idx[k] = off + e;
-                w_val[k] = Tr::delta(Tr::get(pa[v], e), Tr::get(pb[v], e));
-              }
-              ++k;
-            }
+            const bool in = (uint32_t)e < sub_cnt % VE;
+            ta[e] = in ? prevT[el + e] : T(0);
+            tb[e] = in ? nextT[el + e] : T(0);
+            if (in && Tr::changed(ta[e], tb[e])) mv |= 1u << e;
           }
+          memcpy(&pa, ta, 16);
+          memcpy(&pb, tb, 16);
+        }
+        m |= mv << (v * VE);
+        uint32_t tot;
+        uint32_t local = running + warp_rank(mv, &tot);
+        if (lane == 0) cnt_b[(g * VPT + v) * NCW + warp] = tot;
+        const uint32_t li = g * SUB + j * VE;
+        while (mv && local < WCAP) {
+          const int e = __ffs(mv) - 1;
+          mv &= mv - 1;
+          widx[local] = li + e;
+          wval[local] = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+          ++local;
         }
         running += tot;
       }
+      s_mask[(b * kEncodeSubTiles + g) * kEncConsumers + tid] = m;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
     }
-    __syncthreads();
+    k = (k + ti.nsub) % kRing;
+    if (tid == 0) tinfo[b] = ti;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&staged[b]);
 
-    // ---- phase 2: chunk offsets (block scan) + look-back for the super-tile
-    unsigned long long total;
-    const uint32_t my_cnt = s_cnt[tid];
-    s_off[tid] = (uint32_t)block_scan_packed(my_cnt, s_warp, &total);
-    const uint32_t tile_count = (uint32_t)total;
-    if (w == 0) {
-      uint32_t prefix = 0;
-      if (lt == 0 || (a.debug & 1)) {
-        if (tid == 0) st_relaxed_u64(a.status + t, make_status(a.epoch, kFlagPrefix, tile_count));
-      } else {
-        if (tid == 0) st_relaxed_u64(a.status + t, make_status(a.epoch, kFlagAggregate, tile_count));
-        prefix = warp_lookback(a.status, t, (int64_t)t - lt, a.epoch);
-        if (tid == 0)
-          st_relaxed_u64(a.status + t, make_status(a.epoch, kFlagPrefix, prefix + tile_count));
-      }
-      if (tid == 0) {
-        s_prefix = prefix;
-        if (last_tile) a.seg_nnz[s] = (uint64_t)prefix + tile_count;
-      }
+    // ---- write out the previous super-tile's records (resolved meanwhile)
+    if (have_prev) {
+      const int pb = b ^ 1;
+      mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
+      rbits ^= 1u << pb;
+      flush_slice<DT>(a, prev_ti, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
+                      sb_val + pb * CAP + warp * WCAP, s_mask + pb * kEncodeSubTiles * kEncConsumers,
+                      s_cnt + pb * NCH, s_off + pb * NCH, prev_run);
     }
-    __syncthreads();
-    const uint64_t prefix = s_prefix;
-
-    // ---- phase 3: flush this warp's staged records (lane c owns chunk c)
-    const uint32_t ccnt = s_cnt[lane * kWarps + w];
-    uint32_t wincl = ccnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFullMask, wincl, o);
-      if (lane >= o) wincl += y;
-    }
-    const uint32_t wstart = wincl - ccnt;  // chunk's first slot in the warp's staging
-    const uint32_t staged = min(running, WCAP);
-    if (!(a.debug & 2)) {
-      for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        // owner chunk of staged record k: the largest c with start(c) <= k
-        // (starts are non-decreasing; an empty chunk shares its successor's)
-        int c = 0;
-#pragma unroll
-        for (int b = 16; b > 0; b >>= 1)
-          if (__shfl_sync(kFullMask, wstart, c + b) <= k) c += b;
-        const uint32_t cstart = __shfl_sync(kFullMask, wstart, c);
-        if (k < staged) {
-          const uint64_t pos = prefix + s_off[c * kWarps + w] + (k - cstart);
-          if (pos < sg.cap) {
-            a.out_idx[sg.rec + pos] = (uint32_t)(e0 + w_idx[k]);
-            out_val[sg.rec + pos] = w_val[k];
-          }
-        }
-      }
-    }
-    if (running > WCAP && !(a.debug & 2))
-      encode_overflow<DT>(a, sg, e0, cnt, prefix, s_cnt, s_off, wstart);
-    __syncthreads();  // staging, s_cnt and s_prefix are reused by the next super-tile
+    prev_ti = ti;
+    prev_run = running;
+    have_prev = true;
   }
+  // ---- drain: flush the last super-tile, then stop both resolvers
+  const int b = (int)(i & 1u);
+  if (tid == 0) tinfo[b].t = END;  // resolver b has finished super-tile i-2
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&staged[b]);
+  if (have_prev) {
+    const int pb = b ^ 1;
+    mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
+    flush_slice<DT>(a, prev_ti, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
+                    sb_val + pb * CAP + warp * WCAP, s_mask + pb * kEncodeSubTiles * kEncConsumers,
+                    s_cnt + pb * NCH, s_off + pb * NCH, prev_run);
+  }
+  named_barrier(1, kEncConsumers);  // every warp is past its use of tinfo[b ^ 1]
+  if (tid == 0) tinfo[b ^ 1].t = END;
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&staged[b ^ 1]);
 }
 
 // ---- apply (codec.cpp:65-92) ---------------------------------------------------
@@ -465,24 +641,30 @@ int sm_count() {
 }
 
 cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out) {
-  int grid = 0;
-  switch (dtype) {
-    case WS_BF16: grid = occupancy_grid(encode_kernel<WS_BF16>, kThreads); break;
-    case WS_I32: grid = occupancy_grid(encode_kernel<WS_I32>, kThreads); break;
-    case WS_F32: grid = occupancy_grid(encode_kernel<WS_F32>, kThreads); break;
-    default: return cudaErrorInvalidValue;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(encode_kernel<WS_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)EncCfg<WS_BF16>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)EncCfg<WS_I32>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)EncCfg<WS_F32>::kSmem);
+    attr_done = true;
   }
-  grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)grid, std::max(a.ntiles, 1u)));
+  // one persistent block per SM; the producer warp claims super-tiles in order
+  int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(),
+                                                           std::max(a.ntiles, 1u)));
   if (const char* g = getenv("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
+  if (grid_out) *grid_out = grid;
   EncodeArgs a2 = a;
   if (const char* d = getenv("WSYNC_ENCODE_DEBUG")) a2.debug = (uint32_t)atoi(d);
-  if (grid_out) *grid_out = grid;
   cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   switch (dtype) {
-    case WS_BF16: encode_kernel<WS_BF16><<<grid, kThreads, 0, s>>>(a2); break;
-    case WS_I32: encode_kernel<WS_I32><<<grid, kThreads, 0, s>>>(a2); break;
-    default: encode_kernel<WS_F32><<<grid, kThreads, 0, s>>>(a2); break;
+    case WS_BF16: encode_kernel<WS_BF16><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2); break;
+    case WS_I32: encode_kernel<WS_I32><<<grid, kEncodeBlock, EncCfg<WS_I32>::kSmem, s>>>(a2); break;
+    case WS_F32: encode_kernel<WS_F32><<<grid, kEncodeBlock, EncCfg<WS_F32>::kSmem, s>>>(a2); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
