@@ -17,10 +17,14 @@ namespace wsync {
 #ifndef WS_ENC_CONSUMERS
 #define WS_ENC_CONSUMERS 512
 #endif
+#ifndef WS_ENC_BUFFERS
+#define WS_ENC_BUFFERS 3
+#endif
 constexpr int kEncodeThreads = 256;                 // block size of the small codec kernels
 constexpr int kEncodeVPT = 4;                       // their vectors per thread
 constexpr int kEncConsumers = WS_ENC_CONSUMERS;     // K1 consumer threads (16 warps)
-constexpr int kEncodeBlock = kEncConsumers + 3 * 32;  // + TMA producer + 2 resolver warps
+constexpr int kEncBuffers = WS_ENC_BUFFERS;         // record staging buffers (one resolver each)
+constexpr int kEncodeBlock = kEncConsumers + 32 + kEncBuffers * 32;  // + producer + resolvers
 constexpr int kEncodeSubTiles = WS_ENC_SUBTILES;    // sub-tiles (ring stages) per super-tile
 constexpr int kRing = WS_ENC_RING;                  // shared-memory ring stages
 constexpr uint32_t kStageBytes = 16384;             // per array per stage

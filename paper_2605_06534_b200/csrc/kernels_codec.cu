@@ -94,15 +94,17 @@ struct EncCfg {
   static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  static constexpr uint32_t CAP = SUPER / 4;                          // staged records per buffer
+  static constexpr uint32_t CAP = SUPER / 8;                          // staged records per buffer
   static constexpr uint32_t WCAP = CAP / NCW;
   static constexpr int NCH = kEncodeSubTiles * VPT * NCW;             // chunks per super-tile
   static constexpr int CPW = kEncodeSubTiles * VPT;                   // chunks per consumer warp
   static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
-  static constexpr size_t kSmem = kRingBytes + 2 * (size_t)CAP * (4 + sizeof(T)) +
-                                  2 * (size_t)kEncodeSubTiles * kEncConsumers * 4 +  // masks
-                                  2 * NCH * 4 * 2 + 2 * NCW * 4 +                    // cnt/off/wrun
-                                  (kRing + 2) * sizeof(StageMeta) + 32 + 16 + (2 * kRing + 4) * 8;
+  static constexpr int NB = kEncBuffers;                              // staging buffers
+  static constexpr size_t kSmem = kRingBytes + NB * (size_t)CAP * (4 + sizeof(T)) +
+                                  NB * (size_t)kEncodeSubTiles * kEncConsumers * 4 +  // masks
+                                  NB * NCH * 4 * 2 + NB * NCW * 4 +                   // cnt/off/wrun
+                                  (kRing + NB) * sizeof(StageMeta) + 16 + NB * 8 +
+                                  (2 * kRing + 2 * NB) * 8;
   static_assert(NCH % 32 == 0, "chunks per lane");
   static_assert(CPW <= 32 && (CPW & (CPW - 1)) == 0, "chunk search over lanes");
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
@@ -174,12 +176,19 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
 // A consumer warp writes its own staged records of a resolved super-tile:
 // its slice holds its chunks (g, v) in order; records past the slice
 // capacity are re-derived from the kept masks and global memory.
+// What a consumer warp keeps (in registers) about a staged super-tile until
+// it writes the records out.
+struct PendingSlice {
+  uint64_t base, rec, cap;
+  uint32_t lt, nsub, run;
+};
+
 template <int DT>
-__device__ __forceinline__ void flush_slice(const EncodeArgs& a, const StageMeta& ti,
+__device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
                                             uint64_t prefix, const uint32_t* widx,
                                             const typename Traits<DT>::T* wval,
                                             const uint32_t* s_mask, const uint32_t* s_cnt,
-                                            const uint32_t* s_off, uint32_t run) {
+                                            const uint32_t* s_off) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
@@ -187,7 +196,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const StageMeta
   constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, WCAP = C::WCAP;
   constexpr uint32_t VMASK = (1u << VE) - 1u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (run == 0 || (a.debug & 2) || prefix >= ti.sg.cap) return;
+  const uint32_t run = ti.run;
+  if (run == 0 || (a.debug & 2) || prefix >= ti.cap) return;
   const uint64_t e0 = (uint64_t)ti.lt * SUPER;
   T* out_val = reinterpret_cast<T*>(a.out_val);
   const int cl = lane < CPW ? lane : CPW - 1;
@@ -211,9 +221,9 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const StageMeta
     const uint32_t of = __shfl_sync(kFullMask, coff, c);
     if (k < staged) {
       const uint64_t pos = prefix + of + (k - st);
-      if (pos < ti.sg.cap) {
-        a.out_idx[ti.sg.rec + pos] = (uint32_t)(e0 + widx[k]);
-        out_val[ti.sg.rec + pos] = wval[k];
+      if (pos < ti.cap) {
+        a.out_idx[ti.rec + pos] = (uint32_t)(e0 + widx[k]);
+        out_val[ti.rec + pos] = wval[k];
       }
     }
   }
@@ -234,10 +244,10 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const StageMeta
           const int e = __ffs(mv) - 1;
           mv &= mv - 1;
           const uint64_t pos = prefix + of + r;
-          if (st + r >= WCAP && pos < ti.sg.cap) {
-            const uint64_t gi = ti.sg.base + e0 + li + e;
-            a.out_idx[ti.sg.rec + pos] = (uint32_t)(e0 + li + e);
-            out_val[ti.sg.rec + pos] = Tr::delta(prevT[gi], nextT[gi]);
+          if (st + r >= WCAP && pos < ti.cap) {
+            const uint64_t gi = ti.base + e0 + li + e;
+            a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
+            out_val[ti.rec + pos] = Tr::delta(prevT[gi], nextT[gi]);
           }
           ++r;
         }
@@ -251,27 +261,28 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
-  constexpr int VE = C::VE, NCW = C::NCW, NCH = C::NCH;
+  constexpr int VE = C::VE, NCW = C::NCW, NCH = C::NCH, NB = C::NB;
   constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, CAP = C::CAP, WCAP = C::WCAP;
   constexpr uint32_t END = 0xffffffffu;
+  constexpr int MSZ = kEncodeSubTiles * kEncConsumers;  // mask words per buffer
 
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring_prev = dsm;
   uint8_t* ring_next = dsm + kRing * kStageBytes;
-  uint32_t* sb_idx = reinterpret_cast<uint32_t*>(dsm + C::kRingBytes);  // [2][CAP]
-  T* sb_val = reinterpret_cast<T*>(sb_idx + 2 * CAP);                   // [2][CAP]
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(sb_val + 2 * CAP);     // [2][SUBT * consumers]
-  uint32_t* s_cnt = s_mask + 2 * kEncodeSubTiles * kEncConsumers;       // [2][NCH]
-  uint32_t* s_off = s_cnt + 2 * NCH;                                    // [2][NCH]
-  uint32_t* s_wrun = s_off + 2 * NCH;                                   // [2][NCW]
+  uint32_t* sb_idx = reinterpret_cast<uint32_t*>(dsm + C::kRingBytes);  // [NB][CAP]
+  T* sb_val = reinterpret_cast<T*>(sb_idx + NB * CAP);                  // [NB][CAP]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(sb_val + NB * CAP);    // [NB][MSZ]
+  uint32_t* s_cnt = s_mask + NB * MSZ;                                  // [NB][NCH]
+  uint32_t* s_off = s_cnt + NB * NCH;                                   // [NB][NCH]
+  uint32_t* s_wrun = s_off + NB * NCH;                                  // [NB][NCW]
   StageMeta* meta = reinterpret_cast<StageMeta*>(
-      (reinterpret_cast<uintptr_t>(s_wrun + 2 * NCW) + 15) & ~uintptr_t(15));  // [kRing]
-  StageMeta* tinfo = meta + kRing;                                      // [2]
-  unsigned long long* s_prefix = reinterpret_cast<unsigned long long*>(tinfo + 2);  // [2]
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + 2);           // [kRing]
+      (reinterpret_cast<uintptr_t>(s_wrun + NB * NCW) + 15) & ~uintptr_t(15));  // [kRing]
+  StageMeta* tinfo = meta + kRing;                                      // [NB]
+  unsigned long long* s_prefix = reinterpret_cast<unsigned long long*>(tinfo + NB);  // [NB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + NB);          // [kRing]
   uint64_t* empty = full + kRing;                                       // [kRing]
-  uint64_t* staged = empty + kRing;                                     // [2]
-  uint64_t* resolved = staged + 2;                                      // [2]
+  uint64_t* staged = empty + kRing;                                     // [NB]
+  uint64_t* resolved = staged + NB;                                     // [NB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -279,7 +290,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       mbar_init(&full[k], 1);
       mbar_init(&empty[k], NCW);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&staged[b], NCW);
       mbar_init(&resolved[b], 1);
     }
@@ -357,14 +368,22 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     for (int s = tid; s < a.nseg; s += kEncConsumers)
       if (a.segs[s].n == 0) a.seg_nnz[s] = 0;
   }
+  // Super-tile i is staged in buffer i % NB and written out after super-tile
+  // i + NB - 1 is staged, so its look-back has NB - 1 periods to complete.
+  static_assert(NB == 3, "two pending super-tiles are kept in registers");
+  auto flush_tile = [&](int pb, const PendingSlice& p, uint32_t& rbits) {
+    mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
+    rbits ^= 1u << pb;
+    flush_slice<DT>(a, p, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
+                    sb_val + pb * CAP + warp * WCAP, s_mask + pb * MSZ, s_cnt + pb * NCH,
+                    s_off + pb * NCH);
+  };
+  PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this warp
   uint32_t fbits = 0, rbits = 0;
   int k = 0;
-  StageMeta prev_ti{};
-  uint32_t prev_run = 0;
-  bool have_prev = false;
   uint32_t i = 0;
   for (;; ++i) {
-    const int b = (int)(i & 1u);
+    const int b = (int)(i % NB);
     mbar_wait(&full[k], (fbits >> k) & 1u);
     if (meta[k].t == END) break;
     const StageMeta ti = meta[k];
@@ -423,44 +442,27 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         }
         running += tot;
       }
-      s_mask[(b * kEncodeSubTiles + g) * kEncConsumers + tid] = m;
+      s_mask[b * MSZ + g * kEncConsumers + tid] = m;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
     }
     k = (k + ti.nsub) % kRing;
-    if (tid == 0) tinfo[b] = ti;
+    if (tid == 0) tinfo[b] = ti;  // for the resolver only
     __syncwarp();
     if (lane == 0) mbar_arrive(&staged[b]);
-
-    // ---- write out the previous super-tile's records (resolved meanwhile)
-    if (have_prev) {
-      const int pb = b ^ 1;
-      mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
-      rbits ^= 1u << pb;
-      flush_slice<DT>(a, prev_ti, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
-                      sb_val + pb * CAP + warp * WCAP, s_mask + pb * kEncodeSubTiles * kEncConsumers,
-                      s_cnt + pb * NCH, s_off + pb * NCH, prev_run);
-    }
-    prev_ti = ti;
-    prev_run = running;
-    have_prev = true;
+    if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);  // super-tile i-2
+    pend0 = pend1;
+    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, running};
   }
-  // ---- drain: flush the last super-tile, then stop both resolvers
-  const int b = (int)(i & 1u);
-  if (tid == 0) tinfo[b].t = END;  // resolver b has finished super-tile i-2
+  // ---- drain: write out the pending super-tiles, then stop the resolvers
+  if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);
+  if (i >= 1) flush_tile((int)((i - 1) % NB), pend1, rbits);
+  named_barrier(1, kEncConsumers);  // every warp is past its last use of tinfo
+  if (tid == 0)
+    for (int b = 0; b < NB; ++b) tinfo[b].t = END;
   __syncwarp();
-  if (lane == 0) mbar_arrive(&staged[b]);
-  if (have_prev) {
-    const int pb = b ^ 1;
-    mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
-    flush_slice<DT>(a, prev_ti, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
-                    sb_val + pb * CAP + warp * WCAP, s_mask + pb * kEncodeSubTiles * kEncConsumers,
-                    s_cnt + pb * NCH, s_off + pb * NCH, prev_run);
-  }
-  named_barrier(1, kEncConsumers);  // every warp is past its use of tinfo[b ^ 1]
-  if (tid == 0) tinfo[b ^ 1].t = END;
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&staged[b ^ 1]);
+  if (lane == 0)
+    for (int b = 0; b < NB; ++b) mbar_arrive(&staged[b]);
 }
 
 // ---- apply (codec.cpp:65-92) ---------------------------------------------------

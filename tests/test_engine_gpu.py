@@ -156,3 +156,66 @@ def test_matches_reference_engine(reference, dtype, density, sparse):
     for s, (p, desc, off, n) in enumerate(plan.serve_shards):
         want = st.serve(0, p, dtype)
         assert bits(eng.serve_view(s)).tobytes() == want.tobytes(), plan.manifest[p].name
+
+
+def _check_segment_on_device(eng, i):
+    """Size-independent properties of segment i's delta stream, checked with
+    plain torch ops: ascending unique indices, exactly the changed positions,
+    values = next - prev (u16 wrap)."""
+    prev = eng.segment_view(i, 0).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
+    nxt = eng.segment_view(i, 1).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
+    changed = torch.nonzero(prev != nxt).flatten()
+    delta, codec, nnz = eng.segment_delta(i)
+    assert nnz == changed.numel()
+    if codec != "S":
+        return 0
+    idx = delta.indices.to(torch.int64) & 0xFFFFFFFF
+    assert torch.equal(idx, changed)
+    want = (nxt[changed] - prev[changed]) & 0xFFFF
+    assert torch.equal(delta.values.to(torch.int32) & 0xFFFF, want)
+    return nnz
+
+
+@pytest.mark.parametrize("model,density", [("qwen2.5-0.5b", 0.01), ("qwen2.5-0.5b", 0.1)])
+def test_full_model_bf16(restatement, model, density):
+    """A whole model through the engine (many super-tiles per block, so warp
+    drift and the look-back are exercised), checked on the device, plus two
+    segments against the C oracle bit for bit."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.MODELS[model]())
+    eng.generate(seed=11, density=density)
+    rep = eng.sync_step()
+    torch.cuda.synchronize()
+    total = 0
+    for i in range(len(plan.segments)):
+        total += _check_segment_on_device(eng, i)
+        assert torch.equal(eng.serve_view(i).view(torch.int16), eng.segment_view(i, 1).view(torch.int16))
+    assert rep["nnz"] >= total
+    # the largest segment (the embedding) and a bias, bit for bit vs the oracle
+    sizes = [n for (_, _, _, n) in plan.segments]
+    for i in (sizes.index(max(sizes)), sizes.index(min(sizes))):
+        p, desc, off, n = plan.segments[i]
+        meta = plan.manifest[p]
+        pv, nx = restatement.gen_pair_bf16(11, meta.name, meta.shape, desc, density)
+        wi, wv = restatement.diff_shards(BF16, pv, nx)
+        delta, codec, nnz = eng.segment_delta(i)
+        assert codec == "S" and nnz == wi.size
+        assert delta.indices.cpu().numpy().view(np.uint32).tolist() == wi.tolist()
+        assert delta.values.cpu().numpy().view(np.uint16).tobytes() == wv.tobytes()
+    # the reverse sync restores prev everywhere
+    eng.sync_step(reverse=True)
+    for i in range(len(plan.segments)):
+        assert torch.equal(eng.serve_view(i).view(torch.int16), eng.segment_view(i, 0).view(torch.int16))
+
+
+def test_single_shard_many_tiles():
+    """ws_diff_shards on a 300M-element shard: device-checked properties."""
+    import paper_2605_06534_b200 as ws
+    n = 300_000_000 + 5  # ragged tail
+    prev, nxt = ws.gen_pair_bf16(4, "big", (n,), (-1, 0, 0), 0.02)
+    d = ws.diff_shards(prev, nxt)
+    p = prev.view(torch.int16).to(torch.int32) & 0xFFFF
+    q = nxt.view(torch.int16).to(torch.int32) & 0xFFFF
+    changed = torch.nonzero(p != q).flatten()
+    assert torch.equal(d.indices.to(torch.int64) & 0xFFFFFFFF, changed)
+    assert torch.equal(d.values.to(torch.int32) & 0xFFFF, (q[changed] - p[changed]) & 0xFFFF)
