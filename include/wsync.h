@@ -233,6 +233,12 @@ ws_status ws_plan_route(const ws_plan* plan, int i, int32_t* segment,
                         int32_t* coord, int32_t* num_dst_ranks,
                         uint64_t* overlap_elems);
 
+/* Worst-case exchange sizes of this rank in records: what it may send to
+ * each serving coordinate (tp*pp entries) and receive from each rank (world
+ * entries).  The engine allocates its NVLink buffers from these. */
+ws_status ws_plan_exchange_caps(const ws_plan* plan, uint64_t* send_cap_per_coord,
+                                uint64_t* recv_cap_per_rank);
+
 /* ------------------------------------------------------------------------ */
 /* Engine: one weight sync (TransferEngine::sync_step, engine.cpp:66-254)     */
 /* ------------------------------------------------------------------------ */

@@ -156,6 +156,7 @@ _SIGS = {
                              C.POINTER(_u64)], C.c_int),
     "ws_plan_route": ([_vp, C.c_int, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32),
                        C.POINTER(_u64)], C.c_int),
+    "ws_plan_exchange_caps": ([_vp, C.POINTER(_u64), C.POINTER(_u64)], C.c_int),
     "ws_nccl_unique_id": ([C.POINTER(C.c_uint8)], C.c_int),
     "ws_engine_create": ([_vp, C.c_int, C.POINTER(C.c_uint8), C.POINTER(_vp)], C.c_int),
     "ws_engine_destroy": ([_vp], None),

@@ -139,6 +139,16 @@ ws_status ws_plan_route(const ws_plan* plan, int i, int32_t* segment, int32_t* c
   return WS_OK;
 }
 
+ws_status ws_plan_exchange_caps(const ws_plan* plan, uint64_t* send_cap_per_coord,
+                                uint64_t* recv_cap_per_rank) {
+  if (!plan) return set_error(WS_INVALID_ARGUMENT, "ws_plan_exchange_caps: null plan");
+  std::vector<uint64_t> s, r;
+  exchange_caps(*plan->p, plan->p->rank(), &s, &r);
+  if (send_cap_per_coord) std::memcpy(send_cap_per_coord, s.data(), s.size() * 8);
+  if (recv_cap_per_rank) std::memcpy(recv_cap_per_rank, r.data(), r.size() * 8);
+  return WS_OK;
+}
+
 ws_status ws_engine_create(const ws_plan* plan, int device, const uint8_t* unique_id,
                            ws_engine** out) {
   if (!plan || !out) return set_error(WS_INVALID_ARGUMENT, "ws_engine_create: null argument");

@@ -77,4 +77,5 @@ struct ws_engine {
   struct Comm;
   Comm* comm_ = nullptr;
   uint64_t pulled_bytes_ = 0;
+  uint64_t pushed_wire_bytes_ = 0;
 };

@@ -1,24 +1,250 @@
-// exchange.cu -- cross-GPU route of the engine (K3 over NVLink).
+// exchange.cu -- the cross-GPU part of a sync (K3 over NVLink / NVSwitch).
+//
+// The reference moves every pushed shard through a relay: the pusher puts
+// encoded buckets (engine.cpp:136-148) and each puller fetches the shards its
+// serving rank needs (plan_pulls, engine.cpp:158-197), then reslices and
+// applies them (:209-218).  On one box the relay is replaced by one exchange
+// per sync:
+//   1. pack (kernels_route.cu): the records of every route to a serving
+//      coordinate held by another GPU are re-indexed into that coordinate's
+//      serving arena and appended to the coordinate's send region as
+//      self-describing wire records (set records for dense-fallback shards);
+//   2. the per-coordinate record counts are all-gathered (8 bytes per
+//      coordinate per rank), so every rank knows what it will receive;
+//   3. one grouped ncclSend/ncclRecv moves each region to every replica of
+//      its coordinate (the same region goes to all replicas);
+//   4. the receiver scatters the records into its serving arena in place.
+// Region and receive capacities are sized from the static plan for the
+// worst case (every element of every route sent dense), so no step can
+// overflow.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "capi_util.h"
 #include "engine.h"
 
 using namespace wsync;
 
-struct ws_engine::Comm {};
+#define WS_CUDA_TRY(expr, what)                          \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_status(_e, what); \
+  } while (0)
+
+#define WS_NCCL_TRY(expr, what)                                                          \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess)                                                               \
+      return set_error(WS_NCCL, std::string(what) + ": " + ncclGetErrorString(_r));      \
+  } while (0)
+
+struct ws_engine::Comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, coords = 1;
+  // remote routes (this rank as a sender)
+  LocalEntry* d_entries = nullptr;
+  int nentries = 0;
+  uint64_t* d_unit_off = nullptr;
+  std::vector<uint64_t> region_off, region_cap;  // per coordinate, records
+  uint64_t* d_region_off = nullptr;
+  uint64_t* d_region_cap = nullptr;
+  unsigned long long* d_region_cnt = nullptr;
+  uint64_t* d_allcnt = nullptr;                  // [world][coords]
+  uint64_t* h_allcnt = nullptr;                  // pinned copy
+  uint32_t* d_err = nullptr;
+  void* d_send = nullptr;
+  void* d_recv = nullptr;
+  uint64_t send_cap = 0, recv_cap = 0;           // records
+  std::vector<std::vector<int>> dests;           // per coordinate: receiving ranks != me
+
+  ~Comm() {
+    cudaFree(d_entries);
+    cudaFree(d_unit_off);
+    cudaFree(d_region_off);
+    cudaFree(d_region_cap);
+    cudaFree(d_region_cnt);
+    cudaFree(d_allcnt);
+    cudaFree(d_err);
+    cudaFree(d_send);
+    cudaFree(d_recv);
+    if (h_allcnt) cudaFreeHost(h_allcnt);
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+namespace wsync {
+
+// Static exchange sizes of rank `me` (records): send capacity per serving
+// coordinate and receive capacity from every other rank.
+void exchange_caps(const Plan& plan, int me, std::vector<uint64_t>* send_cap,
+                   std::vector<uint64_t>* recv_cap) {
+  const int C = plan.coords(), W = plan.world();
+  send_cap->assign(C, 0);
+  recv_cap->assign(W, 0);
+  const int my_coord = plan.coord_of_rank(me);
+  for (int r = 0; r < W; ++r) {
+    for (const Route& rt : plan.routes_of(r)) {
+      const bool remote_dest = plan.replicas() > 1 || rt.coord != plan.coord_of_rank(r);
+      if (!remote_dest) continue;  // only the sender itself holds that coordinate
+      if (r == me) (*send_cap)[rt.coord] += rt.overlap;
+      else if (rt.coord == my_coord) (*recv_cap)[r] += rt.overlap;
+    }
+  }
+}
+
+}  // namespace wsync
 
 ws_status ws_engine::init_comm(const uint8_t* unique_id) {
-  (void)unique_id;
-  if (plan_.world() > 1) return set_error(WS_INVALID_ARGUMENT, "multi-GPU exchange not built yet");
+  if (plan_.world() == 1) return WS_OK;
+  if (!unique_id) return set_error(WS_INVALID_ARGUMENT, "multi-GPU engine needs an NCCL unique id");
+  auto* c = new Comm;
+  comm_ = c;
+  c->world = plan_.world();
+  c->rank = plan_.rank();
+  c->coords = plan_.coords();
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  WS_NCCL_TRY(ncclCommInitRank(&c->comm, c->world, id, c->rank), "ncclCommInitRank");
+
+  // remote routes: every route whose coordinate has a replica other than me
+  const int me = plan_.rank(), my_coord = plan_.my_coord();
+  std::vector<LocalEntry> remote;
+  const auto& segs = plan_.segments();
+  for (const Route& r : plan_.routes()) {
+    if (plan_.replicas() == 1 && r.coord == my_coord) continue;
+    const ParamMeta& p = plan_.manifest()[r.dst.param];
+    LocalEntry e = make_local_entry(dtype_, p.shape.data(), (int)p.shape.size(), r.seg,
+                                    segs[r.seg].shard.d, r.dst.d, r.dst_offset);
+    e.coord = r.coord;
+    remote.push_back(e);
+  }
+  c->nentries = (int)remote.size();
+  WS_CUDA_TRY(cudaMalloc(&c->d_entries, std::max<size_t>(1, remote.size()) * sizeof(LocalEntry)),
+              "cudaMalloc");
+  if (!remote.empty())
+    WS_CUDA_TRY(cudaMemcpy(c->d_entries, remote.data(), remote.size() * sizeof(LocalEntry),
+                           cudaMemcpyHostToDevice),
+                "H2D");
+  WS_CUDA_TRY(cudaMalloc(&c->d_unit_off, (remote.size() + 1) * 8), "cudaMalloc");
+
+  std::vector<uint64_t> send_cap, recv_cap;
+  exchange_caps(plan_, me, &send_cap, &recv_cap);
+  c->region_off.assign(c->coords, 0);
+  c->region_cap = send_cap;
+  for (int k = 0; k < c->coords; ++k) {
+    c->region_off[k] = c->send_cap;
+    c->send_cap += send_cap[k];
+  }
+  for (auto v : recv_cap) c->recv_cap += v;
+  c->dests.assign(c->coords, {});
+  for (int g = 0; g < c->world; ++g)
+    if (g != me) c->dests[plan_.coord_of_rank(g)].push_back(g);
+
+  const size_t wb = wire_bytes(dtype_);
+  WS_CUDA_TRY(cudaMalloc(&c->d_send, std::max<uint64_t>(1, c->send_cap) * wb), "cudaMalloc send");
+  WS_CUDA_TRY(cudaMalloc(&c->d_recv, std::max<uint64_t>(1, c->recv_cap) * wb), "cudaMalloc recv");
+  WS_CUDA_TRY(cudaMalloc(&c->d_region_off, c->coords * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&c->d_region_cap, c->coords * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&c->d_region_cnt, c->coords * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&c->d_allcnt, (size_t)c->world * c->coords * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&c->d_err, 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMallocHost(&c->h_allcnt, (size_t)c->world * c->coords * 8), "cudaMallocHost");
+  WS_CUDA_TRY(cudaMemcpy(c->d_region_off, c->region_off.data(), c->coords * 8,
+                         cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMemcpy(c->d_region_cap, c->region_cap.data(), c->coords * 8,
+                         cudaMemcpyHostToDevice), "H2D");
   return WS_OK;
 }
 
-void ws_engine::destroy_comm() { delete comm_; comm_ = nullptr; }
+void ws_engine::destroy_comm() {
+  delete comm_;
+  comm_ = nullptr;
+}
 
-ws_status ws_engine::exchange(const ws_sync_options&, int, cudaStream_t, uint32_t*) {
-  return set_error(WS_INVALID_ARGUMENT, "multi-GPU exchange not built yet");
+ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStream_t s,
+                              uint32_t* launches) {
+  Comm* c = comm_;
+  if (!c) return set_error(WS_INVALID_ARGUMENT, "exchange without a communicator");
+  const size_t wb = wire_bytes(dtype_);
+  // 1. pack
+  WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
+  WS_CUDA_TRY(cudaMemsetAsync(c->d_err, 0, 4, s), "memset");
+  PackArgs pa{};
+  pa.r.entries = c->d_entries;
+  pa.r.nentries = c->nentries;
+  pa.r.sparse = o.sparse ? 1 : 0;
+  pa.r.seg_nnz = d_nnz_;
+  pa.r.seg_cap = d_cap_;
+  pa.r.seg_rec = d_rec_;
+  pa.r.seg_base = d_base_;
+  pa.r.rec_idx = d_idx_;
+  pa.r.rec_val = d_val_;
+  pa.r.train_next = arena[next_arena];
+  pa.r.serve = serve;
+  pa.r.unit_off = c->d_unit_off;
+  pa.send = c->d_send;
+  pa.region_off = c->d_region_off;
+  pa.region_cap = c->d_region_cap;
+  pa.region_cnt = c->d_region_cnt;
+  pa.err = c->d_err;
+  WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack");
+  if (c->nentries) *launches += 2;
+  // 2. counts
+  WS_NCCL_TRY(ncclAllGather(c->d_region_cnt, c->d_allcnt, c->coords, ncclUint64, c->comm, s),
+              "ncclAllGather");
+  WS_CUDA_TRY(cudaMemcpyAsync(c->h_allcnt, c->d_allcnt, (size_t)c->world * c->coords * 8,
+                              cudaMemcpyDeviceToHost, s),
+              "D2H counts");
+  uint32_t err = 0;
+  WS_CUDA_TRY(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
+  WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  if (err) return set_error(WS_CAPACITY, "exchange: send region overflow");
+  // 3. one grouped send/recv
+  const int me = c->rank, my_coord = plan_.my_coord();
+  uint64_t recv_total = 0, sent = 0;
+  WS_NCCL_TRY(ncclGroupStart(), "ncclGroupStart");
+  for (int k = 0; k < c->coords; ++k) {
+    const uint64_t n = c->h_allcnt[(size_t)me * c->coords + k];
+    if (!n) continue;
+    for (int g : c->dests[k]) {
+      WS_NCCL_TRY(ncclSend(static_cast<const char*>(c->d_send) + c->region_off[k] * wb, n * wb,
+                           ncclUint8, g, c->comm, s),
+                  "ncclSend");
+      sent += n * wb;
+    }
+  }
+  for (int g = 0; g < c->world; ++g) {
+    if (g == me) continue;
+    const uint64_t n = c->h_allcnt[(size_t)g * c->coords + my_coord];
+    if (!n) continue;
+    if (recv_total + n > c->recv_cap) {
+      ncclGroupEnd();
+      return set_error(WS_CAPACITY, "exchange: receive buffer overflow");
+    }
+    WS_NCCL_TRY(ncclRecv(static_cast<char*>(c->d_recv) + recv_total * wb, n * wb, ncclUint8, g,
+                         c->comm, s),
+                "ncclRecv");
+    recv_total += n;
+  }
+  WS_NCCL_TRY(ncclGroupEnd(), "ncclGroupEnd");
+  // 4. apply what arrived
+  WS_CUDA_TRY(launch_apply_wire(dtype_, c->d_recv, recv_total, serve, s), "apply wire");
+  if (recv_total) *launches += 1;
+  pulled_bytes_ = recv_total * wb;
+  pushed_wire_bytes_ = sent;
+  return WS_OK;
 }
 
 extern "C" ws_status ws_nccl_unique_id(uint8_t out[128]) {
-  (void)out;
-  return set_error(WS_NCCL, "NCCL not built yet");
+  ncclUniqueId id;
+  WS_NCCL_TRY(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  static_assert(sizeof(id) == 128, "NCCL unique id size");
+  std::memcpy(out, &id, sizeof(id));
+  return WS_OK;
 }
+
+
+

@@ -145,7 +145,145 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
   }
 }
 
+template <int DT>
+__global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  const RouteSideArgs& a = pa.r;
+  __shared__ int s_entry;
+  __shared__ uint64_t s_u0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t total = a.unit_off[a.nentries];
+  const T* val = reinterpret_cast<const T*>(a.rec_val);
+  const T* next = reinterpret_cast<const T*>(a.train_next);
+  for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const int e = find_entry(a.unit_off, a.nentries, u);
+      s_entry = e;
+      s_u0 = a.unit_off[e];
+    }
+    __syncthreads();
+    const LocalEntry& E = a.entries[s_entry];
+    const uint64_t lu = u - s_u0;
+    __syncthreads();
+    const int c = E.coord;
+    const uint64_t roff = pa.region_off[c], rcap = pa.region_cap[c];
+    // emits one record per lane with `valid`, reserving slots warp-wide
+    auto emit = [&](bool valid, uint64_t idx, T v, bool set) {
+      const unsigned bal = __ballot_sync(kFullMask, valid);
+      if (!bal) return;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(pa.region_cnt + c, (unsigned long long)__popc(bal));
+      base = __shfl_sync(kFullMask, base, 0);
+      if (!valid) return;
+      const uint64_t slot = base + __popc(bal & ((1u << lane) - 1u));
+      if (slot >= rcap) {
+        atomicOr(pa.err, WS_ERRBIT_CAPACITY);
+        return;
+      }
+      if constexpr (DT == WS_BF16) {
+        reinterpret_cast<uint64_t*>(pa.send)[roff + slot] =
+            (set ? kWireSet : 0ull) | (idx << 16) | (uint64_t)v;
+      } else {
+        ulonglong2 w;
+        w.x = (set ? kWireSet : 0ull) | idx;
+        w.y = (unsigned long long)v;
+        reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
+      }
+    };
+    if (!seg_dense(a, E.seg)) {
+      const uint64_t nnz = a.seg_nnz[E.seg];
+      const uint64_t k0 = lu * kApplyChunk;
+      const uint64_t k1 = min(nnz, k0 + kApplyChunk);
+      const uint64_t rec = a.seg_rec[E.seg];
+      for (uint64_t kb = k0 + (uint64_t)warp * 32; kb < k1; kb += (uint64_t)nwarps * 32) {
+        const uint64_t k = kb + lane;
+        bool valid = k < k1;
+        uint64_t d = 0;
+        T v = 0;
+        if (valid) {
+          const uint32_t i = __ldg(a.rec_idx + rec + k);
+          if (E.identity) {
+            valid = i >= E.keep_lo && i < E.keep_hi;
+            d = (uint64_t)((int64_t)i + E.shift);
+          } else {
+            d = remap_index(E.map, i);
+            valid = d != ~0ull;
+          }
+          v = __ldg(val + rec + k);
+        }
+        emit(valid, E.dst_base + d, v, false);
+      }
+    } else {
+      const BoxCopyArgs& B = E.box;
+      const uint64_t per_row = (B.run + kCopyChunk - 1) / kCopyChunk;
+      const uint64_t row = lu / per_row, c0 = (lu % per_row) * kCopyChunk;
+      const uint64_t c1 = min(B.run, c0 + kCopyChunk);
+      uint64_t so = B.src_base, dso = B.dst_base, rem = row;
+      for (int d = B.nd_outer - 1; d >= 0; --d) {
+        const uint64_t cc = rem % B.outer_ext[d];
+        rem /= B.outer_ext[d];
+        so += cc * B.src_stride[d];
+        dso += cc * B.dst_stride[d];
+      }
+      const T* src = next + a.seg_base[E.seg] + so;
+      for (uint64_t jb = c0 + (uint64_t)warp * 32; jb < c1; jb += (uint64_t)nwarps * 32) {
+        const uint64_t j = jb + lane;
+        const bool valid = j < c1;
+        emit(valid, E.dst_base + dso + j, valid ? src[j] : T(0), true);
+      }
+    }
+  }
+}
+
+template <int DT>
+__global__ void apply_wire_kernel(const void* recv, uint64_t nrec, typename Traits<DT>::T* serve) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nrec;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t key;
+    T v;
+    if constexpr (DT == WS_BF16) {
+      const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(recv) + k);
+      key = (w & kWireSet) | ((w & ~kWireSet) >> 16);
+      v = (T)(w & 0xffffu);
+    } else {
+      const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(recv) + k);
+      key = w.x;
+      v = (T)w.y;
+    }
+    const uint64_t i = key & ~kWireSet;
+    serve[i] = (key & kWireSet) ? v : Tr::add(serve[i], v);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s) {
+  if (a.r.nentries == 0) return cudaSuccess;
+  worklist_kernel<<<1, kWlThreads, 0, s>>>(a.r);
+  switch (dtype) {
+    case WS_BF16: pack_kernel<WS_BF16><<<grid, 256, 0, s>>>(a); break;
+    case WS_I32: pack_kernel<WS_I32><<<grid, 256, 0, s>>>(a); break;
+    case WS_F32: pack_kernel<WS_F32><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_wire(int dtype, const void* recv, uint64_t nrec, void* serve,
+                             cudaStream_t s) {
+  if (!nrec) return cudaSuccess;
+  const int grid = (int)std::min<uint64_t>((nrec + 255) / 256, 148ull * 16);
+  switch (dtype) {
+    case WS_BF16: apply_wire_kernel<WS_BF16><<<grid, 256, 0, s>>>(recv, nrec, (uint16_t*)serve); break;
+    case WS_I32: apply_wire_kernel<WS_I32><<<grid, 256, 0, s>>>(recv, nrec, (uint32_t*)serve); break;
+    case WS_F32: apply_wire_kernel<WS_F32><<<grid, 256, 0, s>>>(recv, nrec, (uint32_t*)serve); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_local_route(int dtype, const RouteSideArgs& a, int grid, cudaStream_t s) {
   if (a.nentries == 0) return cudaSuccess;

@@ -109,4 +109,10 @@ class Plan {
 
 constexpr uint64_t kArenaAlign = 64;  // elements; keeps 16-B vectors aligned for every dtype
 
+// Static exchange sizes of rank `me` in records (worst case: every routed
+// element sent): send capacity per serving coordinate, receive capacity
+// from every rank.  Defined in exchange.cu.
+void exchange_caps(const Plan& plan, int me, std::vector<uint64_t>* send_cap,
+                   std::vector<uint64_t>* recv_cap);
+
 }  // namespace wsync

@@ -15,6 +15,8 @@ constexpr uint64_t kCopyChunk = 65536;   // elements per dense-copy work unit
 struct LocalEntry {
   int32_t seg;
   int32_t identity;
+  int32_t coord;              // destination serving coordinate (pack region)
+  int32_t pad_;
   uint32_t keep_lo, keep_hi;  // identity: keep src-local i in [keep_lo, keep_hi)
   int64_t shift;              // identity: dst-local = i + shift
   uint64_t dst_base;          // serving shard offset (elements)
@@ -39,6 +41,33 @@ struct RouteSideArgs {
 
 // Work list + fused reslice/apply/dense-copy for the local routes.
 cudaError_t launch_local_route(int dtype, const RouteSideArgs& a, int grid, cudaStream_t s);
+
+// Wire records for the NVLink exchange: self-describing (serving-arena
+// index, value), so a receiver needs no route table and arrival order does
+// not matter.  bf16: one u64 = set:1 | index:47 | value:16.  4-byte dtypes:
+// {u64 set:1 | index:63, u32 value, u32 pad}.  "set" records carry dense-
+// fallback values (overwrite, copy_overlap semantics); the others are deltas.
+constexpr uint64_t kWireSet = 1ull << 63;
+inline size_t wire_bytes(int dtype) { return dtype == WS_BF16 ? 8 : 16; }
+
+// Packs the records of the routes to other GPUs into one region per serving
+// coordinate (warp-aggregated atomic reservation; order inside a region is
+// irrelevant).  Sparse segments are re-indexed (reslice) into the
+// destination shard; dense-fallback segments emit set records for the box
+// overlap.
+struct PackArgs {
+  RouteSideArgs r;                  // entries = the remote routes
+  void* send;
+  const uint64_t* region_off;       // per coordinate, in records
+  const uint64_t* region_cap;
+  unsigned long long* region_cnt;   // per coordinate, zeroed before the launch
+  uint32_t* err;                    // WS_ERRBIT_CAPACITY on overflow
+};
+cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s);
+
+// Receiver side: applies nrec wire records to the serving arena in place.
+cudaError_t launch_apply_wire(int dtype, const void* recv, uint64_t nrec, void* serve,
+                             cudaStream_t s);
 
 // Fills a LocalEntry for the route src -> dst of a tensor of `full`.
 LocalEntry make_local_entry(int dtype, const int64_t* full, int nd, int seg, const ws_shard& src,

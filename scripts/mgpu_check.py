@@ -1,0 +1,117 @@
+"""Multi-GPU parity check of the engine (one process per GPU, torchrun).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_check.py
+
+Every rank checks its own serving shards after each sync:
+  * bf16 FSDP-N -> TP2 x N/2 (cross-dim routes for RowLinear): serving ==
+    the generator's `next` values for that shard (regenerated on the device
+    from the global element index, so no rank needs another rank's data);
+    then a reverse sync restores `prev`; then the dense fallback (45%) and
+    sparse=False paths;
+  * I32 and F32 with the reference's own layouts (TrainConfig{N,1,1} ->
+    ServeConfig{N,1}): serving == the compiled reference engine's serving
+    shards (oracle/_ref, run on the same weights on the host).
+Prints one JSON line per rank; exits non-zero on any mismatch.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2605_06534_b200 as ws  # noqa: E402
+
+
+def serve_equals_gen(eng, plan, seed, density, which):
+    bad = []
+    for i, (p, desc, off, n) in enumerate(plan.serve_shards):
+        meta = plan.manifest[p]
+        pv, nx = ws.gen_pair_bf16(seed, meta.name, meta.shape, desc, density, device=eng.device)
+        want = (nx if which == "next" else pv).view(torch.int16)
+        if not torch.equal(eng.serve_view(i).view(torch.int16), want):
+            bad.append(meta.name)
+    return bad
+
+
+def bf16_case(rank, world, uid_fn, manifest, density, seed):
+    tp = 1 if world == 1 else 2
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+                   world=world, rank=rank)
+    eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
+    eng.generate(seed=seed, density=density)
+    rep = eng.sync_step()
+    bad = serve_equals_gen(eng, plan, seed, density, "next")
+    eng.sync_step(reverse=True)
+    bad += serve_equals_gen(eng, plan, seed, density, "prev")
+    eng.sync_step(sparse=False)
+    bad += serve_equals_gen(eng, plan, seed, density, "next")
+    return bad, rep
+
+
+def ref_case(rank, world, uid_fn, dtype, density, sparse):
+    from oracle.oracle import Reference
+    ref = Reference()
+    st = ref.toy_state(3, 64, 128, dtype, (world, 1, 1), (world, 1), density, 7)
+    st.run(mode_async=True, shard_aware=True, sparse=sparse, threshold=0.20, bucket_bytes=8192)
+    manifest = [ws.ParamMeta(n, k, tuple(s), l) for (n, k, s, l) in st.params]
+    plan = ws.Plan(manifest, dtype, ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1),
+                   world=world, rank=rank)
+    eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
+    td = {ws.I32: torch.int32, ws.F32: torch.float32}[dtype]
+    full = {i: (torch.from_numpy(st.weights(i, 0, dtype)).to(eng.device),
+                torch.from_numpy(st.weights(i, 1, dtype)).to(eng.device))
+            for i in range(len(manifest))}
+    for s, (p, desc, off, n) in enumerate(plan.segments):
+        shp = manifest[p].shape
+        eng.segment_view(s, 0).copy_(ws.extract_shard(full[p][0].view(shp).to(td), desc))
+        eng.segment_view(s, 1).copy_(ws.extract_shard(full[p][1].view(shp).to(td), desc))
+    for s, (p, desc, off, n) in enumerate(plan.serve_shards):
+        eng.serve_view(s).copy_(ws.extract_shard(full[p][0].view(manifest[p].shape).to(td), desc))
+    eng.sync_step(sparse=sparse)
+    bad = []
+    for s, (p, desc, off, n) in enumerate(plan.serve_shards):
+        want = st.serve(plan.info.serve_coord, p, dtype)
+        got = eng.serve_view(s).reshape(-1).cpu().numpy()
+        if got.tobytes() != want.tobytes():
+            bad.append(manifest[p].name)
+    return bad
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+
+    def uid():
+        if world == 1:
+            return None
+        obj = [ws.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    results = {}
+    ok = True
+    for name, manifest in (("toy", ws.toy_transformer_manifest(layers=3, hidden=64, vocab=256)),
+                           ("qwen2.5-0.5b[0,1,23]", ws.MODELS["qwen2.5-0.5b"]([0, 1, 23]))):
+        for density in (0.01, 0.45):
+            bad, rep = bf16_case(rank, world, uid, manifest, density, 3)
+            results[f"bf16 {name} d={density}"] = bad or "ok"
+            ok &= not bad
+    for dtype in (ws.I32, ws.F32):
+        for density, sparse in ((0.05, True), (0.45, True), (0.05, False)):
+            bad = ref_case(rank, world, uid, dtype, density, sparse)
+            results[f"ref dtype={dtype} d={density} sparse={sparse}"] = bad or "ok"
+            ok &= not bad
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    print(json.dumps({"rank": rank, "world": world, "ok": ok, "results": results}), flush=True)
+    dist.destroy_process_group()
+    return 0 if all(flags) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
