@@ -64,11 +64,12 @@ struct Traits<WS_F32> {
 template <int DT>
 __device__ __forceinline__ uint32_t change_mask(const uint4& a, const uint4& b) {
   if constexpr (DT == WS_BF16) {
-    const uint32_t x0 = a.x ^ b.x, x1 = a.y ^ b.y, x2 = a.z ^ b.z, x3 = a.w ^ b.w;
-    return ((x0 & 0xffffu) ? 1u : 0u) | ((x0 >> 16) ? 2u : 0u) |
-           ((x1 & 0xffffu) ? 4u : 0u) | ((x1 >> 16) ? 8u : 0u) |
-           ((x2 & 0xffffu) ? 16u : 0u) | ((x2 >> 16) ? 32u : 0u) |
-           ((x3 & 0xffffu) ? 64u : 0u) | ((x3 >> 16) ? 128u : 0u);
+    // SWAR: bit 15 / 31 of t is set iff the low / high halfword of a^b is
+    // nonzero; the eight flags are then gathered into bits 0..7.
+    auto nz = [](uint32_t x) { return (((x & 0x7fff7fffu) + 0x7fff7fffu) | x) & 0x80008000u; };
+    const uint32_t u = (nz(a.x ^ b.x) >> 15) | (nz(a.y ^ b.y) >> 13) | (nz(a.z ^ b.z) >> 11) |
+                       (nz(a.w ^ b.w) >> 9);
+    return (u | (u >> 15)) & 0xffu;
   } else {
     using Tr = Traits<DT>;
     return (Tr::changed(a.x, b.x) ? 1u : 0u) | (Tr::changed(a.y, b.y) ? 2u : 0u) |
@@ -114,16 +115,31 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
+// the phase completes (or ~0.5 ms passes) instead of re-issuing the probe.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 500000;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 // Global -> shared bulk copy completing on `bar` (bytes multiple of 16).
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,

@@ -94,14 +94,13 @@ struct EncCfg {
   static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  static constexpr uint32_t CAP = SUPER / 8;                          // staged records per buffer
+  static constexpr uint32_t CAP = SUPER * 3 / 16;                     // staged records per buffer (18.75%)
   static constexpr uint32_t WCAP = CAP / NCW;
   static constexpr int NCH = kEncodeSubTiles * VPT * NCW;             // chunks per super-tile
   static constexpr int CPW = kEncodeSubTiles * VPT;                   // chunks per consumer warp
   static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
   static constexpr int NB = kEncBuffers;                              // staging buffers
   static constexpr size_t kSmem = kRingBytes + NB * (size_t)CAP * (4 + sizeof(T)) +
-                                  NB * (size_t)kEncodeSubTiles * kEncConsumers * 4 +  // masks
                                   NB * NCH * 4 * 2 + NB * NCW * 4 +                   // cnt/off/wrun
                                   (kRing + NB) * sizeof(StageMeta) + 16 + NB * 8 +
                                   (2 * kRing + 2 * NB) * 8;
@@ -173,22 +172,21 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
   }
 }
 
-// A consumer warp writes its own staged records of a resolved super-tile:
-// its slice holds its chunks (g, v) in order; records past the slice
-// capacity are re-derived from the kept masks and global memory.
 // What a consumer warp keeps (in registers) about a staged super-tile until
 // it writes the records out.
 struct PendingSlice {
   uint64_t base, rec, cap;
-  uint32_t lt, nsub, run;
+  uint32_t lt, nsub, cnt, run;
 };
 
+// A consumer warp writes its own staged records of a resolved super-tile:
+// its slice holds its chunks (g, v) in order; records past the slice
+// capacity (super-tiles denser than 9.4%) are re-derived from global memory.
 template <int DT>
 __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
                                             uint64_t prefix, const uint32_t* widx,
                                             const typename Traits<DT>::T* wval,
-                                            const uint32_t* s_mask, const uint32_t* s_cnt,
-                                            const uint32_t* s_off) {
+                                            const uint32_t* s_cnt, const uint32_t* s_off) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
@@ -231,15 +229,18 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
     const T* prevT = reinterpret_cast<const T*>(a.prev);
     const T* nextT = reinterpret_cast<const T*>(a.next);
     for (int g = 0; g < (int)ti.nsub; ++g) {
-      const uint32_t m = s_mask[g * kEncConsumers + threadIdx.x];
       for (int v = 0; v < (int)VPT; ++v) {
         const int c = g * VPT + v;
-        uint32_t mv = (m >> (v * VE)) & VMASK;
+        const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
+        uint32_t mv = 0;
+        for (int e = 0; e < VE; ++e) {
+          const uint64_t gi = ti.base + e0 + li + e;
+          if (li + e < ti.cnt && Tr::changed(prevT[gi], nextT[gi])) mv |= 1u << e;
+        }
         uint32_t tot;
         uint32_t r = warp_rank(mv, &tot);
         const uint32_t st = __shfl_sync(kFullMask, cstart, c);
         const uint32_t of = __shfl_sync(kFullMask, coff, c);
-        const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
         while (mv) {
           const int e = __ffs(mv) - 1;
           mv &= mv - 1;
@@ -264,15 +265,14 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   constexpr int VE = C::VE, NCW = C::NCW, NCH = C::NCH, NB = C::NB;
   constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, CAP = C::CAP, WCAP = C::WCAP;
   constexpr uint32_t END = 0xffffffffu;
-  constexpr int MSZ = kEncodeSubTiles * kEncConsumers;  // mask words per buffer
 
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring_prev = dsm;
   uint8_t* ring_next = dsm + kRing * kStageBytes;
   uint32_t* sb_idx = reinterpret_cast<uint32_t*>(dsm + C::kRingBytes);  // [NB][CAP]
   T* sb_val = reinterpret_cast<T*>(sb_idx + NB * CAP);                  // [NB][CAP]
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(sb_val + NB * CAP);    // [NB][MSZ]
-  uint32_t* s_cnt = s_mask + NB * MSZ;                                  // [NB][NCH]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(sb_val + NB * CAP) + 3) & ~uintptr_t(3));  // [NB][NCH]
   uint32_t* s_off = s_cnt + NB * NCH;                                   // [NB][NCH]
   uint32_t* s_wrun = s_off + NB * NCH;                                  // [NB][NCW]
   StageMeta* meta = reinterpret_cast<StageMeta*>(
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     const int b = warp - NCW - 1;
     uint32_t par = 0;
     while (true) {
-      mbar_wait(&staged[b], par);
+      while (!mbar_try_wait(&staged[b], par)) __nanosleep(200);  // idle: keep issue slots free
       par ^= 1u;
       const StageMeta ti = tinfo[b];
       if (ti.t == END) break;
@@ -375,8 +375,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
     flush_slice<DT>(a, p, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
-                    sb_val + pb * CAP + warp * WCAP, s_mask + pb * MSZ, s_cnt + pb * NCH,
-                    s_off + pb * NCH);
+                    sb_val + pb * CAP + warp * WCAP, s_cnt + pb * NCH, s_off + pb * NCH);
   };
   PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this warp
   uint32_t fbits = 0, rbits = 0;
@@ -405,7 +404,6 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       const uint32_t nvec = sub_cnt / VE;
       const uint4* P = reinterpret_cast<const uint4*>(ring_prev + kk * kStageBytes);
       const uint4* N = reinterpret_cast<const uint4*>(ring_next + kk * kStageBytes);
-      uint32_t m = 0;
 #pragma unroll
       for (uint32_t v = 0; v < VPT; ++v) {
         const uint32_t j = v * kEncConsumers + tid;
@@ -428,21 +426,23 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           memcpy(&pa, ta, 16);
           memcpy(&pb, tb, 16);
         }
-        m |= mv << (v * VE);
         uint32_t tot;
         uint32_t local = running + warp_rank(mv, &tot);
         if (lane == 0) cnt_b[(g * VPT + v) * NCW + warp] = tot;
         const uint32_t li = g * SUB + j * VE;
+        const T* Pe = reinterpret_cast<const T*>(P) + (size_t)j * VE;
+        const T* Ne = reinterpret_cast<const T*>(N) + (size_t)j * VE;
         while (mv && local < WCAP) {
           const int e = __ffs(mv) - 1;
           mv &= mv - 1;
           widx[local] = li + e;
-          wval[local] = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+          // changed elements are sparse: read them back from the ring
+          wval[local] = j < nvec ? Tr::delta(Pe[e], Ne[e])
+                                 : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
           ++local;
         }
         running += tot;
       }
-      s_mask[b * MSZ + g * kEncConsumers + tid] = m;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
     }
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (lane == 0) mbar_arrive(&staged[b]);
     if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);  // super-tile i-2
     pend0 = pend1;
-    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, running};
+    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, running};
   }
   // ---- drain: write out the pending super-tiles, then stop the resolvers
   if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);
