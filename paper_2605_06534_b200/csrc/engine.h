@@ -41,6 +41,7 @@ struct ws_engine {
   // encode tables (device)
   wsync::SegDev* d_segs_ = nullptr;
   uint32_t* d_tile0_ = nullptr;
+  uint32_t* d_tile_seg_ = nullptr;
   unsigned long long* d_status_ = nullptr;
   unsigned int* d_ticket_ = nullptr;
   uint64_t* d_nnz_ = nullptr;
@@ -58,6 +59,8 @@ struct ws_engine {
 
   // local routes
   wsync::LocalEntry* d_local_ = nullptr;
+  wsync::FuseEntry* d_fuse_ = nullptr;
+  bool fuse_apply_ = true;  // K1 applies local sparse records (WSYNC_NO_FUSED_APPLY=1 disables)
   int nlocal_ = 0;
   uint64_t* d_unit_off_ = nullptr;
 

@@ -22,6 +22,7 @@ ws_engine::~ws_engine() {
   cudaSetDevice(device_);
   cudaFree(d_segs_);
   cudaFree(d_tile0_);
+  cudaFree(d_tile_seg_);
   cudaFree(d_status_);
   cudaFree(d_ticket_);
   cudaFree(d_nnz_);
@@ -31,6 +32,7 @@ ws_engine::~ws_engine() {
   cudaFree(d_idx_);
   cudaFree(d_val_);
   cudaFree(d_local_);
+  cudaFree(d_fuse_);
   cudaFree(d_unit_off_);
   if (h_nnz_pinned_) cudaFreeHost(h_nnz_pinned_);
   if (ring_) {
@@ -80,6 +82,14 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   WS_CUDA_TRY(cudaMalloc(&d_rec_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_base_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemcpy(d_tile0_, tile0.data(), (nseg_ + 1) * 4, cudaMemcpyHostToDevice), "H2D");
+  {  // segment of every super-tile: one load instead of a search in K1's producer
+    std::vector<uint32_t> tile_seg(std::max<uint32_t>(1, ntiles_));
+    for (int i = 0; i < nseg_; ++i)
+      for (uint32_t tt = tile0[i]; tt < tile0[i + 1]; ++tt) tile_seg[tt] = (uint32_t)i;
+    WS_CUDA_TRY(cudaMalloc(&d_tile_seg_, tile_seg.size() * 4), "cudaMalloc");
+    WS_CUDA_TRY(cudaMemcpy(d_tile_seg_, tile_seg.data(), tile_seg.size() * 4,
+                           cudaMemcpyHostToDevice), "H2D");
+  }
   if (nseg_)
     WS_CUDA_TRY(cudaMemcpy(d_base_, base.data(), nseg_ * 8, cudaMemcpyHostToDevice), "H2D");
   WS_CUDA_TRY(cudaMallocHost(&h_nnz_pinned_, ns * 8), "cudaMallocHost");
@@ -95,6 +105,23 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
                                      segs[r.seg].shard.d, r.dst.d, r.dst_offset));
   }
   nlocal_ = (int)local.size();
+  // Per-segment fused-apply entries for K1 (a segment feeds at most one
+  // serving shard of this GPU: one shard per parameter per coordinate).
+  std::vector<FuseEntry> fuse(std::max(1, nseg_));
+  for (auto& f : fuse) f = FuseEntry{};
+  for (const LocalEntry& e : local) {
+    FuseEntry& f = fuse[e.seg];
+    f.mode = e.identity ? 1 : 2;
+    f.keep_lo = e.keep_lo;
+    f.keep_hi = e.keep_hi;
+    f.shift = e.shift;
+    f.dst_base = e.dst_base;
+    f.map = e.map;
+  }
+  WS_CUDA_TRY(cudaMalloc(&d_fuse_, fuse.size() * sizeof(FuseEntry)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(d_fuse_, fuse.data(), fuse.size() * sizeof(FuseEntry),
+                         cudaMemcpyHostToDevice), "H2D");
+  if (const char* f = getenv("WSYNC_NO_FUSED_APPLY")) fuse_apply_ = atoi(f) == 0;
   WS_CUDA_TRY(cudaMalloc(&d_local_, std::max<size_t>(1, local.size()) * sizeof(LocalEntry)),
               "cudaMalloc");
   if (nlocal_)
@@ -203,6 +230,11 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     a.next = arena[na];
     a.segs = d_segs_;
     a.tile0 = d_tile0_;
+    a.tile_seg = d_tile_seg_;
+    if (fuse_apply_) {
+      a.fuse = d_fuse_;
+      a.serve = serve;
+    }
     a.nseg = nseg_;
     a.ntiles = ntiles_;
     a.out_idx = d_idx_;
@@ -228,6 +260,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   r.train_next = arena[na];
   r.serve = serve;
   r.unit_off = d_unit_off_;
+  r.fused = (fuse_apply_ && o.sparse && ntiles_) ? 1 : 0;
   WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
   if (nlocal_) launches += 2;
   WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");

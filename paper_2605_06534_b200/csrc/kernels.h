@@ -44,12 +44,25 @@ struct SegDev {
   uint64_t base, n, rec, cap;
 };
 
+// Fused apply of a segment's records into a serving shard resident on the
+// same GPU (K1 writes each record once; applying it at that moment removes
+// the separate read of the record stream).  mode 0: none, 1: flat shift with
+// a keep window (dim-0 layouts), 2: general box remap.
+struct FuseEntry {
+  int32_t mode;
+  uint32_t keep_lo, keep_hi;
+  int64_t shift;
+  uint64_t dst_base;
+  Remap map;
+};
+
 struct EncodeArgs {
   const void* prev;
   const void* next;
   const SegDev* segs;     // null: the single segment seg0
   SegDev seg0;
   const uint32_t* tile0;  // nseg + 1 prefix of per-segment tile counts (null with seg0)
+  const uint32_t* tile_seg;  // optional: segment of every super-tile (skips the search)
   int32_t nseg;
   uint32_t ntiles;
   uint32_t* out_idx;
@@ -59,6 +72,8 @@ struct EncodeArgs {
   uint32_t epoch;
   unsigned int* ticket;        // zeroed before launch
   uint32_t debug;              // perf experiments only (WSYNC_ENCODE_DEBUG): 1 no look-back, 2 no writes
+  const FuseEntry* fuse;       // optional, per segment: apply records to `serve` as they are written
+  void* serve;
 };
 
 // K1: fused compare + ballot/popc + block scan + decoupled look-back

@@ -176,8 +176,26 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
 // it writes the records out.
 struct PendingSlice {
   uint64_t base, rec, cap;
-  uint32_t lt, nsub, cnt, run;
+  uint32_t lt, nsub, cnt, run, seg;
 };
+
+// serve[dst(i)] += v for a record of a segment with a local serving shard
+// (codec.cpp:80-91 applied at the moment K1 writes the record).
+template <int DT>
+__device__ __forceinline__ void fuse_apply(const FuseEntry* __restrict__ f,
+                                           typename Traits<DT>::T* serve, uint32_t i,
+                                           typename Traits<DT>::T v) {
+  uint64_t d;
+  if (f->mode == 1) {
+    if (i < f->keep_lo || i >= f->keep_hi) return;
+    d = (uint64_t)((int64_t)i + f->shift);
+  } else {
+    d = remap_index(f->map, i);
+    if (d == ~0ull) return;
+  }
+  typename Traits<DT>::T* p = serve + f->dst_base + d;
+  *p = Traits<DT>::add(*p, v);
+}
 
 // A consumer warp writes its own staged records of a resolved super-tile:
 // its slice holds its chunks (g, v) in order; records past the slice
@@ -198,6 +216,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
   if (run == 0 || (a.debug & 2) || prefix >= ti.cap) return;
   const uint64_t e0 = (uint64_t)ti.lt * SUPER;
   T* out_val = reinterpret_cast<T*>(a.out_val);
+  const FuseEntry* fz = (a.fuse && a.fuse[ti.seg].mode) ? a.fuse + ti.seg : nullptr;
+  T* serve = reinterpret_cast<T*>(a.serve);
   const int cl = lane < CPW ? lane : CPW - 1;
   const uint32_t ccnt = lane < CPW ? s_cnt[cl * NCW + w] : 0u;
   const uint32_t coff = s_off[cl * NCW + w];
@@ -220,8 +240,11 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
     if (k < staged) {
       const uint64_t pos = prefix + of + (k - st);
       if (pos < ti.cap) {
-        a.out_idx[ti.rec + pos] = (uint32_t)(e0 + widx[k]);
-        out_val[ti.rec + pos] = wval[k];
+        const uint32_t i = (uint32_t)(e0 + widx[k]);
+        const T v = wval[k];
+        a.out_idx[ti.rec + pos] = i;
+        out_val[ti.rec + pos] = v;
+        if (fz) fuse_apply<DT>(fz, serve, i, v);
       }
     }
   }
@@ -247,8 +270,10 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
           const uint64_t pos = prefix + of + r;
           if (st + r >= WCAP && pos < ti.cap) {
             const uint64_t gi = ti.base + e0 + li + e;
+            const T v = Tr::delta(prevT[gi], nextT[gi]);
             a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
-            out_val[ti.rec + pos] = Tr::delta(prevT[gi], nextT[gi]);
+            out_val[ti.rec + pos] = v;
+            if (fz) fuse_apply<DT>(fz, serve, (uint32_t)(e0 + li + e), v);
           }
           ++r;
         }
@@ -306,6 +331,9 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       uint32_t ebits = (1u << kRing) - 1u;  // the first wait on each empty barrier passes
       int k = 0;
       while (true) {
+        // Claimed only when the ring can take it: claiming further ahead
+        // delays this super-tile's count and lengthens every look-back
+        // (measured: 4.29 -> 3.46 TB/s with one-ahead claiming).
         const uint32_t t = atomicAdd(a.ticket, 1u);
         if (t >= a.ntiles) {
           mbar_wait(&empty[k], (ebits >> k) & 1u);
@@ -313,7 +341,8 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           mbar_arrive(&full[k]);
           break;
         }
-        const int s = a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0;
+        const int s = a.tile_seg ? (int)__ldg(a.tile_seg + t)
+                                 : (a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0);
         const SegDev sg = a.segs ? a.segs[s] : a.seg0;
         const uint32_t lt = a.tile0 ? t - __ldg(a.tile0 + s) : t;
         const uint64_t e0 = (uint64_t)lt * SUPER;
@@ -452,7 +481,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (lane == 0) mbar_arrive(&staged[b]);
     if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);  // super-tile i-2
     pend0 = pend1;
-    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, running};
+    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, running, ti.s};
   }
   // ---- drain: write out the pending super-tiles, then stop the resolvers
   if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);

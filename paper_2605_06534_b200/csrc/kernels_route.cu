@@ -29,6 +29,7 @@ __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const Lo
     const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
     return e.box.rows * per_row;
   }
+  if (a.fused) return 0;  // K1 applied the sparse records as it wrote them
   const uint64_t nnz = a.seg_nnz[e.seg];
   return (nnz + kApplyChunk - 1) / kApplyChunk;
 }

@@ -28,6 +28,7 @@ struct RouteSideArgs {
   const LocalEntry* entries;
   int32_t nentries;
   int32_t sparse;               // 0: every segment dense (SyncOptions::sparse)
+  int32_t fused;                // 1: K1 already applied sparse records (dense copies only)
   const uint64_t* seg_nnz;
   const uint64_t* seg_cap;
   const uint64_t* seg_rec;
