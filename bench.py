@@ -274,7 +274,14 @@ def run_ours(args):
     enc_s = tim["encode_s"] / max(1, tim["steps"])
     train_elems = plan.info.train_elems
     nnz = probe["nnz"]
-    alg_bytes = 4 * train_elems + 6 * nnz  # read prev+next (2 B each), write idx u32 + val u16
+    # K1 reads prev+next (2 B each) and writes idx u32 + val u16 per change;
+    # with the fused apply it also read-modify-writes the 2-B serving element
+    # of every change routed to this GPU's own serving shard (4 B).
+    fused = os.environ.get("WSYNC_NO_FUSED_APPLY", "0") in ("", "0")
+    my_coord = plan.info.serve_coord
+    local_frac = (sum(ov for (_, c, _, ov) in plan.routes if c == my_coord) /
+                  max(1, train_elems))
+    alg_bytes = int(4 * train_elems + 6 * nnz + (4 * nnz * local_frac if fused else 0))
     peak, peak_src = load_peaks()
     achieved = alg_bytes / enc_s / 1e9 if enc_s > 0 else None
     traffic = None
