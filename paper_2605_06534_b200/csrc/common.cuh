@@ -154,6 +154,29 @@ __device__ __forceinline__ void named_barrier(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// ---- system-scope flags (peer GPUs over NVLink) -----------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Spins until *p >= want; false after ~`cycles` (a dead peer must not hang us).
+__device__ __forceinline__ bool wait_geq_sys(const unsigned long long* p, unsigned long long want,
+                                             long long cycles = 60ll * 2000000000ll) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < want) {
+    if (clock64() - t0 > cycles) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
 // ---- decoupled look-back status words ---------------------------------------
 // status = epoch(30b) << 34 | flag(2b) << 32 | value(32b).  A word whose epoch
 // differs from the launch's epoch is "not yet written"; the epoch advances

@@ -26,6 +26,10 @@ struct ws_engine {
  private:
   ws_status ensure_records(double threshold, int sparse);
   ws_status init_comm(const uint8_t* unique_id);  // exchange.cu
+  ws_status init_p2p(const std::vector<uint64_t>& send_full,
+                     const std::vector<uint64_t>& recv_full);
+  ws_status size_send(const std::vector<uint64_t>& region_cap);
+  ws_status size_recv(uint64_t records);
   void destroy_comm();
   ws_status exchange(const ws_sync_options& o, int next_arena, cudaStream_t s, uint32_t* launches);
   uint32_t next_epoch();

@@ -59,8 +59,17 @@ struct ws_engine::Comm {
   void* d_recv = nullptr;
   uint64_t send_cap = 0, recv_cap = 0;           // records
   std::vector<std::vector<int>> dests;           // per coordinate: receiving ranks != me
+  // peer-memory mode
+  bool p2p = false;
+  void* d_p2p = nullptr;                         // [mailbox | receive buffer] (IPC-exported)
+  std::vector<void*> peer;                       // mapped d_p2p of every rank (null: me)
+  P2PArgs pargs{};
+  uint32_t epoch = 0;
 
   ~Comm() {
+    for (void* p : peer)
+      if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(d_p2p);
     cudaFree(d_entries);
     cudaFree(d_unit_off);
     cudaFree(d_region_off);
@@ -130,32 +139,171 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
                 "H2D");
   WS_CUDA_TRY(cudaMalloc(&c->d_unit_off, (remote.size() + 1) * 8), "cudaMalloc");
 
-  std::vector<uint64_t> send_cap, recv_cap;
-  exchange_caps(plan_, me, &send_cap, &recv_cap);
-  c->region_off.assign(c->coords, 0);
-  c->region_cap = send_cap;
-  for (int k = 0; k < c->coords; ++k) {
-    c->region_off[k] = c->send_cap;
-    c->send_cap += send_cap[k];
-  }
-  for (auto v : recv_cap) c->recv_cap += v;
+  // Buffers start at a fraction of the worst case (every routed element sent
+  // dense) and grow on demand: the all-gathered counts tell every rank what
+  // it must send and receive before any byte moves (see exchange()).
+  std::vector<uint64_t> send_full, recv_full;
+  exchange_caps(plan_, me, &send_full, &recv_full);
+  double frac = 0.25;
+  if (const char* f = getenv("WSYNC_EXCHANGE_FRACTION")) frac = atof(f);
+  std::vector<uint64_t> region_cap(c->coords);
+  for (int k = 0; k < c->coords; ++k)
+    region_cap[k] = send_full[k] ? std::max<uint64_t>(4096, (uint64_t)(frac * send_full[k])) : 0;
+  uint64_t recv_full_total = 0;
+  for (auto v : recv_full) recv_full_total += v;
   c->dests.assign(c->coords, {});
   for (int g = 0; g < c->world; ++g)
     if (g != me) c->dests[plan_.coord_of_rank(g)].push_back(g);
 
-  const size_t wb = wire_bytes(dtype_);
-  WS_CUDA_TRY(cudaMalloc(&c->d_send, std::max<uint64_t>(1, c->send_cap) * wb), "cudaMalloc send");
-  WS_CUDA_TRY(cudaMalloc(&c->d_recv, std::max<uint64_t>(1, c->recv_cap) * wb), "cudaMalloc recv");
   WS_CUDA_TRY(cudaMalloc(&c->d_region_off, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_region_cap, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_region_cnt, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_allcnt, (size_t)c->world * c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_err, 4), "cudaMalloc");
   WS_CUDA_TRY(cudaMallocHost(&c->h_allcnt, (size_t)c->world * c->coords * 8), "cudaMallocHost");
+  const char* mode = getenv("WSYNC_EXCHANGE");
+  const bool want_p2p = !(mode && std::string(mode) == "nccl") && c->world <= kMaxWorld &&
+                        c->coords <= kMaxWorld && plan_.replicas() <= kMaxReplicas;
+  if (want_p2p) {
+    ws_status st = init_p2p(send_full, recv_full);
+    if (st == WS_OK) return WS_OK;
+    // fall back to the NCCL exchange (e.g. no CUDA IPC between these GPUs)
+    c->p2p = false;
+  }
+  ws_status st = size_send(region_cap);
+  if (st != WS_OK) return st;
+  return size_recv(recv_full_total ? std::max<uint64_t>(4096, (uint64_t)(frac * recv_full_total)) : 0);
+}
+
+// Peer-memory exchange: every rank exports [mailbox | receive buffer] with
+// CUDA IPC; the layouts of all ranks follow from the static plan (no data
+// exchange needed beyond the 64-byte handles, all-gathered over NCCL).
+ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
+                              const std::vector<uint64_t>& recv_full) {
+  Comm* c = comm_;
+  const int me = c->rank, W = c->world, C = c->coords;
+  const size_t wb = wire_bytes(dtype_);
+  // receive layout of every rank: one region per source, worst-case sized
+  std::vector<std::vector<uint64_t>> off(W, std::vector<uint64_t>(W + 1, 0));
+  std::vector<std::vector<uint64_t>> cap(W);
+  for (int g = 0; g < W; ++g) {
+    std::vector<uint64_t> s_unused;
+    exchange_caps(plan_, g, &s_unused, &cap[g]);
+    for (int s = 0; s < W; ++s) off[g][s + 1] = off[g][s] + cap[g][s];
+  }
+  const size_t bytes = kMailboxBytes + std::max<uint64_t>(1, off[me][W]) * wb;
+  if (cudaMalloc(&c->d_p2p, bytes) != cudaSuccess)
+    return set_error(WS_CUDA, "p2p: receive buffer allocation failed");
+  WS_CUDA_TRY(cudaMemset(c->d_p2p, 0, kMailboxBytes), "memset mailbox");
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, c->d_p2p) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(WS_CUDA, "p2p: cudaIpcGetMemHandle failed");
+  }
+  void* d_h = nullptr;
+  WS_CUDA_TRY(cudaMalloc(&d_h, (size_t)W * sizeof(h)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(static_cast<char*>(d_h) + me * sizeof(h), &h, sizeof(h),
+                         cudaMemcpyHostToDevice), "H2D");
+  cudaStream_t s0;
+  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
+  ncclResult_t nr = ncclAllGather(static_cast<char*>(d_h) + me * sizeof(h), d_h, sizeof(h),
+                                  ncclUint8, c->comm, s0);
+  std::vector<cudaIpcMemHandle_t> all(W);
+  cudaStreamSynchronize(s0);
+  cudaStreamDestroy(s0);
+  cudaMemcpy(all.data(), d_h, (size_t)W * sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d_h);
+  if (nr != ncclSuccess) return set_error(WS_NCCL, "p2p: handle all-gather failed");
+  c->peer.assign(W, nullptr);
+  bool ok = true;
+  for (int g = 0; g < W; ++g) {
+    if (g == me) continue;
+    if (cudaIpcOpenMemHandle(&c->peer[g], all[g], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+    }
+  }
+  // every rank must agree, or one would wait forever for a flag
+  int* d_ok = nullptr;
+  WS_CUDA_TRY(cudaMalloc(&d_ok, sizeof(int)), "cudaMalloc");
+  int h_ok = ok ? 1 : 0;
+  WS_CUDA_TRY(cudaMemcpy(d_ok, &h_ok, sizeof(int), cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
+  nr = ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, s0);
+  cudaStreamSynchronize(s0);
+  cudaStreamDestroy(s0);
+  cudaMemcpy(&h_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d_ok);
+  if (nr != ncclSuccess || !h_ok) return set_error(WS_CUDA, "p2p: CUDA IPC unavailable");
+
+  P2PArgs& P = c->pargs;
+  P = P2PArgs{};
+  P.on = 1;
+  P.world = W;
+  P.rank = me;
+  P.mailbox = static_cast<unsigned long long*>(c->d_p2p);
+  for (int g = 0; g < W; ++g)
+    P.peer_mailbox[g] = static_cast<unsigned long long*>(g == me ? c->d_p2p : c->peer[g]);
+  for (int k = 0; k < kMaxWorld; ++k)
+    for (int r = 0; r < kMaxReplicas; ++r) {
+      P.dest[k][r] = nullptr;
+      P.dest_rank[k][r] = -1;
+    }
+  std::vector<uint64_t> region_cap(C, 0);
+  for (int k = 0; k < C; ++k) {
+    if (!send_full[k]) continue;
+    int r = 0;
+    for (int g : c->dests[k]) {
+      P.dest[k][r] = static_cast<char*>(c->peer[g]) + kMailboxBytes + off[g][me] * wb;
+      P.dest_rank[k][r] = g;
+      region_cap[k] = cap[g][me];
+      ++r;
+    }
+  }
+  P.recv = static_cast<char*>(c->d_p2p) + kMailboxBytes;
+  for (int s = 0; s < W; ++s) {
+    P.recv_off[s] = off[me][s];
+    if (s != me && recv_full[s]) P.expect_mask |= 1u << s;
+  }
+  P.err = c->d_err;
+  c->region_cap = region_cap;
+  c->region_off.assign(C, 0);
+  WS_CUDA_TRY(cudaMemcpy(c->d_region_off, c->region_off.data(), C * 8, cudaMemcpyHostToDevice),
+              "H2D");
+  WS_CUDA_TRY(cudaMemcpy(c->d_region_cap, region_cap.data(), C * 8, cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "memset");
+  c->p2p = true;
+  return WS_OK;
+}
+
+// (Re)allocates the send regions with the given per-coordinate capacities.
+ws_status ws_engine::size_send(const std::vector<uint64_t>& region_cap) {
+  Comm* c = comm_;
+  c->region_cap = region_cap;
+  c->region_off.assign(c->coords, 0);
+  c->send_cap = 0;
+  for (int k = 0; k < c->coords; ++k) {
+    c->region_off[k] = c->send_cap;
+    c->send_cap += region_cap[k];
+  }
+  cudaFree(c->d_send);
+  c->d_send = nullptr;
+  WS_CUDA_TRY(cudaMalloc(&c->d_send, std::max<uint64_t>(1, c->send_cap) * wire_bytes(dtype_)),
+              "cudaMalloc send");
   WS_CUDA_TRY(cudaMemcpy(c->d_region_off, c->region_off.data(), c->coords * 8,
                          cudaMemcpyHostToDevice), "H2D");
   WS_CUDA_TRY(cudaMemcpy(c->d_region_cap, c->region_cap.data(), c->coords * 8,
                          cudaMemcpyHostToDevice), "H2D");
+  return WS_OK;
+}
+
+ws_status ws_engine::size_recv(uint64_t records) {
+  Comm* c = comm_;
+  cudaFree(c->d_recv);
+  c->d_recv = nullptr;
+  c->recv_cap = records;
+  WS_CUDA_TRY(cudaMalloc(&c->d_recv, std::max<uint64_t>(1, records) * wire_bytes(dtype_)),
+              "cudaMalloc recv");
   return WS_OK;
 }
 
@@ -169,6 +317,40 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   Comm* c = comm_;
   if (!c) return set_error(WS_INVALID_ARGUMENT, "exchange without a communicator");
   const size_t wb = wire_bytes(dtype_);
+  if (c->p2p) {
+    // One kernel packs AND moves the records into the peers' receive
+    // buffers over NVLink; the receiving kernel waits on its own mailbox.
+    // No host synchronisation, no collective launch.
+    c->pargs.epoch = ++c->epoch;
+    WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
+    PackArgs pa{};
+    pa.r.entries = c->d_entries;
+    pa.r.nentries = c->nentries;
+    pa.r.sparse = o.sparse ? 1 : 0;
+    pa.r.seg_nnz = d_nnz_;
+    pa.r.seg_cap = d_cap_;
+    pa.r.seg_rec = d_rec_;
+    pa.r.seg_base = d_base_;
+    pa.r.rec_idx = d_idx_;
+    pa.r.rec_val = d_val_;
+    pa.r.train_next = arena[next_arena];
+    pa.r.serve = serve;
+    pa.r.unit_off = c->d_unit_off;
+    pa.region_off = c->d_region_off;
+    pa.region_cap = c->d_region_cap;
+    pa.region_cnt = c->d_region_cnt;
+    pa.err = c->d_err;
+    pa.p2p = c->pargs;
+    WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (p2p)");
+    if (c->nentries) *launches += 2;
+    if (c->pargs.expect_mask) {
+      WS_CUDA_TRY(launch_apply_p2p(dtype_, c->pargs, nullptr, serve, sm_count() * 4, s),
+                  "apply (p2p)");
+      *launches += 1;
+    }
+    pulled_bytes_ = 0;  // filled by exchange_report() when a report is asked for
+    return WS_OK;
+  }
   // 1. pack
   WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
   WS_CUDA_TRY(cudaMemsetAsync(c->d_err, 0, 4, s), "memset");
@@ -192,18 +374,39 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   pa.err = c->d_err;
   WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack");
   if (c->nentries) *launches += 2;
-  // 2. counts
+  // 2. counts (a region that overflowed still counts every record it needs)
   WS_NCCL_TRY(ncclAllGather(c->d_region_cnt, c->d_allcnt, c->coords, ncclUint64, c->comm, s),
               "ncclAllGather");
   WS_CUDA_TRY(cudaMemcpyAsync(c->h_allcnt, c->d_allcnt, (size_t)c->world * c->coords * 8,
                               cudaMemcpyDeviceToHost, s),
               "D2H counts");
-  uint32_t err = 0;
-  WS_CUDA_TRY(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
   WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
-  if (err) return set_error(WS_CAPACITY, "exchange: send region overflow");
-  // 3. one grouped send/recv
   const int me = c->rank, my_coord = plan_.my_coord();
+  // grow what is too small (decided from global knowledge, no extra round)
+  bool grow_send = false;
+  std::vector<uint64_t> need(c->coords);
+  for (int k = 0; k < c->coords; ++k) {
+    need[k] = c->h_allcnt[(size_t)me * c->coords + k];
+    grow_send |= need[k] > c->region_cap[k];
+  }
+  uint64_t recv_need = 0;
+  for (int g = 0; g < c->world; ++g)
+    if (g != me) recv_need += c->h_allcnt[(size_t)g * c->coords + my_coord];
+  if (recv_need > c->recv_cap) {
+    ws_status st = size_recv(recv_need + recv_need / 4);
+    if (st != WS_OK) return st;
+  }
+  if (grow_send) {
+    for (int k = 0; k < c->coords; ++k)
+      need[k] = std::max(c->region_cap[k], need[k] + need[k] / 4);
+    ws_status st = size_send(need);
+    if (st != WS_OK) return st;
+    pa.send = c->d_send;
+    WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
+    WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (grown)");
+    *launches += 2;
+  }
+  // 3. one grouped send/recv
   uint64_t recv_total = 0, sent = 0;
   WS_NCCL_TRY(ncclGroupStart(), "ncclGroupStart");
   for (int k = 0; k < c->coords; ++k) {

@@ -157,6 +157,16 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
   const uint64_t total = a.unit_off[a.nentries];
   const T* val = reinterpret_cast<const T*>(a.rec_val);
   const T* next = reinterpret_cast<const T*>(a.train_next);
+  const P2PArgs& P = pa.p2p;
+  const int W = P.world;
+  if (P.on && threadIdx.x == 0) {
+    // every destination must have consumed our previous step's records
+    for (int c = 0; c < kMaxWorld; ++c)
+      for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
+        if (!wait_geq_sys(P.mailbox + 2 * W + P.dest_rank[c][r], P.epoch - 1))
+          atomicOr(P.err, kErrBitTimeout);
+  }
+  __syncthreads();
   for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
     if (threadIdx.x == 0) {
       const int e = find_entry(a.unit_off, a.nentries, u);
@@ -168,7 +178,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     const uint64_t lu = u - s_u0;
     __syncthreads();
     const int c = E.coord;
-    const uint64_t roff = pa.region_off[c], rcap = pa.region_cap[c];
+    const uint64_t roff = P.on ? 0 : pa.region_off[c], rcap = pa.region_cap[c];
     // emits one record per lane with `valid`, reserving slots warp-wide
     auto emit = [&](bool valid, uint64_t idx, T v, bool set) {
       const unsigned bal = __ballot_sync(kFullMask, valid);
@@ -183,13 +193,23 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
         return;
       }
       if constexpr (DT == WS_BF16) {
-        reinterpret_cast<uint64_t*>(pa.send)[roff + slot] =
-            (set ? kWireSet : 0ull) | (idx << 16) | (uint64_t)v;
+        const uint64_t w = (set ? kWireSet : 0ull) | (idx << 16) | (uint64_t)v;
+        if (!P.on) {
+          reinterpret_cast<uint64_t*>(pa.send)[roff + slot] = w;
+        } else {  // straight into every replica's receive buffer over NVLink
+          for (int r = 0; r < kMaxReplicas && P.dest[c][r]; ++r)
+            reinterpret_cast<uint64_t*>(P.dest[c][r])[slot] = w;
+        }
       } else {
         ulonglong2 w;
         w.x = (set ? kWireSet : 0ull) | idx;
         w.y = (unsigned long long)v;
-        reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
+        if (!P.on) {
+          reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
+        } else {
+          for (int r = 0; r < kMaxReplicas && P.dest[c][r]; ++r)
+            reinterpret_cast<ulonglong2*>(P.dest[c][r])[slot] = w;
+        }
       }
     };
     if (!seg_dense(a, E.seg)) {
@@ -235,27 +255,95 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
       }
     }
   }
+  if (P.on) {
+    // The last block to finish publishes, per destination, how many records
+    // it now holds from us and this step's flag (after a system fence, so the
+    // records are visible before the flag).
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long prev = atomicAdd(P.mailbox + 3 * W, 1ull);
+      if (prev == gridDim.x - 1) {
+        __threadfence();
+        for (int c = 0; c < kMaxWorld; ++c) {
+          const unsigned long long n =
+              *reinterpret_cast<volatile unsigned long long*>(pa.region_cnt + c);
+          for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
+            st_relaxed_sys(P.peer_mailbox[P.dest_rank[c][r]] + P.rank, n);
+        }
+        __threadfence_system();
+        for (int c = 0; c < kMaxWorld; ++c)
+          for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
+            st_release_sys(P.peer_mailbox[P.dest_rank[c][r]] + W + P.rank, P.epoch);
+        P.mailbox[3 * W] = 0;
+      }
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void apply_record(const void* recv, uint64_t k,
+                                             typename Traits<DT>::T* serve) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  uint64_t key;
+  T v;
+  if constexpr (DT == WS_BF16) {
+    const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(recv) + k);
+    key = (w & kWireSet) | ((w & ~kWireSet) >> 16);
+    v = (T)(w & 0xffffu);
+  } else {
+    const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(recv) + k);
+    key = w.x;
+    v = (T)w.y;
+  }
+  const uint64_t i = key & ~kWireSet;
+  serve[i] = (key & kWireSet) ? v : Tr::add(serve[i], v);
 }
 
 template <int DT>
 __global__ void apply_wire_kernel(const void* recv, uint64_t nrec, typename Traits<DT>::T* serve) {
-  using Tr = Traits<DT>;
-  using T = typename Tr::T;
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nrec;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t key;
-    T v;
-    if constexpr (DT == WS_BF16) {
-      const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(recv) + k);
-      key = (w & kWireSet) | ((w & ~kWireSet) >> 16);
-      v = (T)(w & 0xffffu);
-    } else {
-      const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(recv) + k);
-      key = w.x;
-      v = (T)w.y;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    apply_record<DT>(recv, k, serve);
+}
+
+// P2P receiver: every block waits (on its own HBM) for the step flags of the
+// expected sources, then the grid applies the records in the receive buffer
+// (one contiguous region per source); the last block acks the sources so
+// they may overwrite their regions next step.
+template <int DT>
+__global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
+  const int W = P.world;
+  __shared__ unsigned long long s_cnt[kMaxWorld];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W; ++s) {
+      s_cnt[s] = 0;
+      if (!(P.expect_mask & (1u << s))) continue;
+      if (!wait_geq_sys(P.mailbox + W + s, P.epoch)) atomicOr(P.err, kErrBitTimeout);
+      s_cnt[s] = *reinterpret_cast<volatile unsigned long long*>(P.mailbox + s);
     }
-    const uint64_t i = key & ~kWireSet;
-    serve[i] = (key & kWireSet) ? v : Tr::add(serve[i], v);
+  }
+  __syncthreads();
+  uint64_t off[kMaxWorld + 1];
+  off[0] = 0;
+  for (int s = 0; s < W; ++s) off[s + 1] = off[s] + s_cnt[s];
+  const uint64_t total = off[W];
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    while (k >= off[s + 1]) ++s;
+    apply_record<DT>(P.recv, P.recv_off[s] + (k - off[s]), serve);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev = atomicAdd(P.mailbox + 3 * W + 1, 1ull);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (int s = 0; s < W; ++s)
+        if (P.expect_mask & (1u << s)) st_release_sys(P.peer_mailbox[s] + 2 * W + P.rank, P.epoch);
+      P.mailbox[3 * W + 1] = 0;
+    }
   }
 }
 
@@ -268,6 +356,17 @@ cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s) 
     case WS_BF16: pack_kernel<WS_BF16><<<grid, 256, 0, s>>>(a); break;
     case WS_I32: pack_kernel<WS_I32><<<grid, 256, 0, s>>>(a); break;
     case WS_F32: pack_kernel<WS_F32><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, const uint64_t*, void* serve, int grid,
+                            cudaStream_t s) {
+  switch (dtype) {
+    case WS_BF16: apply_p2p_kernel<WS_BF16><<<grid, 256, 0, s>>>(p, (uint16_t*)serve); break;
+    case WS_I32: apply_p2p_kernel<WS_I32><<<grid, 256, 0, s>>>(p, (uint32_t*)serve); break;
+    case WS_F32: apply_p2p_kernel<WS_F32><<<grid, 256, 0, s>>>(p, (uint32_t*)serve); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -56,19 +56,50 @@ inline size_t wire_bytes(int dtype) { return dtype == WS_BF16 ? 8 : 16; }
 // irrelevant).  Sparse segments are re-indexed (reslice) into the
 // destination shard; dense-fallback segments emit set records for the box
 // overlap.
+constexpr int kMaxWorld = 8;      // GPUs of one box
+constexpr int kMaxReplicas = 8;
+
+// Peer-memory (P2P) exchange state shared by the pack and apply kernels.
+// Mailbox of every rank (u64 words, in its own HBM, mapped by all peers):
+//   [0, W) records sent by rank s this step   [W, 2W) step flag from s
+//   [2W, 3W) ack of rank g for our last data   [3W] pack blocks done
+//   [3W + 1] apply blocks done
+struct P2PArgs {
+  int32_t on;                       // 0: NCCL mode (send region + host exchange)
+  int32_t world, rank;
+  uint32_t epoch;                   // this step's number (>= 1), equal on every rank
+  unsigned long long* mailbox;                        // local
+  unsigned long long* peer_mailbox[kMaxWorld];        // mapped peers' mailboxes
+  void* dest[kMaxWorld][kMaxReplicas];                // per coordinate: my region at each replica
+  int32_t dest_rank[kMaxWorld][kMaxReplicas];         // -1 terminated
+  // receiver side
+  const void* recv;                                   // local records, partitioned by source
+  uint64_t recv_off[kMaxWorld];                       // per source, records
+  uint32_t expect_mask;                               // sources that send to this rank
+  uint32_t* err;                                      // WS_ERRBIT_* (timeouts, capacity)
+};
+constexpr uint32_t kErrBitTimeout = 0x4u;
+constexpr size_t kMailboxBytes = 4096;
+
 struct PackArgs {
   RouteSideArgs r;                  // entries = the remote routes
-  void* send;
-  const uint64_t* region_off;       // per coordinate, in records
-  const uint64_t* region_cap;
+  void* send;                       // NCCL mode: local send regions
+  const uint64_t* region_off;       // per coordinate, in records (NCCL mode)
+  const uint64_t* region_cap;       // per coordinate capacity (at the destination in P2P mode)
   unsigned long long* region_cnt;   // per coordinate, zeroed before the launch
   uint32_t* err;                    // WS_ERRBIT_CAPACITY on overflow
+  P2PArgs p2p;
 };
 cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s);
 
 // Receiver side: applies nrec wire records to the serving arena in place.
 cudaError_t launch_apply_wire(int dtype, const void* recv, uint64_t nrec, void* serve,
                              cudaStream_t s);
+
+// P2P receiver: waits for every expected source's step flag, applies all
+// records that arrived in the local receive buffer, acks the sources.
+cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, const uint64_t* region_cnt_unused,
+                            void* serve, int grid, cudaStream_t s);
 
 // Fills a LocalEntry for the route src -> dst of a tensor of `full`.
 LocalEntry make_local_entry(int dtype, const int64_t* full, int nd, int seg, const ws_shard& src,
