@@ -2,12 +2,11 @@
 //
 // K1 (encode) replaces the reference's diff_shards + density check +
 // encode_sparse packing (codec.cpp:34-63, engine.cpp:118-127,
-// codec.cpp:164-183).  One pass over prev/next: 128-bit streaming loads, a
-// per-vector change mask (bit compare for bf16/i32, value compare for f32),
-// popc per thread, a block scan of four packed 16-bit lane counts, and a
-// decoupled look-back across the tiles of each segment, then the records
-// are written at their final ascending position.  Segments are independent
-// look-back chains so every segment's records start at its own base.
+// codec.cpp:164-183): one pass over prev/next that writes every change as an
+// (ascending local index, delta) record at its final position in its
+// segment's stream, via a decoupled look-back prefix sum over super-tiles
+// (segments are independent look-back chains).  The design and the
+// measurements behind it are in DESIGN.md §4.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -20,7 +19,6 @@ namespace {
 
 constexpr int kThreads = kEncodeThreads;
 constexpr int kWarps = kThreads / 32;
-constexpr int kVPT = kEncodeVPT;
 
 __device__ __forceinline__ int find_segment(const uint32_t* tile0, int nseg, uint32_t t) {
   int lo = 0, hi = nseg;  // tile0[lo] <= t < tile0[hi]
@@ -66,20 +64,22 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
 //                streams their sub-tiles of prev and next into a kRing-deep
 //                shared-memory ring with 1-D bulk copies (cp.async.bulk)
 //                completing on per-stage mbarriers;
-//   warps 0-15   consumers: per 16-byte vector the change mask (bit compare
-//                for bf16/i32, value compare for f32); per (sub-tile, vector
-//                slot, warp) chunk the record count; records ranked with a
-//                ballot/popc fast path (shuffle scan when a lane holds two or
-//                more) and staged in the warp's slice of a double-buffered
-//                staging area.  Each stage is released as soon as it is
-//                counted, so HBM streams continuously;
-//   warps 17-18  resolvers (one per staging buffer): scan the chunk counts,
-//                publish the super-tile count, resolve its offset in its
-//                segment with the decoupled look-back, and flush the staged
-//                records to their final ascending positions with coalesced
-//                stores.  Look-back latency never stalls the stream.
-// Super-tiles denser than 25% spill: records past a warp slice are
-// re-derived from the kept masks and global memory by the resolver.
+//   warps 0-15   consumers: per 16-byte vector the change mask (SWAR bit
+//                compare for bf16, lane compare for i32, value compare for
+//                f32); per (sub-tile, vector slot, warp) chunk the record
+//                count; records ranked with a ballot/popc fast path (shuffle
+//                scan when a lane holds two or more) and staged in the warp's
+//                slice of a 3-deep staging area.  Each stage is released as
+//                soon as it is counted, so HBM streams continuously;
+//   warps 17-19  resolvers (one per staging buffer): scan the chunk counts,
+//                publish the super-tile count, and resolve its offset in its
+//                segment with the decoupled look-back;
+//   each consumer warp writes its own staged records of super-tile i to their
+//   final ascending positions after staging super-tile i+2 (the look-back
+//   has had two super-tile periods), applying them in place to a serving
+//   shard on this GPU when the engine asks for the fused apply.
+// Super-tiles denser than 18.75% spill: records past a warp slice are
+// re-derived from global memory by that warp when it writes them out.
 struct StageMeta {
   SegDev sg;
   uint32_t t, s, lt, nsub, cnt, last;
