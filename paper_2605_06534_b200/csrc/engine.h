@@ -64,6 +64,7 @@ struct ws_engine {
   // local routes
   wsync::LocalEntry* d_local_ = nullptr;
   wsync::FuseEntry* d_fuse_ = nullptr;
+  uint32_t* d_fuse_on_ = nullptr;
   bool fuse_apply_ = true;  // K1 applies local sparse records (WSYNC_NO_FUSED_APPLY=1 disables)
   int nlocal_ = 0;
   uint64_t* d_unit_off_ = nullptr;

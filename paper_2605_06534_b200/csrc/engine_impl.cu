@@ -33,6 +33,7 @@ ws_engine::~ws_engine() {
   cudaFree(d_val_);
   cudaFree(d_local_);
   cudaFree(d_fuse_);
+  cudaFree(d_fuse_on_);
   cudaFree(d_unit_off_);
   if (h_nnz_pinned_) cudaFreeHost(h_nnz_pinned_);
   if (ring_) {
@@ -119,6 +120,11 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
     f.map = e.map;
   }
   WS_CUDA_TRY(cudaMalloc(&d_fuse_, fuse.size() * sizeof(FuseEntry)), "cudaMalloc");
+  {
+    std::vector<uint32_t> on(fuse.size(), 1u);  // fuse until a sync says a segment runs dense
+    WS_CUDA_TRY(cudaMalloc(&d_fuse_on_, on.size() * 4), "cudaMalloc");
+    WS_CUDA_TRY(cudaMemcpy(d_fuse_on_, on.data(), on.size() * 4, cudaMemcpyHostToDevice), "H2D");
+  }
   WS_CUDA_TRY(cudaMemcpy(d_fuse_, fuse.data(), fuse.size() * sizeof(FuseEntry),
                          cudaMemcpyHostToDevice), "H2D");
   if (const char* f = getenv("WSYNC_NO_FUSED_APPLY")) fuse_apply_ = atoi(f) == 0;
@@ -233,6 +239,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     a.tile_seg = d_tile_seg_;
     if (fuse_apply_) {
       a.fuse = d_fuse_;
+      a.fuse_on = d_fuse_on_;
       a.serve = serve;
     }
     a.nseg = nseg_;
@@ -261,6 +268,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   r.serve = serve;
   r.unit_off = d_unit_off_;
   r.fused = (fuse_apply_ && o.sparse && ntiles_) ? 1 : 0;
+  r.fuse_on = d_fuse_on_;
   WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
   if (nlocal_) launches += 2;
   WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");

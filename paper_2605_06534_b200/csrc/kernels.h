@@ -73,6 +73,7 @@ struct EncodeArgs {
   unsigned int* ticket;        // zeroed before launch
   uint32_t debug;              // perf experiments only (WSYNC_ENCODE_DEBUG): 1 no look-back, 2 no writes
   const FuseEntry* fuse;       // optional, per segment: apply records to `serve` as they are written
+  const uint32_t* fuse_on;     // per segment: fuse this step (device-adapted from the last one)
   void* serve;
 };
 

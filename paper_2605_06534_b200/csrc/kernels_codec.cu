@@ -216,7 +216,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
   if (run == 0 || (a.debug & 2) || prefix >= ti.cap) return;
   const uint64_t e0 = (uint64_t)ti.lt * SUPER;
   T* out_val = reinterpret_cast<T*>(a.out_val);
-  const FuseEntry* fz = (a.fuse && a.fuse[ti.seg].mode) ? a.fuse + ti.seg : nullptr;
+  const FuseEntry* fz =
+      (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
   T* serve = reinterpret_cast<T*>(a.serve);
   const int cl = lane < CPW ? lane : CPW - 1;
   const uint32_t ccnt = lane < CPW ? s_cnt[cl * NCW + w] : 0u;
@@ -255,10 +256,23 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
       for (int v = 0; v < (int)VPT; ++v) {
         const int c = g * VPT + v;
         const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
+        const uint64_t gv = ti.base + e0 + li;  // multiple of VE: 16-byte aligned
+        uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
         uint32_t mv = 0;
-        for (int e = 0; e < VE; ++e) {
-          const uint64_t gi = ti.base + e0 + li + e;
-          if (li + e < ti.cnt && Tr::changed(prevT[gi], nextT[gi])) mv |= 1u << e;
+        if (li + VE <= ti.cnt) {
+          pa = ld_stream(reinterpret_cast<const uint4*>(prevT + gv));
+          pb = ld_stream(reinterpret_cast<const uint4*>(nextT + gv));
+          mv = change_mask<DT>(pa, pb);
+        } else {
+          T ta[VE], tb[VE];
+          for (int e = 0; e < VE; ++e) {
+            const bool in = li + e < ti.cnt;
+            ta[e] = in ? prevT[gv + e] : T(0);
+            tb[e] = in ? nextT[gv + e] : T(0);
+            if (in && Tr::changed(ta[e], tb[e])) mv |= 1u << e;
+          }
+          memcpy(&pa, ta, 16);
+          memcpy(&pb, tb, 16);
         }
         uint32_t tot;
         uint32_t r = warp_rank(mv, &tot);
@@ -269,8 +283,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
           mv &= mv - 1;
           const uint64_t pos = prefix + of + r;
           if (st + r >= WCAP && pos < ti.cap) {
-            const uint64_t gi = ti.base + e0 + li + e;
-            const T v = Tr::delta(prevT[gi], nextT[gi]);
+            const T v = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
             a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
             out_val[ti.rec + pos] = v;
             if (fz) fuse_apply<DT>(fz, serve, (uint32_t)(e0 + li + e), v);

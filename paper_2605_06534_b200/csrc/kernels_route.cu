@@ -29,7 +29,7 @@ __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const Lo
     const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
     return e.box.rows * per_row;
   }
-  if (a.fused) return 0;  // K1 applied the sparse records as it wrote them
+  if (a.fused && a.fuse_on[e.seg]) return 0;  // K1 applied the sparse records as it wrote them
   const uint64_t nnz = a.seg_nnz[e.seg];
   return (nnz + kApplyChunk - 1) / kApplyChunk;
 }
@@ -43,6 +43,13 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
   for (int base = 0; base < a.nentries; base += kWlThreads) {
     const int e = base + tid;
     const uint64_t u = e < a.nentries ? entry_units(a, a.entries[e]) : 0;
+    if (e < a.nentries && a.fused) {
+      // Next sync: fuse the apply into K1 only for segments that stayed well
+      // below the dense threshold; the others skip the scattered
+      // read-modify-writes of records a dense copy would overwrite anyway.
+      const int s = a.entries[e].seg;
+      a.fuse_on[s] = a.seg_nnz[s] * 2 <= a.seg_cap[s] ? 1u : 0u;
+    }
     uint64_t inc = u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -28,7 +28,8 @@ struct RouteSideArgs {
   const LocalEntry* entries;
   int32_t nentries;
   int32_t sparse;               // 0: every segment dense (SyncOptions::sparse)
-  int32_t fused;                // 1: K1 already applied sparse records (dense copies only)
+  int32_t fused;                // 1: K1 applied the sparse records of segments with fuse_on set
+  uint32_t* fuse_on;            // per segment; re-decided here for the next sync from this one
   const uint64_t* seg_nnz;
   const uint64_t* seg_cap;
   const uint64_t* seg_rec;
