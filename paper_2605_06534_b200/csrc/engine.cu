@@ -179,7 +179,7 @@ ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev, void* train_next_
   eng->arena[0] = train_prev_dev;
   eng->arena[1] = train_next_dev;
   eng->serve = serve_dev;
-  return WS_OK;
+  return eng->map_serve();
 }
 
 ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density, ws_stream_t stream) {

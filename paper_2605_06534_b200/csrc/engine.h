@@ -22,6 +22,9 @@ struct ws_engine {
   // caller-owned arenas (ws_engine_bind)
   void* arena[2] = {nullptr, nullptr};
   void* serve = nullptr;
+  // Multi-GPU P2P: maps every replica's serving arena for direct dense
+  // copies.  Collective: every rank binds (ws_engine_bind) in the same order.
+  ws_status map_serve();
 
  private:
   ws_status ensure_records(double threshold, int sparse);

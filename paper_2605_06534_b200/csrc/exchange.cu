@@ -17,6 +17,7 @@
 // Region and receive capacities are sized from the static plan for the
 // worst case (every element of every route sent dense), so no step can
 // overflow.
+#include <cuda.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -63,11 +64,14 @@ struct ws_engine::Comm {
   bool p2p = false;
   void* d_p2p = nullptr;                         // [mailbox | receive buffer] (IPC-exported)
   std::vector<void*> peer;                       // mapped d_p2p of every rank (null: me)
+  std::vector<void*> peer_serve_map;             // mapped serving allocations (null: me)
   P2PArgs pargs{};
   uint32_t epoch = 0;
 
   ~Comm() {
     for (void* p : peer)
+      if (p) cudaIpcCloseMemHandle(p);
+    for (void* p : peer_serve_map)
       if (p) cudaIpcCloseMemHandle(p);
     cudaFree(d_p2p);
     cudaFree(d_entries);
@@ -273,6 +277,108 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
   WS_CUDA_TRY(cudaMemcpy(c->d_region_cap, region_cap.data(), C * 8, cudaMemcpyHostToDevice), "H2D");
   WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "memset");
   c->p2p = true;
+  return WS_OK;
+}
+
+namespace {
+
+// Base of the allocation holding `p` (driver entry point; the library does
+// not link libcuda).  IPC handles are per allocation, and the serving arena
+// may be a view into a larger caller allocation.
+bool allocation_base(void* p, void** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) return false;
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<void*>(b);
+  return true;
+}
+
+struct ServeHandle {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+  uint64_t ok;
+};
+
+}  // namespace
+
+// Maps the serving arena of every replica of the coordinates this rank sends
+// to, so dense-fallback boxes are stored straight into them (pack kernel).
+// Any rank failing (e.g. a virtual-memory allocation without an IPC handle)
+// turns the direct path off everywhere; dense boxes then travel as records.
+ws_status ws_engine::map_serve() {
+  Comm* c = comm_;
+  if (!c || !c->p2p || !serve) return WS_OK;
+  const int me = c->rank, W = c->world;
+  for (void* p : c->peer_serve_map)
+    if (p) cudaIpcCloseMemHandle(p);
+  c->peer_serve_map.assign(W, nullptr);
+  c->pargs.dense_direct = 0;
+  ServeHandle mine{};
+  void* base = nullptr;
+  if (allocation_base(serve, &base) && cudaIpcGetMemHandle(&mine.h, base) == cudaSuccess) {
+    mine.offset = static_cast<char*>(serve) - static_cast<char*>(base);
+    mine.ok = 1;
+  }
+  cudaGetLastError();
+  ServeHandle* d_h = nullptr;
+  WS_CUDA_TRY(cudaMalloc(&d_h, (size_t)W * sizeof(ServeHandle)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(d_h + me, &mine, sizeof(mine), cudaMemcpyHostToDevice), "H2D");
+  cudaStream_t s0;
+  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
+  ncclResult_t nr = ncclAllGather(d_h + me, d_h, sizeof(ServeHandle), ncclUint8, c->comm, s0);
+  cudaStreamSynchronize(s0);
+  std::vector<ServeHandle> all(W);
+  cudaMemcpy(all.data(), d_h, (size_t)W * sizeof(ServeHandle), cudaMemcpyDeviceToHost);
+  if (nr != ncclSuccess) {
+    cudaStreamDestroy(s0);
+    cudaFree(d_h);
+    return set_error(WS_NCCL, "map_serve: handle all-gather failed");
+  }
+  int ok = 1;
+  for (int g = 0; g < W; ++g) ok &= all[g].ok ? 1 : 0;
+  std::vector<char> needed(W, 0);
+  for (int k = 0; k < c->coords; ++k)
+    for (int g : c->dests[k]) needed[g] = 1;
+  for (int g = 0; g < W && ok; ++g) {
+    if (g == me || !needed[g]) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[g].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    c->peer_serve_map[g] = p;
+  }
+  // agree (all-reduce min over the flags, reusing the handle buffer)
+  int* d_ok = reinterpret_cast<int*>(d_h);
+  cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+  nr = ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, s0);
+  cudaStreamSynchronize(s0);
+  cudaStreamDestroy(s0);
+  cudaMemcpy(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d_h);
+  if (nr != ncclSuccess) return set_error(WS_NCCL, "map_serve: agreement failed");
+  P2PArgs& P = c->pargs;
+  for (int k = 0; k < kMaxWorld; ++k)
+    for (int r = 0; r < kMaxReplicas; ++r) P.serve_dst[k][r] = nullptr;
+  const char* env = getenv("WSYNC_DENSE_DIRECT");
+  if (!ok || (env && env[0] == '0')) return WS_OK;
+  for (int k = 0; k < c->coords; ++k) {
+    int r = 0;
+    for (int g : c->dests[k])
+      P.serve_dst[k][r++] = static_cast<char*>(c->peer_serve_map[g]) + all[g].offset;
+  }
+  P.dense_direct = 1;
   return WS_OK;
 }
 

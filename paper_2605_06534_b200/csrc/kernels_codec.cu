@@ -210,7 +210,6 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
   using T = typename Tr::T;
   constexpr int VE = C::VE, NCW = C::NCW, CPW = C::CPW;
   constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, WCAP = C::WCAP;
-  constexpr uint32_t VMASK = (1u << VE) - 1u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t run = ti.run;
   if (run == 0 || (a.debug & 2) || prefix >= ti.cap) return;

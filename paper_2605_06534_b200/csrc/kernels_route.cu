@@ -255,6 +255,37 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
         dso += cc * B.dst_stride[d];
       }
       const T* src = next + a.seg_base[E.seg] + so;
+      if (P.on && P.dense_direct) {
+        // peer stores into every replica's serving arena; the replicas share
+        // dst offsets and 16-byte aligned bases, so one alignment test serves all
+        const uint64_t dofs = E.dst_base + dso;
+        int nrep = 0;
+        while (nrep < kMaxReplicas && P.serve_dst[c][nrep]) ++nrep;
+        const T* s0 = src + c0;
+        const uint64_t n = c1 - c0;
+        constexpr int V = 16 / sizeof(T);
+        const uintptr_t sa = reinterpret_cast<uintptr_t>(s0);
+        const uintptr_t da = (dofs + c0) * sizeof(T);
+        uint64_t head = n, body = 0;
+        if (((sa ^ da) & 15) == 0) {
+          head = ((16 - (sa & 15)) & 15) / sizeof(T);
+          if (head > n) head = n;
+          body = (n - head) / V;
+        }
+        for (uint64_t j = threadIdx.x; j < head; j += blockDim.x)
+          for (int r = 0; r < nrep; ++r)
+            reinterpret_cast<T*>(P.serve_dst[c][r])[dofs + c0 + j] = s0[j];
+        const uint4* sv = reinterpret_cast<const uint4*>(s0 + head);
+        for (uint64_t j = threadIdx.x; j < body; j += blockDim.x) {
+          const uint4 v = ld_stream(sv + j);
+          for (int r = 0; r < nrep; ++r)
+            reinterpret_cast<uint4*>(reinterpret_cast<T*>(P.serve_dst[c][r]) + dofs + c0 + head)[j] = v;
+        }
+        for (uint64_t j = head + body * V + threadIdx.x; j < n; j += blockDim.x)
+          for (int r = 0; r < nrep; ++r)
+            reinterpret_cast<T*>(P.serve_dst[c][r])[dofs + c0 + j] = s0[j];
+        continue;
+      }
       for (uint64_t jb = c0 + (uint64_t)warp * 32; jb < c1; jb += (uint64_t)nwarps * 32) {
         const uint64_t j = jb + lane;
         const bool valid = j < c1;

@@ -73,6 +73,11 @@ struct P2PArgs {
   unsigned long long* peer_mailbox[kMaxWorld];        // mapped peers' mailboxes
   void* dest[kMaxWorld][kMaxReplicas];                // per coordinate: my region at each replica
   int32_t dest_rank[kMaxWorld][kMaxReplicas];         // -1 terminated
+  // Dense-fallback boxes bypass the records: with dense_direct the pack
+  // kernel copies them straight into every replica's (IPC-mapped) serving
+  // arena, 2 bytes per bf16 element over NVLink instead of an 8-byte record.
+  int32_t dense_direct;
+  void* serve_dst[kMaxWorld][kMaxReplicas];           // per coordinate: replica serving arenas
   // receiver side
   const void* recv;                                   // local records, partitioned by source
   uint64_t recv_off[kMaxWorld];                       // per source, records
