@@ -141,6 +141,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Pulls the sector holding `p` into L2 without blocking the warp.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // Global -> shared bulk copy completing on `bar` (bytes multiple of 16).
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {

@@ -34,6 +34,7 @@ struct ws_engine {
   ws_status size_send(const std::vector<uint64_t>& region_cap);
   ws_status size_recv(uint64_t records);
   void destroy_comm();
+  ws_status exchange_begin(cudaStream_t s, uint32_t* launches);  // P2P "reached step" flags
   ws_status exchange(const ws_sync_options& o, int next_arena, cudaStream_t s, uint32_t* launches);
   uint32_t next_epoch();
 
@@ -49,6 +50,20 @@ struct ws_engine {
   wsync::SegDev* d_segs_ = nullptr;
   uint32_t* d_tile0_ = nullptr;
   uint32_t* d_tile_seg_ = nullptr;
+  uint32_t* d_tile_cnt_ = nullptr;   // K1's unordered layout (see EncodeArgs)
+  uint32_t* d_tile_base_ = nullptr;
+  uint32_t tile_elems_ = 0;
+  std::vector<uint32_t> plan_tile0_;
+  // ascending stream of one segment, compacted on demand (segment_delta)
+  uint32_t* d_seq_idx_ = nullptr;
+  void* d_seq_val_ = nullptr;
+  uint64_t seq_alloc_ = 0;
+  void fill_tiles(wsync::RouteSideArgs& r) const {
+    r.tile0 = d_tile0_;
+    r.tile_cnt = d_tile_cnt_;
+    r.tile_base = d_tile_base_;
+    r.tile_elems = tile_elems_;
+  }
   unsigned long long* d_status_ = nullptr;
   unsigned int* d_ticket_ = nullptr;
   uint64_t* d_nnz_ = nullptr;

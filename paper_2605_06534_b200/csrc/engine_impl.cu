@@ -23,6 +23,10 @@ ws_engine::~ws_engine() {
   cudaFree(d_segs_);
   cudaFree(d_tile0_);
   cudaFree(d_tile_seg_);
+  cudaFree(d_tile_cnt_);
+  cudaFree(d_tile_base_);
+  cudaFree(d_seq_idx_);
+  cudaFree(d_seq_val_);
   cudaFree(d_status_);
   cudaFree(d_ticket_);
   cudaFree(d_nnz_);
@@ -65,6 +69,7 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   tile0[nseg_] = (uint32_t)t;
   if (t >= (1ull << 31)) return set_error(WS_CAPACITY, "too many encode tiles");
   ntiles_ = (uint32_t)t;
+  tile_elems_ = tile;
   segs_.resize(nseg_);
   std::vector<uint64_t> base(nseg_);
   for (int i = 0; i < nseg_; ++i) {
@@ -77,12 +82,17 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   WS_CUDA_TRY(cudaMalloc(&d_status_, std::max<size_t>(1, ntiles_) * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemset(d_status_, 0, std::max<size_t>(1, ntiles_) * 8), "cudaMemset");
   WS_CUDA_TRY(cudaMalloc(&d_ticket_, 256), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_tile_cnt_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_tile_base_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemset(d_tile_cnt_, 0, std::max<size_t>(1, ntiles_) * 4), "cudaMemset");
+  WS_CUDA_TRY(cudaMemset(d_tile_base_, 0, std::max<size_t>(1, ntiles_) * 4), "cudaMemset");
   WS_CUDA_TRY(cudaMalloc(&d_nnz_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemset(d_nnz_, 0, ns * 8), "cudaMemset");
   WS_CUDA_TRY(cudaMalloc(&d_cap_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_rec_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_base_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemcpy(d_tile0_, tile0.data(), (nseg_ + 1) * 4, cudaMemcpyHostToDevice), "H2D");
+  plan_tile0_ = tile0;
   {  // segment of every super-tile: one load instead of a search in K1's producer
     std::vector<uint32_t> tile_seg(std::max<uint32_t>(1, ntiles_));
     for (int i = 0; i < nseg_; ++i)
@@ -223,6 +233,10 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   last_stream_ = s;
 
   WS_CUDA_TRY(cudaEventRecord(ev_[0], s), "event");
+  if (plan_.world() > 1) {
+    st = exchange_begin(s, &launches);
+    if (st != WS_OK) return st;
+  }
   if (next_host) {
     WS_CUDA_TRY(cudaMemcpyAsync(arena[na], next_host, plan_.train_arena_elems() * esz,
                                 cudaMemcpyHostToDevice, s),
@@ -231,7 +245,12 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   WS_CUDA_TRY(cudaEventRecord(ev_[1], s), "event");
   last_sparse_ = o.sparse != 0;
   if (o.sparse && ntiles_) {
+    // K1 reserves each super-tile's records with an atomic on its segment's count
+    WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
     EncodeArgs a{};
+    a.unordered = 1;
+    a.tile_cnt = d_tile_cnt_;
+    a.tile_base = d_tile_base_;
     a.prev = arena[pa];
     a.next = arena[na];
     a.segs = d_segs_;
@@ -264,6 +283,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   r.seg_base = d_base_;
   r.rec_idx = d_idx_;
   r.rec_val = d_val_;
+  fill_tiles(r);
   r.train_next = arena[na];
   r.serve = serve;
   r.unit_off = d_unit_off_;
@@ -322,12 +342,35 @@ ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val
                                    char* codec) {
   if (i < 0 || i >= nseg_) return set_error(WS_INVALID_ARGUMENT, "segment index out of range");
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
   uint64_t n = 0;
   WS_CUDA_TRY(cudaMemcpy(&n, d_nnz_ + i, 8, cudaMemcpyDeviceToHost), "D2H nnz");
-  if (idx) *idx = d_idx_ ? d_idx_ + segs_[i].rec : nullptr;
-  if (val) *val = d_val_ ? (const char*)d_val_ + segs_[i].rec * dtype_size(dtype_) : nullptr;
+  const bool sparse = last_sparse_ && n <= segs_[i].cap;
+  const size_t esz = dtype_size(dtype_);
+  // K1 left the records grouped by super-tile in reservation order; hand
+  // out the ascending stream (codec.cpp:48-49 order), compacted here.
+  const uint64_t need = std::max<uint64_t>(1, segs_[i].cap);
+  if (need > seq_alloc_) {
+    cudaFree(d_seq_idx_);
+    cudaFree(d_seq_val_);
+    d_seq_idx_ = nullptr;
+    d_seq_val_ = nullptr;
+    WS_CUDA_TRY(cudaMalloc(&d_seq_idx_, need * 4), "cudaMalloc");
+    WS_CUDA_TRY(cudaMalloc(&d_seq_val_, need * esz), "cudaMalloc");
+    seq_alloc_ = need;
+  }
+  if (sparse && n) {
+    const uint32_t t0 = plan_tile0_[i], nt = plan_tile0_[i + 1] - t0;
+    WS_CUDA_TRY(launch_compact(dtype_, d_tile_cnt_ + t0, d_tile_base_ + t0, nt, segs_[i].cap,
+                               d_idx_ + segs_[i].rec, (const char*)d_val_ + segs_[i].rec * esz,
+                               d_seq_idx_, d_seq_val_, nullptr),
+                "compact");
+    WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  }
+  if (idx) *idx = d_seq_idx_;
+  if (val) *val = d_seq_val_;
   if (nnz) *nnz = n;
-  if (codec) *codec = (last_sparse_ && n <= segs_[i].cap) ? 'S' : 'D';
+  if (codec) *codec = sparse ? 'S' : 'D';
   return WS_OK;
 }
 

@@ -418,6 +418,16 @@ void ws_engine::destroy_comm() {
   comm_ = nullptr;
 }
 
+ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
+  Comm* c = comm_;
+  if (!c || !c->p2p || !c->pargs.dense_direct || !c->pargs.expect_mask) return WS_OK;
+  P2PArgs p = c->pargs;
+  p.epoch = c->epoch + 1;  // the number exchange() gives this sync
+  WS_CUDA_TRY(launch_p2p_ready(p, s), "p2p ready");
+  *launches += 1;
+  return WS_OK;
+}
+
 ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStream_t s,
                               uint32_t* launches) {
   Comm* c = comm_;
@@ -439,6 +449,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     pa.r.seg_base = d_base_;
     pa.r.rec_idx = d_idx_;
     pa.r.rec_val = d_val_;
+    fill_tiles(pa.r);
     pa.r.train_next = arena[next_arena];
     pa.r.serve = serve;
     pa.r.unit_off = c->d_unit_off;
@@ -470,6 +481,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   pa.r.seg_base = d_base_;
   pa.r.rec_idx = d_idx_;
   pa.r.rec_val = d_val_;
+  fill_tiles(pa.r);
   pa.r.train_next = arena[next_arena];
   pa.r.serve = serve;
   pa.r.unit_off = c->d_unit_off;

@@ -20,6 +20,9 @@ namespace wsync {
 #ifndef WS_ENC_BUFFERS
 #define WS_ENC_BUFFERS 3
 #endif
+#ifndef WS_ENC_CAPDIV
+#define WS_ENC_CAPDIV 16  // staged records per super-tile buffer: 3/CAPDIV of its elements
+#endif
 constexpr int kEncodeThreads = 256;                 // block size of the small codec kernels
 constexpr int kEncodeVPT = 4;                       // their vectors per thread
 constexpr int kEncConsumers = WS_ENC_CONSUMERS;     // K1 consumer threads (16 warps)
@@ -75,7 +78,21 @@ struct EncodeArgs {
   const FuseEntry* fuse;       // optional, per segment: apply records to `serve` as they are written
   const uint32_t* fuse_on;     // per segment: fuse this step (device-adapted from the last one)
   void* serve;
+  // Unordered mode (the engine): a super-tile reserves its records' place in
+  // its segment with one atomic on seg_nnz (zeroed before the launch) instead
+  // of the look-back, so no super-tile waits on another.  Records stay
+  // ascending inside a super-tile; (tile_base, tile_cnt) locate them, and
+  // launch_compact restores the ascending segment stream when one is asked for.
+  int32_t unordered;
+  uint32_t* tile_cnt;          // per global super-tile
+  uint32_t* tile_base;         // per global super-tile: first record in the segment stream
 };
+
+// Ascending segment stream from an unordered K1 output: the segment's
+// super-tiles' records in tile order (one block; API/wire path, not the sync).
+cudaError_t launch_compact(int dtype, const uint32_t* tile_cnt, const uint32_t* tile_base,
+                           uint32_t ntiles, uint64_t cap, const uint32_t* in_idx,
+                           const void* in_val, uint32_t* out_idx, void* out_val, cudaStream_t s);
 
 // K1: fused compare + ballot/popc + block scan + decoupled look-back
 // compaction over all segments.  Returns the persistent grid used.

@@ -94,7 +94,7 @@ struct EncCfg {
   static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  static constexpr uint32_t CAP = SUPER * 3 / 16;                     // staged records per buffer (18.75%)
+  static constexpr uint32_t CAP = SUPER * 3 / WS_ENC_CAPDIV;          // staged records per buffer (18.75%)
   static constexpr uint32_t WCAP = CAP / NCW;
   static constexpr int NCH = kEncodeSubTiles * VPT * NCW;             // chunks per super-tile
   static constexpr int CPW = kEncodeSubTiles * VPT;                   // chunks per consumer warp
@@ -156,6 +156,18 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
   const uint32_t count = __shfl_sync(kFullMask, incl, 31);
 #pragma unroll
   for (int q = 0; q < PER; ++q) s_off[lane * PER + q] = incl - sum + loc[q];
+  if (a.unordered) {  // one atomic reserves the super-tile's place in its segment
+    if (lane == 0) {
+      unsigned long long base = 0;
+      if (count)
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_nnz + ti.s),
+                         (unsigned long long)count);
+      a.tile_cnt[ti.t] = count;
+      a.tile_base[ti.t] = (uint32_t)base;  // <= segment size < 2^32
+      *s_prefix = base;
+    }
+    return;
+  }
   const bool head = ti.lt == 0 || (a.debug & 1);
   if (lane == 0)
     st_relaxed_u64(a.status + ti.t,
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     const int b = warp - NCW - 1;
     uint32_t par = 0;
     while (true) {
-      while (!mbar_try_wait(&staged[b], par)) __nanosleep(200);  // idle: keep issue slots free
+      mbar_wait(&staged[b], par);  // suspended in hardware while idle
       par ^= 1u;
       const StageMeta ti = tinfo[b];
       if (ti.t == END) break;
@@ -432,6 +444,19 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     T* wval = sb_val + b * CAP + warp * WCAP;
     uint32_t* cnt_b = s_cnt + b * NCH;
     uint32_t running = 0;  // records of this warp in this super-tile (warp-uniform)
+    // Fused apply of this super-tile happens two super-tiles from now: pull
+    // the serving sectors its records will update into L2 while staging, so
+    // the read-modify-writes in flush_slice hit L2 instead of stalling on HBM.
+    const T* pf = nullptr;
+    uint32_t pf_lo = 0, pf_hi = 0;
+    if (a.fuse && a.fuse_on[ti.s]) {
+      const FuseEntry* f = a.fuse + ti.s;
+      if (f->mode == 1) {
+        pf = reinterpret_cast<const T*>(a.serve) + ((int64_t)f->dst_base + f->shift);
+        pf_lo = f->keep_lo;
+        pf_hi = f->keep_hi;
+      }
+    }
 #pragma unroll 1
     for (int g = 0; g < kEncodeSubTiles; ++g) {
       if ((uint32_t)g >= ti.nsub) {
@@ -477,6 +502,10 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           const int e = __ffs(mv) - 1;
           mv &= mv - 1;
           widx[local] = li + e;
+          if (pf) {
+            const uint32_t gi = (uint32_t)e0 + li + e;
+            if (gi >= pf_lo && gi < pf_hi) prefetch_l2(pf + gi);
+          }
           // changed elements are sparse: read them back from the ring
           wval[local] = j < nvec ? Tr::delta(Pe[e], Ne[e])
                                  : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
@@ -504,6 +533,59 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   __syncwarp();
   if (lane == 0)
     for (int b = 0; b < NB; ++b) mbar_arrive(&staged[b]);
+}
+
+// ---- compaction of an unordered K1 output ---------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(1024) compact_kernel(const uint32_t* tile_cnt,
+                                                       const uint32_t* tile_base, uint32_t ntiles,
+                                                       uint64_t cap, const uint32_t* in_idx,
+                                                       const T* in_val, uint32_t* out_idx,
+                                                       T* out_val) {
+  __shared__ uint32_t s_off[1024];
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint64_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t t0 = 0; t0 < ntiles; t0 += 1024) {
+    const uint32_t c = t0 + tid < ntiles ? tile_cnt[t0 + tid] : 0u;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = s_warp[lane];
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    s_off[tid] = s_warp[warp] + inc - c;
+    __syncthreads();
+    const uint64_t carry = s_carry;
+    for (int j = warp; j < 1024 && t0 + j < ntiles; j += 32) {
+      const uint32_t n = tile_cnt[t0 + j];
+      const uint64_t b = tile_base[t0 + j], o = carry + s_off[j];
+      for (uint32_t k = lane; k < n; k += 32)
+        if (b + k < cap && o + k < cap) {
+          out_idx[o + k] = in_idx[b + k];
+          out_val[o + k] = in_val[b + k];
+        }
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry = carry + s_off[1023] + c;
+    __syncthreads();
+  }
 }
 
 // ---- apply (codec.cpp:65-92) ---------------------------------------------------
@@ -880,6 +962,19 @@ cudaError_t launch_gen_bf16(uint64_t key, const int64_t* full, int nd, const ws_
   if (n == 0) return cudaSuccess;
   gen_kernel<<<stream_grid(n, 256), 256, 0, s>>>(key, b, (uint32_t)nd, fs[0], fs[1], fs[2], fs[3],
                                                  n, change_thr, prev, next);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(int dtype, const uint32_t* tile_cnt, const uint32_t* tile_base,
+                           uint32_t ntiles, uint64_t cap, const uint32_t* in_idx,
+                           const void* in_val, uint32_t* out_idx, void* out_val, cudaStream_t s) {
+  if (!ntiles) return cudaSuccess;
+  if (dtype == WS_BF16)
+    compact_kernel<uint16_t><<<1, 1024, 0, s>>>(tile_cnt, tile_base, ntiles, cap, in_idx,
+                                                (const uint16_t*)in_val, out_idx, (uint16_t*)out_val);
+  else
+    compact_kernel<uint32_t><<<1, 1024, 0, s>>>(tile_cnt, tile_base, ntiles, cap, in_idx,
+                                                (const uint32_t*)in_val, out_idx, (uint32_t*)out_val);
   return cudaGetLastError();
 }
 

@@ -23,15 +23,49 @@ __device__ __forceinline__ bool seg_dense(const RouteSideArgs& a, int seg) {
   return !a.sparse || a.seg_nnz[seg] > a.seg_cap[seg];
 }
 
-// Units of one entry: record chunks (sparse) or row-run chunks (dense).
+// Super-tiles [*ta, *tb) of an entry's segment that can hold records for it:
+// an identity route only reads its keep window.
+__device__ __forceinline__ void entry_tiles(const RouteSideArgs& a, const LocalEntry& e,
+                                            uint32_t* ta, uint32_t* tb) {
+  const uint32_t nt = a.tile0[e.seg + 1] - a.tile0[e.seg];
+  if (e.identity) {
+    *ta = e.keep_lo / a.tile_elems;
+    const uint32_t hi = (uint32_t)(((uint64_t)e.keep_hi + a.tile_elems - 1) / a.tile_elems);
+    *tb = hi < nt ? hi : nt;
+    if (*ta > *tb) *ta = *tb;
+  } else {
+    *ta = 0;
+    *tb = nt;
+  }
+}
+
+// Units of one entry: groups of kTilesPerUnit super-tiles of records
+// (sparse) or row-run chunks (dense).
 __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const LocalEntry& e) {
   if (seg_dense(a, e.seg)) {
     const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
     return e.box.rows * per_row;
   }
   if (a.fused && a.fuse_on[e.seg]) return 0;  // K1 applied the sparse records as it wrote them
-  const uint64_t nnz = a.seg_nnz[e.seg];
-  return (nnz + kApplyChunk - 1) / kApplyChunk;
+  if (a.seg_nnz[e.seg] == 0) return 0;
+  uint32_t ta, tb;
+  entry_tiles(a, e, &ta, &tb);
+  return (tb - ta + kTilesPerUnit - 1) / kTilesPerUnit;
+}
+
+// Record range [*k0, *k1) (segment-stream positions) of the super-tile this
+// warp owns in unit lu of entry E; empty when the unit has fewer tiles.
+__device__ __forceinline__ void warp_tile_records(const RouteSideArgs& a, const LocalEntry& E,
+                                                  uint64_t lu, int warp, uint64_t* k0,
+                                                  uint64_t* k1) {
+  uint32_t ta, tb;
+  entry_tiles(a, E, &ta, &tb);
+  const uint64_t t = ta + lu * kTilesPerUnit + (uint64_t)warp;
+  *k0 = *k1 = 0;
+  if (t >= tb) return;
+  const uint32_t gt = a.tile0[E.seg] + (uint32_t)t;
+  *k0 = a.tile_base[gt];
+  *k1 = *k0 + a.tile_cnt[gt];
 }
 
 __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
@@ -107,20 +141,20 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
     const uint64_t lu = u - s_u0;
     __syncthreads();
     if (!seg_dense(a, E.seg)) {
-      const uint64_t nnz = a.seg_nnz[E.seg];
-      const uint64_t k0 = lu * kApplyChunk;
-      const uint64_t k1 = min(nnz, k0 + kApplyChunk);
+      uint64_t k0, k1;
+      warp_tile_records(a, E, lu, threadIdx.x >> 5, &k0, &k1);
       const uint64_t rec = a.seg_rec[E.seg];
       T* dst = serve + E.dst_base;
+      const int lane = threadIdx.x & 31;
       if (E.identity) {
-        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        for (uint64_t k = k0 + lane; k < k1; k += 32) {
           const uint32_t i = __ldg(a.rec_idx + rec + k);
           if (i < E.keep_lo || i >= E.keep_hi) continue;
           const uint64_t d = (uint64_t)((int64_t)i + E.shift);
           dst[d] = Tr::add(dst[d], __ldg(val + rec + k));
         }
       } else {
-        for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        for (uint64_t k = k0 + lane; k < k1; k += 32) {
           const uint64_t d = remap_index(E.map, __ldg(a.rec_idx + rec + k));
           if (d == ~0ull) continue;
           dst[d] = Tr::add(dst[d], __ldg(val + rec + k));
@@ -170,7 +204,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     // every destination must have consumed our previous step's records
     for (int c = 0; c < kMaxWorld; ++c)
       for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
-        if (!wait_geq_sys(P.mailbox + 2 * W + P.dest_rank[c][r], P.epoch - 1))
+        if (!wait_geq_sys(P.mailbox + 2 * W + P.dest_rank[c][r], P.epoch - 1) ||
+            (P.dense_direct && !wait_geq_sys(P.mailbox + 4 * W + P.dest_rank[c][r], P.epoch)))
           atomicOr(P.err, kErrBitTimeout);
   }
   __syncthreads();
@@ -220,11 +255,10 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
       }
     };
     if (!seg_dense(a, E.seg)) {
-      const uint64_t nnz = a.seg_nnz[E.seg];
-      const uint64_t k0 = lu * kApplyChunk;
-      const uint64_t k1 = min(nnz, k0 + kApplyChunk);
+      uint64_t k0, k1;
+      warp_tile_records(a, E, lu, warp, &k0, &k1);
       const uint64_t rec = a.seg_rec[E.seg];
-      for (uint64_t kb = k0 + (uint64_t)warp * 32; kb < k1; kb += (uint64_t)nwarps * 32) {
+      for (uint64_t kb = k0; kb < k1; kb += 32) {
         const uint64_t k = kb + lane;
         bool valid = k < k1;
         uint64_t d = 0;
@@ -350,6 +384,14 @@ __global__ void apply_wire_kernel(const void* recv, uint64_t nrec, typename Trai
 // expected sources, then the grid applies the records in the receive buffer
 // (one contiguous region per source); the last block acks the sources so
 // they may overwrite their regions next step.
+__global__ void p2p_ready_kernel(P2PArgs P) {
+  const int s = threadIdx.x;
+  if (s < P.world && (P.expect_mask & (1u << s))) {
+    __threadfence_system();
+    st_release_sys(P.peer_mailbox[s] + 4 * P.world + P.rank, P.epoch);
+  }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
   const int W = P.world;
@@ -396,6 +438,11 @@ cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s) 
     case WS_F32: pack_kernel<WS_F32><<<grid, 256, 0, s>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_ready(const P2PArgs& p, cudaStream_t s) {
+  p2p_ready_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -5,7 +5,7 @@
 
 namespace wsync {
 
-constexpr uint64_t kApplyChunk = 8192;   // records per apply work unit
+constexpr uint32_t kTilesPerUnit = 8;    // super-tiles of records per work unit (one per warp)
 constexpr uint64_t kCopyChunk = 65536;   // elements per dense-copy work unit
 
 // One (trainer segment -> serving shard) route whose destination is resident
@@ -36,6 +36,12 @@ struct RouteSideArgs {
   const uint64_t* seg_base;     // segment offsets in the trainer arena
   const uint32_t* rec_idx;
   const void* rec_val;
+  // K1's unordered record layout: super-tile t of a segment holds records
+  // [tile_base[t], tile_base[t] + tile_cnt[t]) of the segment's region.
+  const uint32_t* tile0;        // nseg + 1: first global super-tile of every segment
+  const uint32_t* tile_cnt;
+  const uint32_t* tile_base;
+  uint32_t tile_elems;          // elements per super-tile
   const void* train_next;
   void* serve;
   uint64_t* unit_off;           // nentries + 1
@@ -64,7 +70,9 @@ constexpr int kMaxReplicas = 8;
 // Mailbox of every rank (u64 words, in its own HBM, mapped by all peers):
 //   [0, W) records sent by rank s this step   [W, 2W) step flag from s
 //   [2W, 3W) ack of rank g for our last data   [3W] pack blocks done
-//   [3W + 1] apply blocks done
+//   [3W + 1] apply blocks done                 [4W, 5W) rank g reached step e
+// The "reached" flag orders direct dense stores after everything the
+// receiver's own stream did to its serving arena before the sync.
 struct P2PArgs {
   int32_t on;                       // 0: NCCL mode (send region + host exchange)
   int32_t world, rank;
@@ -101,6 +109,10 @@ cudaError_t launch_pack(int dtype, const PackArgs& a, int grid, cudaStream_t s);
 // Receiver side: applies nrec wire records to the serving arena in place.
 cudaError_t launch_apply_wire(int dtype, const void* recv, uint64_t nrec, void* serve,
                              cudaStream_t s);
+
+// P2P receiver, first thing in a sync: tells every source it may store into
+// this rank's serving arena for step p.epoch.
+cudaError_t launch_p2p_ready(const P2PArgs& p, cudaStream_t s);
 
 // P2P receiver: waits for every expected source's step flag, applies all
 // records that arrived in the local receive buffer, acks the sources.

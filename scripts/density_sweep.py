@@ -52,6 +52,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="qwen3-8b")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--densities", default=None, help="comma-separated subset")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -68,7 +69,7 @@ def main():
                    ws.ServeConfig(tp, 1, world // tp), world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=local, unique_id=uid)
     dense_eq = 2 * plan.info.model_elems
-    for d in DENSITIES:
+    for d in ([float(x) for x in args.densities.split(',')] if args.densities else DENSITIES):
         eng.generate(seed=1, density=d)
         rep = eng.sync_step(reverse=False)
         eng.sync_step(reverse=True, report=False)

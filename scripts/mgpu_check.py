@@ -106,11 +106,14 @@ def main():
             bad = ref_case(rank, world, uid, dtype, density, sparse)
             results[f"ref dtype={dtype} d={density} sparse={sparse}"] = bad or "ok"
             ok &= not bad
-    flags = [None] * world
-    dist.all_gather_object(flags, ok)
-    print(json.dumps({"rank": rank, "world": world, "ok": ok, "results": results}), flush=True)
+    # rank 0 prints every rank's line (concurrent writers can interleave)
+    allres = [None] * world
+    dist.all_gather_object(allres, {"rank": rank, "world": world, "ok": ok, "results": results})
+    if rank == 0:
+        for r in allres:
+            print(json.dumps(r), flush=True)
     dist.destroy_process_group()
-    return 0 if all(flags) else 1
+    return 0 if all(r["ok"] for r in allres) else 1
 
 
 if __name__ == "__main__":
