@@ -12,7 +12,7 @@ namespace wsync {
 #define WS_ENC_SUBTILES 4
 #endif
 #ifndef WS_ENC_RING
-#define WS_ENC_RING 3
+#define WS_ENC_RING 4
 #endif
 #ifndef WS_ENC_CONSUMERS
 #define WS_ENC_CONSUMERS 512

@@ -66,86 +66,72 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
 //                completing on per-stage mbarriers;
 //   warps 0-15   consumers: per 16-byte vector the change mask (SWAR bit
 //                compare for bf16, lane compare for i32, value compare for
-//                f32); per (sub-tile, vector slot, warp) chunk the record
-//                count; records ranked with a ballot/popc fast path (shuffle
-//                scan when a lane holds two or more) and staged in the warp's
-//                slice of a 3-deep staging area.  Each stage is released as
-//                soon as it is counted, so HBM streams continuously;
-//   warps 17-19  resolvers (one per staging buffer): scan the chunk counts,
-//                publish the super-tile count, and resolve its offset in its
-//                segment with the decoupled look-back;
-//   each consumer warp writes its own staged records of super-tile i to their
-//   final ascending positions after staging super-tile i+2 (the look-back
-//   has had two super-tile periods), applying them in place to a serving
-//   shard on this GPU when the engine asks for the fused apply.
-// Super-tiles denser than 18.75% spill: records past a warp slice are
-// re-derived from global memory by that warp when it writes them out.
+//                f32); every change is appended to the thread's private
+//                shared-memory slots and marked in the super-tile's change
+//                bitmap -- no warp-level communication per vector.  Each
+//                stage is released as soon as it is read, so HBM streams
+//                continuously;
+//   warps 17-19  resolvers (one per staging buffer): popcount-scan the
+//                bitmap (the ascending rank of every change inside its
+//                super-tile) and place the super-tile in its segment's
+//                stream: one atomic reservation (the engine: super-tiles in
+//                any order, records ascending inside each) or the decoupled
+//                look-back (ws_diff_shards: one ascending stream);
+//   each consumer warp writes its staged records of super-tile i to
+//   base + rank after staging super-tile i + NB - 1, applying them in place
+//   to a serving shard on this GPU when the engine asks for the fused apply.
+// A thread with more than SLOTS changes in one super-tile re-derives the
+// rest from global memory at write-out; the bitmap still gives their ranks.
 struct StageMeta {
   SegDev sg;
   uint32_t t, s, lt, nsub, cnt, last;
   uint32_t pad[2];
 };
 
+#ifndef WS_ENC_SLOTS
+#define WS_ENC_SLOTS 8
+#endif
+
 template <int DT>
 struct EncCfg {
   using T = typename Traits<DT>::T;
-  static constexpr int VE = Traits<DT>::kVE;
+  static constexpr int VE = Traits<DT>::kVE;                          // elements per vector
   static constexpr int NCW = kEncConsumers / 32;                      // consumer warps
   static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  static constexpr uint32_t CAP = SUPER * 3 / WS_ENC_CAPDIV;          // staged records per buffer (18.75%)
-  static constexpr uint32_t WCAP = CAP / NCW;
-  static constexpr int NCH = kEncodeSubTiles * VPT * NCW;             // chunks per super-tile
-  static constexpr int CPW = kEncodeSubTiles * VPT;                   // chunks per consumer warp
-  static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
+  static constexpr int K = WS_ENC_SLOTS;                              // staged changes per thread per super-tile
+  static constexpr uint32_t WORDS = SUPER / 32;                       // change-bitmap words
   static constexpr int NB = kEncBuffers;                              // staging buffers
-  static constexpr size_t kSmem = kRingBytes + NB * (size_t)CAP * (4 + sizeof(T)) +
-                                  NB * NCH * 4 * 2 + NB * NCW * 4 +                   // cnt/off/wrun
-                                  (kRing + NB) * sizeof(StageMeta) + 16 + NB * 8 +
-                                  (2 * kRing + 2 * NB) * 8;
-  static_assert(NCH % 32 == 0, "chunks per lane");
-  static_assert(CPW <= 32 && (CPW & (CPW - 1)) == 0, "chunk search over lanes");
+  static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
+  // per buffer: bitmap u32[WORDS] | word prefix u32[WORDS] | val T[K][threads] | idx u16[K][threads]
+  static constexpr size_t kBufBytes =
+      WORDS * 8 + (size_t)K * kEncConsumers * (sizeof(T) + 2);
+  static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
+                                  (kRing + NB) * sizeof(StageMeta) + NB * 8 +
+                                  (2 * kRing + 2 * NB) * 8 + 32;
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
+  static_assert(SUPER <= 65536, "u16 in-tile index");
+  static_assert(WORDS % 128 == 0, "bitmap words per resolver lane in 16-byte loads");
+  static_assert(kBufBytes % 16 == 0, "buffer alignment");
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
-// Warp exclusive rank of popc(mv) and the warp total: a ballot fast path
-// when no lane holds two or more records, a shuffle scan otherwise.
-__device__ __forceinline__ uint32_t warp_rank(uint32_t mv, uint32_t* tot) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t c = __popc(mv);
-  const unsigned b1 = __ballot_sync(kFullMask, c > 0);
-  const unsigned b2 = __ballot_sync(kFullMask, c > 1);
-  if (!b2) {
-    *tot = __popc(b1);
-    return __popc(b1 & ((1u << lane) - 1u));
-  }
-  uint32_t incl = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
-    if (lane >= o) incl += y;
-  }
-  *tot = __shfl_sync(kFullMask, incl, 31);
-  return incl - c;
-}
-
-// Resolver step for one staged super-tile (one warp): scan the chunk counts
-// into chunk offsets, publish the super-tile's count, resolve its offset in
-// its segment with the decoupled look-back, publish the inclusive prefix.
+// Resolver step for one staged super-tile (one warp): word prefix of the
+// change bitmap, the super-tile's count, and its place in its segment.
 template <int DT>
 __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMeta& ti,
-                                             const uint32_t* s_cnt, uint32_t* s_off,
+                                             const uint32_t* bm, uint32_t* wpre,
                                              unsigned long long* s_prefix) {
   using C = EncCfg<DT>;
-  constexpr int PER = C::NCH / 32;
+  constexpr int PER = C::WORDS / 32;
   const int lane = threadIdx.x & 31;
-  uint32_t loc[PER], sum = 0;
+  const uint4* b4 = reinterpret_cast<const uint4*>(bm + lane * PER);
+  uint32_t sum = 0;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    loc[q] = sum;
-    sum += s_cnt[lane * PER + q];
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 w = b4[q];
+    sum += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
   }
   uint32_t incl = sum;
 #pragma unroll
@@ -154,8 +140,22 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
     if (lane >= o) incl += y;
   }
   const uint32_t count = __shfl_sync(kFullMask, incl, 31);
+  uint32_t run = incl - sum;
+  uint4* p4 = reinterpret_cast<uint4*>(wpre + lane * PER);
 #pragma unroll
-  for (int q = 0; q < PER; ++q) s_off[lane * PER + q] = incl - sum + loc[q];
+  for (int q = 0; q < PER / 4; ++q) {
+    const uint4 w = b4[q];
+    uint4 o;
+    o.x = run;
+    run += __popc(w.x);
+    o.y = run;
+    run += __popc(w.y);
+    o.z = run;
+    run += __popc(w.z);
+    o.w = run;
+    run += __popc(w.w);
+    p4[q] = o;
+  }
   if (a.unordered) {  // one atomic reserves the super-tile's place in its segment
     if (lane == 0) {
       unsigned long long base = 0;
@@ -184,126 +184,164 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
   }
 }
 
-// What a consumer warp keeps (in registers) about a staged super-tile until
-// it writes the records out.
+// What a consumer thread keeps (in registers) about a staged super-tile
+// until it writes the records out.
 struct PendingSlice {
   uint64_t base, rec, cap;
-  uint32_t lt, nsub, cnt, run, seg;
+  uint32_t lt, nsub, cnt, seg;
+  uint32_t mine;  // this thread's changes in the super-tile
 };
 
 // serve[dst(i)] += v for a record of a segment with a local serving shard
 // (codec.cpp:80-91 applied at the moment K1 writes the record).
 template <int DT>
-__device__ __forceinline__ void fuse_apply(const FuseEntry* __restrict__ f,
-                                           typename Traits<DT>::T* serve, uint32_t i,
-                                           typename Traits<DT>::T v) {
+__device__ __forceinline__ typename Traits<DT>::T* fuse_target(const FuseEntry* __restrict__ f,
+                                                                typename Traits<DT>::T* serve,
+                                                                uint32_t i) {
   uint64_t d;
   if (f->mode == 1) {
-    if (i < f->keep_lo || i >= f->keep_hi) return;
+    if (i < f->keep_lo || i >= f->keep_hi) return nullptr;
     d = (uint64_t)((int64_t)i + f->shift);
   } else {
     d = remap_index(f->map, i);
-    if (d == ~0ull) return;
+    if (d == ~0ull) return nullptr;
   }
-  typename Traits<DT>::T* p = serve + f->dst_base + d;
-  *p = Traits<DT>::add(*p, v);
+  return serve + f->dst_base + d;
 }
 
-// A consumer warp writes its own staged records of a resolved super-tile:
-// its slice holds its chunks (g, v) in order; records past the slice
-// capacity (super-tiles denser than 9.4%) are re-derived from global memory.
+#ifndef WS_FLUSH_BATCH
+#define WS_FLUSH_BATCH 2
+#endif
+
+// Ascending rank of in-tile element li among the super-tile's changes.
+__device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint32_t* wpre, uint32_t li) {
+  const uint32_t w = li >> 5;
+  return wpre[w] + __popc(bm[w] & ((1u << (li & 31)) - 1u));
+}
+
+// A consumer warp writes the staged records of its threads for a resolved
+// super-tile (warp-cooperative: record r of the warp is slot r - start(l)
+// of the lane l owning it), then the spilled ones, then clears its bitmap
+// words for the buffer's next super-tile.
 template <int DT>
 __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
-                                            uint64_t prefix, const uint32_t* widx,
-                                            const typename Traits<DT>::T* wval,
-                                            const uint32_t* s_cnt, const uint32_t* s_off) {
+                                            uint64_t prefix, uint32_t* bm, const uint32_t* wpre,
+                                            const uint16_t* sidx,
+                                            const typename Traits<DT>::T* sval) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
-  constexpr int VE = C::VE, NCW = C::NCW, CPW = C::CPW;
-  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, WCAP = C::WCAP;
+  constexpr int VE = C::VE, K = C::K;
+  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t run = ti.run;
-  if (run == 0 || (a.debug & 2) || prefix >= ti.cap) return;
+  if (!__any_sync(kFullMask, ti.mine != 0)) return;  // no bit of this warp is set
   const uint64_t e0 = (uint64_t)ti.lt * SUPER;
-  T* out_val = reinterpret_cast<T*>(a.out_val);
-  const FuseEntry* fz =
-      (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
-  T* serve = reinterpret_cast<T*>(a.serve);
-  const int cl = lane < CPW ? lane : CPW - 1;
-  const uint32_t ccnt = lane < CPW ? s_cnt[cl * NCW + w] : 0u;
-  const uint32_t coff = s_off[cl * NCW + w];
-  uint32_t ci = ccnt;
+  if (!(a.debug & 2) && prefix < ti.cap) {
+    T* out_val = reinterpret_cast<T*>(a.out_val);
+    const FuseEntry* fz =
+        (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
+    T* serve = reinterpret_cast<T*>(a.serve);
+    const uint32_t mine = ti.mine < (uint32_t)K ? ti.mine : (uint32_t)K;
+    uint32_t start = mine;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFullMask, ci, o);
-    if (lane >= o) ci += y;
-  }
-  const uint32_t cstart = ci - ccnt;
-  const uint32_t staged = min(run, WCAP);
-  for (uint32_t k0 = 0; k0 < staged; k0 += 32) {
-    const uint32_t k = k0 + lane;
-    int c = 0;  // owner chunk: the largest c with start(c) <= k
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFullMask, start, o);
+      if (lane >= o) start += y;
+    }
+    const uint32_t staged = __shfl_sync(kFullMask, start, 31);
+    start -= mine;
+    constexpr int FB = WS_FLUSH_BATCH;
+    for (uint32_t r0 = 0; r0 < staged; r0 += 32 * FB) {
+      uint64_t pos[FB];
+      uint32_t ii[FB];
+      T vv[FB], old[FB];
+      T* tp[FB];
 #pragma unroll
-    for (int b = CPW / 2; b > 0; b >>= 1)
-      if (__shfl_sync(kFullMask, cstart, c + b) <= k) c += b;
-    const uint32_t st = __shfl_sync(kFullMask, cstart, c);
-    const uint32_t of = __shfl_sync(kFullMask, coff, c);
-    if (k < staged) {
-      const uint64_t pos = prefix + of + (k - st);
-      if (pos < ti.cap) {
-        const uint32_t i = (uint32_t)(e0 + widx[k]);
-        const T v = wval[k];
-        a.out_idx[ti.rec + pos] = i;
-        out_val[ti.rec + pos] = v;
-        if (fz) fuse_apply<DT>(fz, serve, i, v);
+      for (int j = 0; j < FB; ++j) {
+        const uint32_t r = r0 + j * 32 + lane;
+        int l = 0;  // owner lane: the largest l with start(l) <= r
+#pragma unroll
+        for (int b = 16; b > 0; b >>= 1)
+          if (__shfl_sync(kFullMask, start, l + b) <= r) l += b;
+        const uint32_t st = __shfl_sync(kFullMask, start, l);
+        pos[j] = ~0ull;
+        tp[j] = nullptr;
+        if (r < staged) {
+          const uint32_t slot = (r - st) * kEncConsumers + w * 32 + l;
+          const uint32_t li = sidx[slot];
+          const uint64_t p = prefix + tile_rank(bm, wpre, li);
+          if (p < ti.cap) {
+            pos[j] = p;
+            ii[j] = (uint32_t)(e0 + li);
+            vv[j] = sval[slot];
+            if (fz) tp[j] = fuse_target<DT>(fz, serve, ii[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < FB; ++j)
+        if (tp[j]) old[j] = *tp[j];
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        if (pos[j] == ~0ull) continue;
+        a.out_idx[ti.rec + pos[j]] = ii[j];
+        out_val[ti.rec + pos[j]] = vv[j];
+        if (tp[j]) *tp[j] = Tr::add(old[j], vv[j]);
+      }
+    }
+    if (ti.mine > (uint32_t)K) {  // spill (rare, lane-divergent): changes past the slots
+      const T* prevT = reinterpret_cast<const T*>(a.prev);
+      const T* nextT = reinterpret_cast<const T*>(a.next);
+      uint32_t r = 0;
+      for (uint32_t g = 0; g < ti.nsub; ++g) {
+        for (uint32_t v = 0; v < VPT; ++v) {
+          const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
+          if (li >= ti.cnt) continue;
+          const uint64_t gv = ti.base + e0 + li;  // multiple of VE: 16-byte aligned
+          uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
+          uint32_t mv = 0;
+          if (li + VE <= ti.cnt) {
+            pa = ld_stream(reinterpret_cast<const uint4*>(prevT + gv));
+            pb = ld_stream(reinterpret_cast<const uint4*>(nextT + gv));
+            mv = change_mask<DT>(pa, pb);
+          } else {
+            T ta[VE], tb[VE];
+            for (int e = 0; e < VE; ++e) {
+              const bool in = li + e < ti.cnt;
+              ta[e] = in ? prevT[gv + e] : T(0);
+              tb[e] = in ? nextT[gv + e] : T(0);
+              if (in && Tr::changed(ta[e], tb[e])) mv |= 1u << e;
+            }
+            memcpy(&pa, ta, 16);
+            memcpy(&pb, tb, 16);
+          }
+          while (mv) {
+            const int e = __ffs(mv) - 1;
+            mv &= mv - 1;
+            if (r >= (uint32_t)K) {
+              const uint64_t pos = prefix + tile_rank(bm, wpre, li + e);
+              if (pos < ti.cap) {
+                const T dv = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+                a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
+                out_val[ti.rec + pos] = dv;
+                if (fz) {
+                  T* p = fuse_target<DT>(fz, serve, (uint32_t)(e0 + li + e));
+                  if (p) *p = Tr::add(*p, dv);
+                }
+              }
+            }
+            ++r;
+          }
+        }
       }
     }
   }
-  if (run > WCAP) {  // spill (warp-uniform)
-    const T* prevT = reinterpret_cast<const T*>(a.prev);
-    const T* nextT = reinterpret_cast<const T*>(a.next);
-    for (int g = 0; g < (int)ti.nsub; ++g) {
-      for (int v = 0; v < (int)VPT; ++v) {
-        const int c = g * VPT + v;
-        const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
-        const uint64_t gv = ti.base + e0 + li;  // multiple of VE: 16-byte aligned
-        uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
-        uint32_t mv = 0;
-        if (li + VE <= ti.cnt) {
-          pa = ld_stream(reinterpret_cast<const uint4*>(prevT + gv));
-          pb = ld_stream(reinterpret_cast<const uint4*>(nextT + gv));
-          mv = change_mask<DT>(pa, pb);
-        } else {
-          T ta[VE], tb[VE];
-          for (int e = 0; e < VE; ++e) {
-            const bool in = li + e < ti.cnt;
-            ta[e] = in ? prevT[gv + e] : T(0);
-            tb[e] = in ? nextT[gv + e] : T(0);
-            if (in && Tr::changed(ta[e], tb[e])) mv |= 1u << e;
-          }
-          memcpy(&pa, ta, 16);
-          memcpy(&pb, tb, 16);
-        }
-        uint32_t tot;
-        uint32_t r = warp_rank(mv, &tot);
-        const uint32_t st = __shfl_sync(kFullMask, cstart, c);
-        const uint32_t of = __shfl_sync(kFullMask, coff, c);
-        while (mv) {
-          const int e = __ffs(mv) - 1;
-          mv &= mv - 1;
-          const uint64_t pos = prefix + of + r;
-          if (st + r >= WCAP && pos < ti.cap) {
-            const T v = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
-            a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
-            out_val[ti.rec + pos] = v;
-            if (fz) fuse_apply<DT>(fz, serve, (uint32_t)(e0 + li + e), v);
-          }
-          ++r;
-        }
-      }
-    }
-  }
+  __syncwarp();  // every lane of the warp is done reading the bitmap
+  constexpr uint32_t LPW = 32 / VE;  // lanes sharing one bitmap word
+  if ((threadIdx.x & (LPW - 1)) == 0)
+    for (uint32_t g = 0; g < ti.nsub; ++g)
+      for (uint32_t v = 0; v < VPT; ++v)
+        bm[(g * SUB + (v * kEncConsumers + threadIdx.x) * VE) >> 5] = 0;
 }
 
 template <int DT>
@@ -311,29 +349,31 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
-  constexpr int VE = C::VE, NCW = C::NCW, NCH = C::NCH, NB = C::NB;
-  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, CAP = C::CAP, WCAP = C::WCAP;
+  constexpr int VE = C::VE, NCW = C::NCW, NB = C::NB, K = C::K;
+  constexpr uint32_t VPT = C::VPT, SUB = C::SUB, SUPER = C::SUPER, WORDS = C::WORDS;
   constexpr uint32_t END = 0xffffffffu;
 
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring_prev = dsm;
   uint8_t* ring_next = dsm + kRing * kStageBytes;
-  uint32_t* sb_idx = reinterpret_cast<uint32_t*>(dsm + C::kRingBytes);  // [NB][CAP]
-  T* sb_val = reinterpret_cast<T*>(sb_idx + NB * CAP);                  // [NB][CAP]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(sb_val + NB * CAP) + 3) & ~uintptr_t(3));  // [NB][NCH]
-  uint32_t* s_off = s_cnt + NB * NCH;                                   // [NB][NCH]
-  uint32_t* s_wrun = s_off + NB * NCH;                                  // [NB][NCW]
-  StageMeta* meta = reinterpret_cast<StageMeta*>(
-      (reinterpret_cast<uintptr_t>(s_wrun + NB * NCW) + 15) & ~uintptr_t(15));  // [kRing]
-  StageMeta* tinfo = meta + kRing;                                      // [NB]
+  uint8_t* bufs = dsm + C::kRingBytes;  // NB x kBufBytes
+  auto buf_bm = [&](int b) { return reinterpret_cast<uint32_t*>(bufs + b * C::kBufBytes); };
+  auto buf_wpre = [&](int b) { return buf_bm(b) + WORDS; };
+  auto buf_val = [&](int b) { return reinterpret_cast<T*>(buf_wpre(b) + WORDS); };
+  auto buf_idx = [&](int b) {
+    return reinterpret_cast<uint16_t*>(buf_val(b) + (size_t)K * kEncConsumers);
+  };
+  StageMeta* meta = reinterpret_cast<StageMeta*>(bufs + NB * C::kBufBytes);  // [kRing]
+  StageMeta* tinfo = meta + kRing;                                          // [NB]
   unsigned long long* s_prefix = reinterpret_cast<unsigned long long*>(tinfo + NB);  // [NB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + NB);          // [kRing]
-  uint64_t* empty = full + kRing;                                       // [kRing]
-  uint64_t* staged = empty + kRing;                                     // [NB]
-  uint64_t* resolved = staged + NB;                                     // [NB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + NB);              // [kRing]
+  uint64_t* empty = full + kRing;                                           // [kRing]
+  uint64_t* staged = empty + kRing;                                         // [NB]
+  uint64_t* resolved = staged + NB;                                         // [NB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t i = tid; i < NB * WORDS; i += blockDim.x)
+    buf_bm(i / WORDS)[i % WORDS] = 0;
   if (tid == 0) {
     for (int k = 0; k < kRing; ++k) {
       mbar_init(&full[k], 1);
@@ -405,11 +445,11 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     const int b = warp - NCW - 1;
     uint32_t par = 0;
     while (true) {
-      mbar_wait(&staged[b], par);  // suspended in hardware while idle
+      mbar_wait(&staged[b], par);
       par ^= 1u;
       const StageMeta ti = tinfo[b];
       if (ti.t == END) break;
-      resolve_tile<DT>(a, ti, s_cnt + b * NCH, s_off + b * NCH, &s_prefix[b]);
+      resolve_tile<DT>(a, ti, buf_bm(b), buf_wpre(b), &s_prefix[b]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&resolved[b]);
     }
@@ -422,15 +462,14 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       if (a.segs[s].n == 0) a.seg_nnz[s] = 0;
   }
   // Super-tile i is staged in buffer i % NB and written out after super-tile
-  // i + NB - 1 is staged, so its look-back has NB - 1 periods to complete.
+  // i + NB - 1 is staged, so its placement has NB - 1 periods to complete.
   static_assert(NB == 3, "two pending super-tiles are kept in registers");
   auto flush_tile = [&](int pb, const PendingSlice& p, uint32_t& rbits) {
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
-    flush_slice<DT>(a, p, s_prefix[pb], sb_idx + pb * CAP + warp * WCAP,
-                    sb_val + pb * CAP + warp * WCAP, s_cnt + pb * NCH, s_off + pb * NCH);
+    flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb));
   };
-  PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this warp
+  PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this thread
   uint32_t fbits = 0, rbits = 0;
   int k = 0;
   uint32_t i = 0;
@@ -440,29 +479,12 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (meta[k].t == END) break;
     const StageMeta ti = meta[k];
     const uint64_t e0 = (uint64_t)ti.lt * SUPER;
-    uint32_t* widx = sb_idx + b * CAP + warp * WCAP;
-    T* wval = sb_val + b * CAP + warp * WCAP;
-    uint32_t* cnt_b = s_cnt + b * NCH;
-    uint32_t running = 0;  // records of this warp in this super-tile (warp-uniform)
-    // Fused apply of this super-tile happens two super-tiles from now: pull
-    // the serving sectors its records will update into L2 while staging, so
-    // the read-modify-writes in flush_slice hit L2 instead of stalling on HBM.
-    const T* pf = nullptr;
-    uint32_t pf_lo = 0, pf_hi = 0;
-    if (a.fuse && a.fuse_on[ti.s]) {
-      const FuseEntry* f = a.fuse + ti.s;
-      if (f->mode == 1) {
-        pf = reinterpret_cast<const T*>(a.serve) + ((int64_t)f->dst_base + f->shift);
-        pf_lo = f->keep_lo;
-        pf_hi = f->keep_hi;
-      }
-    }
+    uint32_t* bm = buf_bm(b);
+    T* sval = buf_val(b) + tid;
+    uint16_t* sidx = buf_idx(b) + tid;
+    uint32_t mine = 0;  // this thread's changes in this super-tile
 #pragma unroll 1
-    for (int g = 0; g < kEncodeSubTiles; ++g) {
-      if ((uint32_t)g >= ti.nsub) {
-        if (lane < (int)VPT) cnt_b[(g * VPT + lane) * NCW + warp] = 0;
-        continue;
-      }
+    for (int g = 0; g < (int)ti.nsub; ++g) {
       const int kk = (k + g) % kRing;
       if (g > 0) mbar_wait(&full[kk], (fbits >> kk) & 1u);
       fbits ^= 1u << kk;
@@ -473,7 +495,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
 #pragma unroll
       for (uint32_t v = 0; v < VPT; ++v) {
         const uint32_t j = v * kEncConsumers + tid;
-        uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
+        uint4 pa, pb;
         uint32_t mv = 0;
         if (j < nvec) {
           pa = P[j];
@@ -492,26 +514,23 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           memcpy(&pa, ta, 16);
           memcpy(&pb, tb, 16);
         }
-        uint32_t tot;
-        uint32_t local = running + warp_rank(mv, &tot);
-        if (lane == 0) cnt_b[(g * VPT + v) * NCW + warp] = tot;
-        const uint32_t li = g * SUB + j * VE;
-        const T* Pe = reinterpret_cast<const T*>(P) + (size_t)j * VE;
-        const T* Ne = reinterpret_cast<const T*>(N) + (size_t)j * VE;
-        while (mv && local < WCAP) {
-          const int e = __ffs(mv) - 1;
-          mv &= mv - 1;
-          widx[local] = li + e;
-          if (pf) {
-            const uint32_t gi = (uint32_t)e0 + li + e;
-            if (gi >= pf_lo && gi < pf_hi) prefetch_l2(pf + gi);
-          }
-          // changed elements are sparse: read them back from the ring
-          wval[local] = j < nvec ? Tr::delta(Pe[e], Ne[e])
-                                 : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
-          ++local;
+        if (mv) {
+          const uint32_t li = g * SUB + j * VE;
+          atomicOr(bm + (li >> 5), mv << (li & 31));
+          const T* Pe = reinterpret_cast<const T*>(P) + (size_t)j * VE;
+          const T* Ne = reinterpret_cast<const T*>(N) + (size_t)j * VE;
+          do {
+            const int e = __ffs(mv) - 1;
+            mv &= mv - 1;
+            if (mine < (uint32_t)K) {
+              sidx[mine * kEncConsumers] = (uint16_t)(li + e);
+              // changed elements are sparse: read them back from the ring
+              sval[mine * kEncConsumers] = j < nvec ? Tr::delta(Pe[e], Ne[e])
+                                                    : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+            }
+            ++mine;
+          } while (mv);
         }
-        running += tot;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
@@ -522,7 +541,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (lane == 0) mbar_arrive(&staged[b]);
     if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);  // super-tile i-2
     pend0 = pend1;
-    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, running, ti.s};
+    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, ti.s, mine};
   }
   // ---- drain: write out the pending super-tiles, then stop the resolvers
   if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);

@@ -32,6 +32,7 @@ def timed(eng, steps, **kw):
     if dist.is_initialized():
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.timing(reset=True)
     s.record()
     for _ in range(steps):
         eng.sync_step(reverse=rev, report=False, **kw)
@@ -39,6 +40,9 @@ def timed(eng, steps, **kw):
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
+    tm = eng.timing(reset=True)
+    timed.stages = {k: round(tm[k] * 1e3 / max(1, tm["steps"]), 3)
+                    for k in ("encode_s", "apply_s", "route_s") if k in tm}
     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -74,6 +78,7 @@ def main():
         rep = eng.sync_step(reverse=False)
         eng.sync_step(reverse=True, report=False)
         ms_sparse = timed(eng, args.steps, sparse=True, density_threshold=0.20)
+        stages = timed.stages
         ms_dense = timed(eng, args.steps, sparse=False)
         if rank == 0:
             print(json.dumps({
@@ -82,7 +87,7 @@ def main():
                 "sparse_gbs": round(dense_eq / ms_sparse / 1e6, 1),
                 "dense_gbs": round(dense_eq / ms_dense / 1e6, 1),
                 "sparse_shards": rep["sparse_shards"], "dense_shards": rep["dense_shards"],
-                "sparse_faster": ms_sparse < ms_dense}), flush=True)
+                "sparse_faster": ms_sparse < ms_dense, "sparse_stages_ms": stages}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
