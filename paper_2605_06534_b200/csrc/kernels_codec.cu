@@ -82,6 +82,8 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
 //   to a serving shard on this GPU when the engine asks for the fused apply.
 // A thread with more than SLOTS changes in one super-tile re-derives the
 // rest from global memory at write-out; the bitmap still gives their ranks.
+constexpr int kStagedBar = 2;  // named barriers 2.. : "super-tile staged in buffer b"
+
 struct StageMeta {
   SegDev sg;
   uint32_t t, s, lt, nsub, cnt, last;
@@ -89,7 +91,13 @@ struct StageMeta {
 };
 
 #ifndef WS_ENC_SLOTS
-#define WS_ENC_SLOTS 8
+#define WS_ENC_SLOTS 6
+#endif
+#ifndef WS_ENC_PREFETCH
+#define WS_ENC_PREFETCH 1
+#endif
+#ifndef WS_ENC_EVICT
+#define WS_ENC_EVICT 0  // (measured: no gain) prev/next streamed evict-first, prefetched serving words evict-last
 #endif
 
 template <int DT>
@@ -103,10 +111,14 @@ struct EncCfg {
   static constexpr int K = WS_ENC_SLOTS;                              // staged changes per thread per super-tile
   static constexpr uint32_t WORDS = SUPER / 32;                       // change-bitmap words
   static constexpr int NB = kEncBuffers;                              // staging buffers
+  // bf16: the serving word a fused record updates is fetched (cp.async) into
+  // shared memory when the record is staged
+  static constexpr bool PRE = WS_ENC_PREFETCH && DT == WS_BF16;
   static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
-  // per buffer: bitmap u32[WORDS] | word prefix u32[WORDS] | val T[K][threads] | idx u16[K][threads]
+  // per buffer: bitmap u32[WORDS] | [serving words u32[K][threads]] | val T[K][threads] |
+  //             word prefix u16[WORDS] | idx u16[K][threads]
   static constexpr size_t kBufBytes =
-      WORDS * 8 + (size_t)K * kEncConsumers * (sizeof(T) + 2);
+      WORDS * 6 + (size_t)K * kEncConsumers * (sizeof(T) + 2 + (PRE ? 4 : 0));
   static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
                                   (kRing + NB) * sizeof(StageMeta) + NB * 8 +
                                   (2 * kRing + 2 * NB) * 8 + 32;
@@ -121,7 +133,7 @@ struct EncCfg {
 // change bitmap, the super-tile's count, and its place in its segment.
 template <int DT>
 __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMeta& ti,
-                                             const uint32_t* bm, uint32_t* wpre,
+                                             const uint32_t* bm, uint16_t* wpre,
                                              unsigned long long* s_prefix) {
   using C = EncCfg<DT>;
   constexpr int PER = C::WORDS / 32;
@@ -140,21 +152,21 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
     if (lane >= o) incl += y;
   }
   const uint32_t count = __shfl_sync(kFullMask, incl, 31);
-  uint32_t run = incl - sum;
-  uint4* p4 = reinterpret_cast<uint4*>(wpre + lane * PER);
+  uint32_t run = incl - sum;  // < 2^16: at most SUPER - 32
+  uint2* p2 = reinterpret_cast<uint2*>(wpre + lane * PER);
 #pragma unroll
   for (int q = 0; q < PER / 4; ++q) {
     const uint4 w = b4[q];
-    uint4 o;
+    uint2 o;
     o.x = run;
     run += __popc(w.x);
-    o.y = run;
+    o.x |= run << 16;
     run += __popc(w.y);
-    o.z = run;
+    o.y = run;
     run += __popc(w.z);
-    o.w = run;
+    o.y |= run << 16;
     run += __popc(w.w);
-    p4[q] = o;
+    p2[q] = o;
   }
   if (a.unordered) {  // one atomic reserves the super-tile's place in its segment
     if (lane == 0) {
@@ -214,7 +226,7 @@ __device__ __forceinline__ typename Traits<DT>::T* fuse_target(const FuseEntry* 
 #endif
 
 // Ascending rank of in-tile element li among the super-tile's changes.
-__device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint32_t* wpre, uint32_t li) {
+__device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint16_t* wpre, uint32_t li) {
   const uint32_t w = li >> 5;
   return wpre[w] + __popc(bm[w] & ((1u << (li & 31)) - 1u));
 }
@@ -225,9 +237,10 @@ __device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint32_t
 // words for the buffer's next super-tile.
 template <int DT>
 __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
-                                            uint64_t prefix, uint32_t* bm, const uint32_t* wpre,
+                                            uint64_t prefix, uint32_t* bm, const uint16_t* wpre,
                                             const uint16_t* sidx,
-                                            const typename Traits<DT>::T* sval) {
+                                            const typename Traits<DT>::T* sval,
+                                            const uint32_t* spre) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
@@ -240,6 +253,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
     T* out_val = reinterpret_cast<T*>(a.out_val);
     const FuseEntry* fz =
         (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
+    // identity-mapped fused segments had their serving words fetched at staging
+    const bool pre = C::PRE && fz && fz->mode == 1;
     T* serve = reinterpret_cast<T*>(a.serve);
     const uint32_t mine = ti.mine < (uint32_t)K ? ti.mine : (uint32_t)K;
     uint32_t start = mine;
@@ -253,7 +268,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
     constexpr int FB = WS_FLUSH_BATCH;
     for (uint32_t r0 = 0; r0 < staged; r0 += 32 * FB) {
       uint64_t pos[FB];
-      uint32_t ii[FB];
+      uint32_t ii[FB], sl[FB];
       T vv[FB], old[FB];
       T* tp[FB];
 #pragma unroll
@@ -268,6 +283,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         tp[j] = nullptr;
         if (r < staged) {
           const uint32_t slot = (r - st) * kEncConsumers + w * 32 + l;
+          sl[j] = slot;
           const uint32_t li = sidx[slot];
           const uint64_t p = prefix + tile_rank(bm, wpre, li);
           if (p < ti.cap) {
@@ -280,7 +296,14 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
       }
 #pragma unroll
       for (int j = 0; j < FB; ++j)
-        if (tp[j]) old[j] = *tp[j];
+        if (tp[j]) {
+          if (pre) {  // the half of the prefetched word holding the element
+            const uint32_t wv = spre[sl[j]];
+            old[j] = (T)((reinterpret_cast<uintptr_t>(tp[j]) & 2) ? (wv >> 16) : (wv & 0xffffu));
+          } else {
+            old[j] = *tp[j];
+          }
+        }
 #pragma unroll
       for (int j = 0; j < FB; ++j) {
         if (pos[j] == ~0ull) continue;
@@ -358,18 +381,20 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   uint8_t* ring_next = dsm + kRing * kStageBytes;
   uint8_t* bufs = dsm + C::kRingBytes;  // NB x kBufBytes
   auto buf_bm = [&](int b) { return reinterpret_cast<uint32_t*>(bufs + b * C::kBufBytes); };
-  auto buf_wpre = [&](int b) { return buf_bm(b) + WORDS; };
-  auto buf_val = [&](int b) { return reinterpret_cast<T*>(buf_wpre(b) + WORDS); };
-  auto buf_idx = [&](int b) {
+  auto buf_pre = [&](int b) { return buf_bm(b) + WORDS; };  // K x threads words when PRE
+  auto buf_val = [&](int b) {
+    return reinterpret_cast<T*>(buf_pre(b) + (C::PRE ? (size_t)K * kEncConsumers : 0));
+  };
+  auto buf_wpre = [&](int b) {
     return reinterpret_cast<uint16_t*>(buf_val(b) + (size_t)K * kEncConsumers);
   };
+  auto buf_idx = [&](int b) { return buf_wpre(b) + WORDS; };
   StageMeta* meta = reinterpret_cast<StageMeta*>(bufs + NB * C::kBufBytes);  // [kRing]
   StageMeta* tinfo = meta + kRing;                                          // [NB]
   unsigned long long* s_prefix = reinterpret_cast<unsigned long long*>(tinfo + NB);  // [NB]
   uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + NB);              // [kRing]
   uint64_t* empty = full + kRing;                                           // [kRing]
-  uint64_t* staged = empty + kRing;                                         // [NB]
-  uint64_t* resolved = staged + NB;                                         // [NB]
+  uint64_t* resolved = empty + kRing;                                       // [NB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t i = tid; i < NB * WORDS; i += blockDim.x)
@@ -379,10 +404,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       mbar_init(&full[k], 1);
       mbar_init(&empty[k], NCW);
     }
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&staged[b], NCW);
-      mbar_init(&resolved[b], 1);
-    }
+    for (int b = 0; b < NB; ++b) mbar_init(&resolved[b], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -393,6 +415,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     // ---------------- producer ----------------
     if (lane == 0) {
       uint32_t ebits = (1u << kRing) - 1u;  // the first wait on each empty barrier passes
+      const uint64_t pol = policy_evict_first();
       int k = 0;
       while (true) {
         // Claimed only when the ring can take it: claiming further ahead
@@ -430,8 +453,13 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           mbar_arrive_expect_tx(&full[k], 2 * bytes);
           if (bytes) {
             const uint64_t el = sg.base + e0 + (uint64_t)g * SUB;
-            tma_load_1d(ring_prev + k * kStageBytes, prevT + el, bytes, &full[k]);
-            tma_load_1d(ring_next + k * kStageBytes, nextT + el, bytes, &full[k]);
+            if (WS_ENC_EVICT) {
+              tma_load_1d_hint(ring_prev + k * kStageBytes, prevT + el, bytes, &full[k], pol);
+              tma_load_1d_hint(ring_next + k * kStageBytes, nextT + el, bytes, &full[k], pol);
+            } else {
+              tma_load_1d(ring_prev + k * kStageBytes, prevT + el, bytes, &full[k]);
+              tma_load_1d(ring_next + k * kStageBytes, nextT + el, bytes, &full[k]);
+            }
           }
           k = (k + 1) % kRing;
         }
@@ -443,10 +471,9 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   if (warp > NCW) {
     // ---------------- resolvers: warp NCW+1+b owns staging buffer b ----------------
     const int b = warp - NCW - 1;
-    uint32_t par = 0;
     while (true) {
-      mbar_wait(&staged[b], par);
-      par ^= 1u;
+      // blocked in hardware (no polling) until the 16 consumer warps arrive
+      named_barrier(kStagedBar + b, kEncConsumers + 32);
       const StageMeta ti = tinfo[b];
       if (ti.t == END) break;
       resolve_tile<DT>(a, ti, buf_bm(b), buf_wpre(b), &s_prefix[b]);
@@ -464,12 +491,18 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   // Super-tile i is staged in buffer i % NB and written out after super-tile
   // i + NB - 1 is staged, so its placement has NB - 1 periods to complete.
   static_assert(NB == 3, "two pending super-tiles are kept in registers");
-  auto flush_tile = [&](int pb, const PendingSlice& p, uint32_t& rbits) {
+  auto flush_tile = [&](int pb, const PendingSlice& p, uint32_t& rbits, bool drain) {
+    if (C::PRE) {  // this super-tile's serving words are in (the two later groups may not be)
+      if (drain) cp_async_wait<0>(); else cp_async_wait<2>();
+      __syncwarp();
+    }
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
-    flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb));
+    flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
+                    buf_pre(pb));
   };
   PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this thread
+  const uint64_t pol_keep = policy_evict_last();
   uint32_t fbits = 0, rbits = 0;
   int k = 0;
   uint32_t i = 0;
@@ -482,7 +515,18 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     uint32_t* bm = buf_bm(b);
     T* sval = buf_val(b) + tid;
     uint16_t* sidx = buf_idx(b) + tid;
+    uint32_t* spre = buf_pre(b) + tid;
     uint32_t mine = 0;  // this thread's changes in this super-tile
+    const T* pf = nullptr;  // fused identity segment: serving element of in-tile index 0
+    uint32_t pf_lo = 0, pf_n = 0;
+    if (C::PRE && a.fuse && a.fuse_on[ti.s]) {
+      const FuseEntry* f = a.fuse + ti.s;
+      if (f->mode == 1) {
+        pf = reinterpret_cast<const T*>(a.serve) + ((int64_t)f->dst_base + f->shift) + e0;
+        pf_lo = f->keep_lo > e0 ? (uint32_t)(f->keep_lo - e0) : 0u;
+        pf_n = f->keep_hi > e0 + pf_lo ? (uint32_t)(f->keep_hi - e0 - pf_lo) : 0u;
+      }
+    }
 #pragma unroll 1
     for (int g = 0; g < (int)ti.nsub; ++g) {
       const int kk = (k + g) % kRing;
@@ -524,6 +568,12 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
             mv &= mv - 1;
             if (mine < (uint32_t)K) {
               sidx[mine * kEncConsumers] = (uint16_t)(li + e);
+              if (C::PRE && pf && li + e - pf_lo < pf_n) {
+                const void* src = reinterpret_cast<const void*>(
+                    reinterpret_cast<uintptr_t>(pf + li + e) & ~uintptr_t(3));
+                if (WS_ENC_EVICT) cp_async4_hint(spre + mine * kEncConsumers, src, pol_keep);
+                else cp_async4(spre + mine * kEncConsumers, src);
+              }
               // changed elements are sparse: read them back from the ring
               sval[mine * kEncConsumers] = j < nvec ? Tr::delta(Pe[e], Ne[e])
                                                     : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
@@ -536,22 +586,22 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
     }
     k = (k + ti.nsub) % kRing;
+    if (C::PRE) cp_async_commit();  // one group per super-tile
     if (tid == 0) tinfo[b] = ti;  // for the resolver only
     __syncwarp();
-    if (lane == 0) mbar_arrive(&staged[b]);
-    if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);  // super-tile i-2
+    named_arrive(kStagedBar + b, kEncConsumers + 32);
+    if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, false);  // super-tile i-2
     pend0 = pend1;
     pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, ti.s, mine};
   }
   // ---- drain: write out the pending super-tiles, then stop the resolvers
-  if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits);
-  if (i >= 1) flush_tile((int)((i - 1) % NB), pend1, rbits);
+  if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, true);
+  if (i >= 1) flush_tile((int)((i - 1) % NB), pend1, rbits, true);
   named_barrier(1, kEncConsumers);  // every warp is past its last use of tinfo
   if (tid == 0)
     for (int b = 0; b < NB; ++b) tinfo[b].t = END;
   __syncwarp();
-  if (lane == 0)
-    for (int b = 0; b < NB; ++b) mbar_arrive(&staged[b]);
+  for (int b = 0; b < NB; ++b) named_arrive(kStagedBar + b, kEncConsumers + 32);
 }
 
 // ---- compaction of an unordered K1 output ---------------------------------------
