@@ -162,6 +162,21 @@ ws_status ws_gen_pair_bf16(uint64_t seed, const char* param_name,
                            uint64_t change_thr, uint16_t* prev_dev,
                            uint16_t* next_dev, ws_stream_t stream);
 
+/* Same with a change threshold per index along dim 0 (thr_dim0_dev: device
+ * array of full_shape[0] entries), e.g. per-expert densities of a stacked
+ * [E, ...] expert tensor. */
+ws_status ws_gen_pair_bf16_dim0(uint64_t seed, const char* param_name,
+                                const int64_t* full_shape, int ndims, ws_shard desc,
+                                const uint64_t* thr_dim0_dev, uint16_t* prev_dev,
+                                uint16_t* next_dev, ws_stream_t stream);
+
+/* Skewed per-expert change densities (BASELINE config 4): Zipf(zipf_s)
+ * weights over the ranks 1..experts, normalised to mean 1, assigned to the
+ * experts by a Fisher-Yates shuffle driven by splitmix64(perm_seed + k);
+ * out[e] = floor(min(1, density * weight) * 2^32). */
+ws_status ws_expert_thresholds(int experts, double density, double zipf_s,
+                               uint64_t perm_seed, uint64_t* out);
+
 /* ------------------------------------------------------------------------ */
 /* Planner (host, plan.hpp / shard.hpp)                                      */
 /* ------------------------------------------------------------------------ */
@@ -278,6 +293,11 @@ ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev,
  * serving arena with the matching `prev` values (ServeState::init). */
 ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density,
                              ws_stream_t stream);
+
+/* Same, with the change density of every EXPERT-kind tensor skewed per
+ * expert (ws_expert_thresholds(E, density, zipf_s, perm_seed)). */
+ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double density,
+                                   double zipf_s, uint64_t perm_seed, ws_stream_t stream);
 
 /* One sync on `stream`.  When report is non-null the call synchronises and
  * fills it; otherwise it only enqueues (graph-capturable when world == 1). */

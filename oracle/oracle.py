@@ -78,6 +78,8 @@ class Restatement:
         L.wso_is_sparse.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
         L.wso_param_key.argtypes = [C.c_uint64, C.c_char_p]
         L.wso_param_key.restype = C.c_uint64
+        L.wso_gen_pair_bf16_dim0.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_int, C.c_int64,
+                                             C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.wso_gen_pair_bf16.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_int, C.c_int64,
                                         C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p]
         L.wso_sparse_payload_size.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64]
@@ -147,10 +149,16 @@ class Restatement:
     def param_key(self, seed, name):
         return self.lib.wso_param_key(seed, name.encode())
 
-    def gen_pair_bf16(self, seed, name, full_shape, desc, density):
+    def gen_pair_bf16(self, seed, name, full_shape, desc, density, thr_dim0=None):
         n = shard_elems(full_shape, desc)
         prev = np.empty(n, np.uint16)
         nxt = np.empty(n, np.uint16)
+        if thr_dim0 is not None:
+            tab = np.ascontiguousarray(thr_dim0, np.uint64)
+            self.lib.wso_gen_pair_bf16_dim0(self.param_key(seed, name), _shape(full_shape),
+                                            len(full_shape), desc[0], desc[1], desc[2],
+                                            _ptr(tab), _ptr(prev), _ptr(nxt))
+            return prev, nxt
         self.lib.wso_gen_pair_bf16(self.param_key(seed, name), _shape(full_shape),
                                    len(full_shape), desc[0], desc[1], desc[2],
                                    change_threshold(density), _ptr(prev), _ptr(nxt))
@@ -167,6 +175,31 @@ class Restatement:
         if rc:
             raise OracleError(rc)
         return out[:n.value].tobytes()
+
+
+def expert_thresholds(experts, density, zipf_s, perm_seed=0):
+    """Config 4's per-expert change thresholds (Zipf(s) over
+    the experts, normalised to mean density), restated in plain Python:
+    weights r^-s of ranks 1..E, ranks assigned by a Fisher-Yates shuffle
+    driven by splitmix64(perm_seed + k * golden) (the rng.hpp:73-78 mixer)."""
+    M = (1 << 64) - 1
+    w = [float(r + 1) ** (-zipf_s) for r in range(experts)]
+    total = sum(w)
+    rank = list(range(experts))
+    st = perm_seed & M
+    for i in range(experts - 1, 0, -1):
+        st = (st + 0x9E3779B97F4A7C15) & M
+        x = st
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        x ^= x >> 31
+        j = x % (i + 1)
+        rank[i], rank[j] = rank[j], rank[i]
+    out = []
+    for e in range(experts):
+        d = min(max(density * w[rank[e]] * experts / total, 0.0), 1.0)
+        out.append(int(d * 4294967296.0))
+    return out
 
 
 def change_threshold(density):

@@ -283,6 +283,24 @@ void wso_gen_pair_bf16(uint64_t key, const int64_t* full_shape, int ndims,
   }
 }
 
+void wso_gen_pair_bf16_dim0(uint64_t key, const int64_t* full_shape, int ndims,
+                            int dim, int64_t start, int64_t end,
+                            const uint64_t* thr_dim0, uint16_t* prev, uint16_t* next) {
+  const box_t S = shard_box(full_shape, ndims, dim, start, end);
+  const uint64_t n = box_elems(&S);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t rem = i, g = 0, mul = 1, c0 = 0;
+    for (int d = ndims - 1; d >= 0; --d) {
+      const uint64_t c = rem % (uint64_t)S.ext[d] + (uint64_t)S.lo[d];
+      rem /= (uint64_t)S.ext[d];
+      g += c * mul;
+      mul *= (uint64_t)full_shape[d];
+      c0 = c;
+    }
+    gen_elem(key, g, thr_dim0[c0], &prev[i], &next[i]);
+  }
+}
+
 /* ---- sparse payload: codec.cpp:145-183 ------------------------------------ */
 uint64_t wso_sparse_payload_size(int dtype, int ndims, int index_width,
                                  uint64_t nnz) {

@@ -92,6 +92,10 @@ uint64_t wso_param_key(uint64_t seed, const char* name);
 void wso_gen_pair_bf16(uint64_t key, const int64_t* full_shape, int ndims,
                        int dim, int64_t start, int64_t end,
                        uint64_t change_thr, uint16_t* prev, uint16_t* next);
+/* Same with a threshold per index along dim 0 (per-expert densities). */
+void wso_gen_pair_bf16_dim0(uint64_t key, const int64_t* full_shape, int ndims,
+                            int dim, int64_t start, int64_t end,
+                            const uint64_t* thr_dim0, uint16_t* prev, uint16_t* next);
 
 /* Sparse wire payload, codec.cpp:145-183 (encode) and :196-263 (decode).
  * dtype 2 (BF16) uses magic "CWS2"/"CWD2" and 2-byte values (DESIGN.md

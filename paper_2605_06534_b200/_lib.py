@@ -146,6 +146,9 @@ _SIGS = {
     "ws_extract_shard": ([C.c_int, C.POINTER(_i64), C.c_int, Shard, _vp, _vp, _vp], C.c_int),
     "ws_gen_pair_bf16": ([_u64, C.c_char_p, C.POINTER(_i64), C.c_int, Shard, _u64, _vp, _vp,
                           _vp], C.c_int),
+    "ws_gen_pair_bf16_dim0": ([_u64, C.c_char_p, C.POINTER(_i64), C.c_int, Shard, _vp, _vp, _vp,
+                               _vp], C.c_int),
+    "ws_expert_thresholds": ([C.c_int, C.c_double, C.c_double, _u64, C.POINTER(_u64)], C.c_int),
     "ws_plan_create": ([C.POINTER(Param), C.c_int, C.c_int, C.POINTER(TrainLayout),
                         C.POINTER(ServeLayout), C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "ws_plan_destroy": ([_vp], None),
@@ -162,6 +165,7 @@ _SIGS = {
     "ws_engine_destroy": ([_vp], None),
     "ws_engine_bind": ([_vp, _vp, _vp, _vp], C.c_int),
     "ws_engine_generate": ([_vp, _u64, C.c_double, _vp], C.c_int),
+    "ws_engine_generate_skewed": ([_vp, _u64, C.c_double, C.c_double, _u64, _vp], C.c_int),
     "ws_engine_sync_step": ([_vp, C.POINTER(SyncOptions), _vp, C.POINTER(Report)], C.c_int),
     "ws_engine_sync_step_host": ([_vp, _vp, C.POINTER(SyncOptions), _vp, C.POINTER(_u64),
                                   C.POINTER(Report)], C.c_int),

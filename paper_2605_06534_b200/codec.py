@@ -168,11 +168,27 @@ def copy_overlap(dst: torch.Tensor, dst_desc, src: torch.Tensor, src_desc, full_
     return copied.value
 
 
-def gen_pair_bf16(seed: int, name: str, full_shape, desc, density: float, device="cuda"):
-    """Synthetic bf16 pair for one shard (device generator)."""
+def expert_thresholds(experts: int, density: float, zipf_s: float, perm_seed: int = 0):
+    """Per-expert change thresholds (floor(density_e * 2^32)) of config 4."""
+    out = (C.c_uint64 * experts)()
+    check(lib.ws_expert_thresholds(experts, density, zipf_s, perm_seed, out))
+    return [int(x) for x in out]
+
+
+def gen_pair_bf16(seed: int, name: str, full_shape, desc, density: float, device="cuda",
+                  thr_dim0=None):
+    """Synthetic bf16 pair for one shard (device generator); thr_dim0: optional
+    per-dim-0-index thresholds (expert_thresholds) replacing `density`."""
     shp = shard_shape(full_shape, desc)
     prev = torch.empty(shp, dtype=torch.bfloat16, device=device)
     nxt = torch.empty(shp, dtype=torch.bfloat16, device=device)
+    if thr_dim0 is not None:
+        tab = torch.tensor(list(thr_dim0), dtype=torch.int64, device=device)
+        check(lib.ws_gen_pair_bf16_dim0(seed, name.encode(), shape_array(full_shape),
+                                        len(full_shape), shard(desc), _ptr(tab), _ptr(prev),
+                                        _ptr(nxt), _stream()))
+        torch.cuda.current_stream(device).synchronize()
+        return prev, nxt
     thr = int(min(max(density, 0.0), 1.0) * 4294967296.0)
     check(lib.ws_gen_pair_bf16(seed, name.encode(), shape_array(full_shape), len(full_shape),
                                shard(desc), thr, _ptr(prev), _ptr(nxt), _stream()))

@@ -79,11 +79,22 @@ const char* ws_last_error(void) { return g_last_error.c_str(); }
 
 int ws_abi_version(void) { return 1; }
 
-size_t ws_diff_workspace_bytes(uint64_t n) {
-  // [ticket @0][look-back status words @256: one per tile, the smallest
-  // tile being the reslice tile of 1024 records].
+namespace {
+// [ticket @0][look-back status words @256: one per tile, the smallest tile
+// being the reslice tile of 1024 records][K1 spill scratch for the grid
+// ws_diff_shards uses on n elements (4-byte records: the largest)].
+size_t status_bytes(uint64_t n) {
   const uint64_t tiles = (n + kResliceTile - 1) / kResliceTile + 1;
-  return (size_t)(256 + ((tiles * 8 + 255) / 256) * 256);
+  return ((tiles * 8 + 255) / 256) * 256;
+}
+uint32_t diff_blocks(uint64_t n) {
+  const uint64_t t = (n + encode_tile_elems(WS_F32) - 1) / encode_tile_elems(WS_F32);
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kMaxEncodeGrid, t));
+}
+}  // namespace
+
+size_t ws_diff_workspace_bytes(uint64_t n) {
+  return 256 + status_bytes(n) + encode_spill_bytes(WS_F32, diff_blocks(n));
 }
 
 namespace {
@@ -91,13 +102,16 @@ struct Workspace {
   unsigned int* ticket;
   unsigned long long* status;
   size_t status_words;
+  void* spill;
 };
-Workspace carve(void* ws, size_t bytes) {
+Workspace carve(void* ws, size_t bytes, uint64_t n) {
   char* b = static_cast<char*>(ws);
   Workspace w;
   w.ticket = reinterpret_cast<unsigned int*>(b);
   w.status = reinterpret_cast<unsigned long long*>(b + 256);
-  w.status_words = bytes > 256 ? (bytes - 256) / 8 : 0;
+  w.status_words = status_bytes(n) / 8;
+  w.spill = b + 256 + status_bytes(n);
+  (void)bytes;
   return w;
 }
 uint32_t g_epoch = 1;
@@ -119,7 +133,7 @@ ws_status ws_diff_shards(ws_dtype dtype, const void* prev_dev, const void* next_
   if (workspace_bytes < ws_diff_workspace_bytes(n))
     return set_error(WS_CAPACITY, "ws_diff_shards: workspace too small");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Workspace w = carve(workspace_dev, workspace_bytes);
+  Workspace w = carve(workspace_dev, workspace_bytes, n);
   const uint32_t tile = encode_tile_elems(dtype);
   const uint32_t ntiles = (uint32_t)((n + tile - 1) / tile);
   if (ntiles == 0) return cuda_status(cudaMemsetAsync(nnz_dev, 0, 8, s), "ws_diff_shards");
@@ -137,6 +151,8 @@ ws_status ws_diff_shards(ws_dtype dtype, const void* prev_dev, const void* next_
   a.status = w.status;
   a.epoch = next_epoch();
   a.ticket = w.ticket;
+  a.spill = w.spill;
+  a.spill_blocks = diff_blocks(n);
   return cuda_status(launch_encode(dtype, a, s), "ws_diff_shards");
 }
 
@@ -168,7 +184,7 @@ ws_status ws_reslice_delta(ws_dtype dtype, const int64_t* full_shape, int ndims,
   if (!err_dev) return set_error(WS_INVALID_ARGUMENT, "ws_reslice_delta: err_dev is required");
   if (workspace_bytes < ws_diff_workspace_bytes(nnz))
     return set_error(WS_CAPACITY, "ws_reslice_delta: workspace too small");
-  Workspace w = carve(workspace_dev, workspace_bytes);
+  Workspace w = carve(workspace_dev, workspace_bytes, nnz);
   ResliceArgs a{};
   a.map = make_remap(full_shape, ndims, src, dst);
   a.src_elems = shard_elems(full_shape, ndims, src);
@@ -226,6 +242,26 @@ ws_status ws_gen_pair_bf16(uint64_t seed, const char* param_name, const int64_t*
                                      change_thr, prev_dev, next_dev,
                                      reinterpret_cast<cudaStream_t>(stream)),
                      "ws_gen_pair_bf16");
+}
+
+ws_status ws_gen_pair_bf16_dim0(uint64_t seed, const char* param_name, const int64_t* full_shape,
+                                int ndims, ws_shard desc, const uint64_t* thr_dim0_dev,
+                                uint16_t* prev_dev, uint16_t* next_dev, ws_stream_t stream) {
+  ws_status st = check_shard(full_shape, ndims, desc, "ws_gen_pair_bf16_dim0");
+  if (st != WS_OK) return st;
+  if (!thr_dim0_dev) return set_error(WS_INVALID_ARGUMENT, "ws_gen_pair_bf16_dim0: null table");
+  return cuda_status(launch_gen_bf16(param_key(seed, param_name), full_shape, ndims, desc, 0,
+                                     prev_dev, next_dev, reinterpret_cast<cudaStream_t>(stream),
+                                     thr_dim0_dev),
+                     "ws_gen_pair_bf16_dim0");
+}
+
+ws_status ws_expert_thresholds(int experts, double density, double zipf_s, uint64_t perm_seed,
+                               uint64_t* out) {
+  if (experts <= 0 || !out || !(density >= 0.0) || !(zipf_s >= 0.0))
+    return set_error(WS_INVALID_ARGUMENT, "ws_expert_thresholds: bad argument");
+  expert_thresholds(experts, density, zipf_s, perm_seed, out);
+  return WS_OK;
 }
 
 }  // extern "C"

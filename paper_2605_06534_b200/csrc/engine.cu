@@ -187,6 +187,13 @@ ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density, ws_s
   return eng->generate(seed, density, reinterpret_cast<cudaStream_t>(stream));
 }
 
+ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double density, double zipf_s,
+                                   uint64_t perm_seed, ws_stream_t stream) {
+  if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_generate_skewed: null engine");
+  if (!(zipf_s >= 0.0)) return set_error(WS_INVALID_ARGUMENT, "zipf_s must be >= 0");
+  return eng->generate(seed, density, reinterpret_cast<cudaStream_t>(stream), zipf_s, perm_seed);
+}
+
 ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts, ws_stream_t stream,
                               ws_report* report) {
   if (!eng || !opts) return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_step: null argument");

@@ -12,7 +12,8 @@ struct ws_engine {
   ~ws_engine();
 
   ws_status init(const uint8_t* unique_id);
-  ws_status generate(uint64_t seed, double density, cudaStream_t s);
+  ws_status generate(uint64_t seed, double density, cudaStream_t s, double zipf_s = -1.0,
+                     uint64_t perm_seed = 0);
   ws_status sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
                       uint64_t* nnz_host, ws_report* report);
   ws_status segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
@@ -50,6 +51,8 @@ struct ws_engine {
   wsync::SegDev* d_segs_ = nullptr;
   uint32_t* d_tile0_ = nullptr;
   uint32_t* d_tile_seg_ = nullptr;
+  void* d_spill_ = nullptr;          // K1 spill scratch (encode_spill_bytes)
+  uint32_t spill_blocks_ = 0;
   uint32_t* d_tile_cnt_ = nullptr;   // K1's unordered layout (see EncodeArgs)
   uint32_t* d_tile_base_ = nullptr;
   uint32_t tile_elems_ = 0;

@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdint>
+#include <vector>
 
 #include "capi_util.h"
 #include "engine.h"
@@ -23,6 +25,7 @@ ws_engine::~ws_engine() {
   cudaFree(d_segs_);
   cudaFree(d_tile0_);
   cudaFree(d_tile_seg_);
+  cudaFree(d_spill_);
   cudaFree(d_tile_cnt_);
   cudaFree(d_tile_base_);
   cudaFree(d_seq_idx_);
@@ -82,6 +85,8 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   WS_CUDA_TRY(cudaMalloc(&d_status_, std::max<size_t>(1, ntiles_) * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemset(d_status_, 0, std::max<size_t>(1, ntiles_) * 8), "cudaMemset");
   WS_CUDA_TRY(cudaMalloc(&d_ticket_, 256), "cudaMalloc");
+  spill_blocks_ = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(), ntiles_));
+  WS_CUDA_TRY(cudaMalloc(&d_spill_, encode_spill_bytes(dtype_, spill_blocks_)), "cudaMalloc spill");
   WS_CUDA_TRY(cudaMalloc(&d_tile_cnt_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_tile_base_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
   WS_CUDA_TRY(cudaMemset(d_tile_cnt_, 0, std::max<size_t>(1, ntiles_) * 4), "cudaMemset");
@@ -195,27 +200,55 @@ ws_status ws_engine::ensure_records(double threshold, int sparse) {
   return WS_OK;
 }
 
-ws_status ws_engine::generate(uint64_t seed, double density, cudaStream_t s) {
+ws_status ws_engine::generate(uint64_t seed, double density, cudaStream_t s, double zipf_s,
+                              uint64_t perm_seed) {
   if (dtype_ != WS_BF16) return set_error(WS_INVALID_ARGUMENT, "generate: bf16 engines only");
   if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "generate: unbound");
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
   const double d = std::min(std::max(density, 0.0), 1.0);
   const uint64_t thr = (uint64_t)(d * 4294967296.0);
+  // skewed mode: one threshold table per EXPERT tensor (dim 0 = expert)
+  std::vector<uint64_t> tab;
+  std::vector<size_t> tab_off(plan_.manifest().size(), SIZE_MAX);
+  if (zipf_s >= 0.0) {
+    for (size_t i = 0; i < plan_.manifest().size(); ++i) {
+      const ParamMeta& p = plan_.manifest()[i];
+      if (p.kind != WS_EXPERT || p.shape.empty()) continue;
+      tab_off[i] = tab.size();
+      tab.resize(tab.size() + p.shape[0]);
+      expert_thresholds((int)p.shape[0], d, zipf_s, perm_seed, tab.data() + tab_off[i]);
+    }
+  }
+  uint64_t* d_tab = nullptr;
+  if (!tab.empty()) {
+    WS_CUDA_TRY(cudaMalloc(&d_tab, tab.size() * 8), "cudaMalloc");
+    WS_CUDA_TRY(cudaMemcpy(d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), "H2D");
+  }
+  auto table = [&](int param) -> const uint64_t* {
+    return tab_off[param] == SIZE_MAX ? nullptr : d_tab + tab_off[param];
+  };
+  ws_status st = WS_OK;
   for (const Segment& sg : plan_.segments()) {
     const ParamMeta& p = plan_.manifest()[sg.shard.param];
-    WS_CUDA_TRY(launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
-                                (int)p.shape.size(), sg.shard.d, thr,
-                                (uint16_t*)arena[0] + sg.offset, (uint16_t*)arena[1] + sg.offset, s),
-                "generate");
+    cudaError_t e = launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
+                                    (int)p.shape.size(), sg.shard.d, thr,
+                                    (uint16_t*)arena[0] + sg.offset,
+                                    (uint16_t*)arena[1] + sg.offset, s, table(sg.shard.param));
+    if (e != cudaSuccess && st == WS_OK) st = cuda_status(e, "generate");
   }
   for (const ServeShard& ss : plan_.serve_shards()) {
     const ParamMeta& p = plan_.manifest()[ss.shard.param];
-    WS_CUDA_TRY(launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
-                                (int)p.shape.size(), ss.shard.d, thr,
-                                (uint16_t*)serve + ss.offset, nullptr, s),
-                "generate");
+    cudaError_t e = launch_gen_bf16(param_key(seed, p.name.c_str()), p.shape.data(),
+                                    (int)p.shape.size(), ss.shard.d, thr,
+                                    (uint16_t*)serve + ss.offset, nullptr, s,
+                                    table(ss.shard.param));
+    if (e != cudaSuccess && st == WS_OK) st = cuda_status(e, "generate");
   }
-  return WS_OK;
+  if (d_tab) {
+    cudaStreamSynchronize(s);
+    cudaFree(d_tab);
+  }
+  return st;
 }
 
 ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
@@ -249,6 +282,8 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
     EncodeArgs a{};
     a.unordered = 1;
+    a.spill = d_spill_;
+    a.spill_blocks = spill_blocks_;
     a.tile_cnt = d_tile_cnt_;
     a.tile_base = d_tile_base_;
     a.prev = arena[pa];
@@ -284,6 +319,9 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   r.rec_idx = d_idx_;
   r.rec_val = d_val_;
   fill_tiles(r);
+  r.segs = d_segs_;
+  r.stream_apply = 1;
+  r.train_prev = arena[pa];
   r.train_next = arena[na];
   r.serve = serve;
   r.unit_off = d_unit_off_;

@@ -450,6 +450,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     pa.r.rec_idx = d_idx_;
     pa.r.rec_val = d_val_;
     fill_tiles(pa.r);
+    pa.r.segs = d_segs_;
     pa.r.train_next = arena[next_arena];
     pa.r.serve = serve;
     pa.r.unit_off = c->d_unit_off;
@@ -482,6 +483,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   pa.r.rec_idx = d_idx_;
   pa.r.rec_val = d_val_;
   fill_tiles(pa.r);
+  pa.r.segs = d_segs_;
   pa.r.train_next = arena[next_arena];
   pa.r.serve = serve;
   pa.r.unit_off = c->d_unit_off;

@@ -86,7 +86,15 @@ struct EncodeArgs {
   int32_t unordered;
   uint32_t* tile_cnt;          // per global super-tile
   uint32_t* tile_base;         // per global super-tile: first record in the segment stream
+  // Changes past a thread's shared-memory slots go to its warp's region of
+  // this scratch (encode_spill_bytes(dtype, spill_blocks)); the grid is
+  // clamped to spill_blocks.
+  void* spill;
+  uint32_t spill_blocks;
 };
+
+constexpr uint32_t kMaxEncodeGrid = 160;  // >= SMs of a B200 (148)
+size_t encode_spill_bytes(int dtype, uint32_t blocks);
 
 // Ascending segment stream from an unordered K1 output: the segment's
 // super-tiles' records in tile order (one block; API/wire path, not the sync).
@@ -145,8 +153,11 @@ uint64_t make_box_copy(int dtype, const int64_t* full, int nd, const ws_shard& d
 // Synthetic bf16 pair for one shard; also used to initialise serving shards
 // (prev only when next == nullptr).
 cudaError_t launch_gen_bf16(uint64_t key, const int64_t* full, int nd, const ws_shard& desc,
-                            uint64_t change_thr, uint16_t* prev, uint16_t* next,
-                            cudaStream_t s);
+                            uint64_t change_thr, uint16_t* prev, uint16_t* next, cudaStream_t s,
+                            const uint64_t* thr_dim0 = nullptr);
+// Per-expert change thresholds (ws_expert_thresholds).
+void expert_thresholds(int experts, double density, double zipf_s, uint64_t perm_seed,
+                       uint64_t* out);
 
 // Host helpers.
 uint64_t param_key(uint64_t seed, const char* name);

@@ -8,8 +8,11 @@
 // (segments are independent look-back chains).  The design and the
 // measurements behind it are in DESIGN.md §4.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
+#include <cmath>
 
 #include "kernels.h"
 
@@ -91,7 +94,7 @@ struct StageMeta {
 };
 
 #ifndef WS_ENC_SLOTS
-#define WS_ENC_SLOTS 6
+#define WS_ENC_SLOTS 4
 #endif
 #ifndef WS_ENC_PREFETCH
 #define WS_ENC_PREFETCH 1
@@ -109,6 +112,8 @@ struct EncCfg {
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
   static constexpr int K = WS_ENC_SLOTS;                              // staged changes per thread per super-tile
+  static constexpr uint32_t SPW = SUPER / NCW;                        // spill capacity per warp (all its elements)
+  using SpillRec = typename std::conditional<sizeof(T) == 2, uint32_t, uint2>::type;  // li | val
   static constexpr uint32_t WORDS = SUPER / 32;                       // change-bitmap words
   static constexpr int NB = kEncBuffers;                              // staging buffers
   // bf16: the serving word a fused record updates is fetched (cp.async) into
@@ -121,7 +126,7 @@ struct EncCfg {
       WORDS * 6 + (size_t)K * kEncConsumers * (sizeof(T) + 2 + (PRE ? 4 : 0));
   static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
                                   (kRing + NB) * sizeof(StageMeta) + NB * 8 +
-                                  (2 * kRing + 2 * NB) * 8 + 32;
+                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + 32;
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
   static_assert(SUPER <= 65536, "u16 in-tile index");
   static_assert(WORDS % 128 == 0, "bitmap words per resolver lane in 16-byte loads");
@@ -240,7 +245,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
                                             uint64_t prefix, uint32_t* bm, const uint16_t* wpre,
                                             const uint16_t* sidx,
                                             const typename Traits<DT>::T* sval,
-                                            const uint32_t* spre) {
+                                            const uint32_t* spre, uint32_t* ovf,
+                                            const typename EncCfg<DT>::SpillRec* spill) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
@@ -312,54 +318,36 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         if (tp[j]) *tp[j] = Tr::add(old[j], vv[j]);
       }
     }
-    if (ti.mine > (uint32_t)K) {  // spill (rare, lane-divergent): changes past the slots
-      const T* prevT = reinterpret_cast<const T*>(a.prev);
-      const T* nextT = reinterpret_cast<const T*>(a.next);
-      uint32_t r = 0;
-      for (uint32_t g = 0; g < ti.nsub; ++g) {
-        for (uint32_t v = 0; v < VPT; ++v) {
-          const uint32_t li = g * SUB + (v * kEncConsumers + threadIdx.x) * VE;
-          if (li >= ti.cnt) continue;
-          const uint64_t gv = ti.base + e0 + li;  // multiple of VE: 16-byte aligned
-          uint4 pa = make_uint4(0, 0, 0, 0), pb = make_uint4(0, 0, 0, 0);
-          uint32_t mv = 0;
-          if (li + VE <= ti.cnt) {
-            pa = ld_stream(reinterpret_cast<const uint4*>(prevT + gv));
-            pb = ld_stream(reinterpret_cast<const uint4*>(nextT + gv));
-            mv = change_mask<DT>(pa, pb);
-          } else {
-            T ta[VE], tb[VE];
-            for (int e = 0; e < VE; ++e) {
-              const bool in = li + e < ti.cnt;
-              ta[e] = in ? prevT[gv + e] : T(0);
-              tb[e] = in ? nextT[gv + e] : T(0);
-              if (in && Tr::changed(ta[e], tb[e])) mv |= 1u << e;
-            }
-            memcpy(&pa, ta, 16);
-            memcpy(&pb, tb, 16);
-          }
-          while (mv) {
-            const int e = __ffs(mv) - 1;
-            mv &= mv - 1;
-            if (r >= (uint32_t)K) {
-              const uint64_t pos = prefix + tile_rank(bm, wpre, li + e);
-              if (pos < ti.cap) {
-                const T dv = Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
-                a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li + e);
-                out_val[ti.rec + pos] = dv;
-                if (fz) {
-                  T* p = fuse_target<DT>(fz, serve, (uint32_t)(e0 + li + e));
-                  if (p) *p = Tr::add(*p, dv);
-                }
-              }
-            }
-            ++r;
-          }
+    // changes past the slots: from this warp's spill region (written at
+    // staging, still in L2), in any order -- the bitmap gives their ranks
+    const uint32_t nov = *ovf;
+    for (uint32_t r0 = 0; r0 < nov; r0 += 32) {
+      const uint32_t r = r0 + lane;
+      if (r >= nov) continue;
+      uint32_t li;
+      T dv;
+      if constexpr (sizeof(T) == 2) {
+        const uint32_t x = spill[r];
+        li = x & 0xffffu;
+        dv = (T)(x >> 16);
+      } else {
+        const uint2 x = spill[r];
+        li = x.x;
+        dv = (T)x.y;
+      }
+      const uint64_t pos = prefix + tile_rank(bm, wpre, li);
+      if (pos < ti.cap) {
+        a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li);
+        out_val[ti.rec + pos] = dv;
+        if (fz) {
+          T* p = fuse_target<DT>(fz, serve, (uint32_t)(e0 + li));
+          if (p) *p = Tr::add(*p, dv);
         }
       }
     }
   }
   __syncwarp();  // every lane of the warp is done reading the bitmap
+  if (lane == 0) *ovf = 0;
   constexpr uint32_t LPW = 32 / VE;  // lanes sharing one bitmap word
   if ((threadIdx.x & (LPW - 1)) == 0)
     for (uint32_t g = 0; g < ti.nsub; ++g)
@@ -395,10 +383,15 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(s_prefix + NB);              // [kRing]
   uint64_t* empty = full + kRing;                                           // [kRing]
   uint64_t* resolved = empty + kRing;                                       // [NB]
+  uint32_t* s_ovf = reinterpret_cast<uint32_t*>(resolved + NB);             // [NB][NCW]
+  using SpillRec = typename C::SpillRec;
+  SpillRec* spill_blk = reinterpret_cast<SpillRec*>(a.spill) +
+                        (size_t)blockIdx.x * NB * NCW * C::SPW;             // [NB][NCW][SPW]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t i = tid; i < NB * WORDS; i += blockDim.x)
     buf_bm(i / WORDS)[i % WORDS] = 0;
+  for (uint32_t i = tid; i < NB * NCW; i += blockDim.x) s_ovf[i] = 0;
   if (tid == 0) {
     for (int k = 0; k < kRing; ++k) {
       mbar_init(&full[k], 1);
@@ -499,7 +492,8 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
     flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
-                    buf_pre(pb));
+                    buf_pre(pb), s_ovf + pb * NCW + warp,
+                    spill_blk + ((size_t)pb * NCW + warp) * C::SPW);
   };
   PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this thread
   const uint64_t pol_keep = policy_evict_last();
@@ -566,7 +560,14 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           do {
             const int e = __ffs(mv) - 1;
             mv &= mv - 1;
-            if (mine < (uint32_t)K) {
+            const T dv = j < nvec ? Tr::delta(Pe[e], Ne[e])
+                                  : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+            if (mine >= (uint32_t)K) {  // past the slots: this warp's spill region
+              const uint32_t o = atomicAdd(s_ovf + b * NCW + warp, 1u);
+              SpillRec* sp = spill_blk + ((size_t)b * NCW + warp) * C::SPW + o;
+              if constexpr (sizeof(T) == 2) *sp = (uint32_t)(li + e) | ((uint32_t)dv << 16);
+              else *sp = make_uint2(li + e, (uint32_t)dv);
+            } else {
               sidx[mine * kEncConsumers] = (uint16_t)(li + e);
               if (C::PRE && pf && li + e - pf_lo < pf_n) {
                 const void* src = reinterpret_cast<const void*>(
@@ -574,9 +575,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
                 if (WS_ENC_EVICT) cp_async4_hint(spre + mine * kEncConsumers, src, pol_keep);
                 else cp_async4(spre + mine * kEncConsumers, src);
               }
-              // changed elements are sparse: read them back from the ring
-              sval[mine * kEncConsumers] = j < nvec ? Tr::delta(Pe[e], Ne[e])
-                                                    : Tr::delta(Tr::get(pa, e), Tr::get(pb, e));
+              sval[mine * kEncConsumers] = dv;
             }
             ++mine;
           } while (mv);
@@ -793,18 +792,20 @@ __global__ void box_copy_kernel(BoxCopyArgs a) {
 
 __global__ void gen_kernel(uint64_t key, Box box, uint32_t full_ext_nd, uint64_t full_strides0,
                            uint64_t full_strides1, uint64_t full_strides2, uint64_t full_strides3,
-                           uint64_t n, uint64_t change_thr, uint16_t* prev, uint16_t* next) {
+                           uint64_t n, uint64_t change_thr, const uint64_t* thr_dim0,
+                           uint16_t* prev, uint16_t* next) {
   const uint64_t fs[4] = {full_strides0, full_strides1, full_strides2, full_strides3};
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t rem = i, g = 0;
+    uint64_t rem = i, g = 0, c0 = 0;
     for (int d = (int)full_ext_nd - 1; d >= 0; --d) {
       const uint64_t c = rem % box.ext[d] + box.lo[d];
       rem /= box.ext[d];
       g += c * fs[d];
+      c0 = c;
     }
     uint16_t p, q;
-    gen_elem_bf16(key, g, change_thr, p, q);
+    gen_elem_bf16(key, g, thr_dim0 ? thr_dim0[c0] : change_thr, p, q);
     prev[i] = p;
     if (next) next[i] = q;
   }
@@ -834,6 +835,16 @@ int sm_count() {
   return n;
 }
 
+size_t encode_spill_bytes(int dtype, uint32_t blocks) {
+  size_t per = 0;
+  switch (dtype) {
+    case WS_BF16: per = sizeof(EncCfg<WS_BF16>::SpillRec) * EncCfg<WS_BF16>::SPW; break;
+    case WS_I32: per = sizeof(EncCfg<WS_I32>::SpillRec) * EncCfg<WS_I32>::SPW; break;
+    default: per = sizeof(EncCfg<WS_F32>::SpillRec) * EncCfg<WS_F32>::SPW; break;
+  }
+  return per * kEncBuffers * (kEncConsumers / 32) * blocks;
+}
+
 cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out) {
   static bool attr_done = false;
   if (!attr_done) {
@@ -849,6 +860,8 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
   int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(),
                                                            std::max(a.ntiles, 1u)));
   if (const char* g = getenv("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
+  if (!a.spill || a.spill_blocks == 0) return cudaErrorInvalidValue;
+  grid = std::min<int>(grid, (int)a.spill_blocks);
   if (grid_out) *grid_out = grid;
   EncodeArgs a2 = a;
   if (const char* d = getenv("WSYNC_ENCODE_DEBUG")) a2.debug = (uint32_t)atoi(d);
@@ -1005,6 +1018,31 @@ uint64_t make_box_copy(int dtype, const int64_t* full, int nd, const ws_shard& d
   return count;
 }
 
+void expert_thresholds(int experts, double density, double zipf_s, uint64_t perm_seed,
+                       uint64_t* out) {
+  // Zipf(s) weight of rank r (1-based), normalised to mean 1
+  std::vector<double> w(experts);
+  double sum = 0;
+  for (int r = 0; r < experts; ++r) sum += (w[r] = std::pow((double)(r + 1), -zipf_s));
+  // rank of every expert: a Fisher-Yates shuffle driven by splitmix64(perm_seed + k)
+  std::vector<int> rank(experts);
+  for (int e = 0; e < experts; ++e) rank[e] = e;
+  uint64_t st = perm_seed;
+  for (int i = experts - 1; i > 0; --i) {
+    st += 0x9e3779b97f4a7c15ull;
+    uint64_t x = st;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    std::swap(rank[i], rank[x % (uint64_t)(i + 1)]);
+  }
+  for (int e = 0; e < experts; ++e) {
+    double d = density * w[rank[e]] * experts / sum;
+    d = d < 0 ? 0 : (d > 1 ? 1 : d);
+    out[e] = (uint64_t)(d * 4294967296.0);
+  }
+}
+
 uint64_t param_key(uint64_t seed, const char* name) {
   uint64_t h = 0xcbf29ce484222325ull;  // fnv1a64 (rng.hpp:80-87)
   for (const unsigned char* p = (const unsigned char*)name; *p; ++p) {
@@ -1019,8 +1057,8 @@ uint64_t param_key(uint64_t seed, const char* name) {
 }
 
 cudaError_t launch_gen_bf16(uint64_t key, const int64_t* full, int nd, const ws_shard& desc,
-                            uint64_t change_thr, uint16_t* prev, uint16_t* next,
-                            cudaStream_t s) {
+                            uint64_t change_thr, uint16_t* prev, uint16_t* next, cudaStream_t s,
+                            const uint64_t* thr_dim0) {
   const Box b = shard_box(full, nd, desc);
   uint64_t n = 1, fs[4] = {0, 0, 0, 0}, st = 1;
   for (int d = 0; d < nd; ++d) n *= b.ext[d];
@@ -1030,7 +1068,7 @@ cudaError_t launch_gen_bf16(uint64_t key, const int64_t* full, int nd, const ws_
   }
   if (n == 0) return cudaSuccess;
   gen_kernel<<<stream_grid(n, 256), 256, 0, s>>>(key, b, (uint32_t)nd, fs[0], fs[1], fs[2], fs[3],
-                                                 n, change_thr, prev, next);
+                                                 n, change_thr, thr_dim0, prev, next);
   return cudaGetLastError();
 }
 

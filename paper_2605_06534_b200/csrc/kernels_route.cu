@@ -23,6 +23,12 @@ __device__ __forceinline__ bool seg_dense(const RouteSideArgs& a, int seg) {
   return !a.sparse || a.seg_nnz[seg] > a.seg_cap[seg];
 }
 
+// sparse, not fused, and dense enough to apply by streaming (local routes)
+__device__ __forceinline__ bool seg_stream(const RouteSideArgs& a, int seg) {
+  return a.stream_apply && !(a.fused && a.fuse_on[seg]) &&
+         a.seg_nnz[seg] * kStreamDiv > a.segs[seg].n;
+}
+
 // Super-tiles [*ta, *tb) of an entry's segment that can hold records for it:
 // an identity route only reads its keep window.
 __device__ __forceinline__ void entry_tiles(const RouteSideArgs& a, const LocalEntry& e,
@@ -42,7 +48,7 @@ __device__ __forceinline__ void entry_tiles(const RouteSideArgs& a, const LocalE
 // Units of one entry: groups of kTilesPerUnit super-tiles of records
 // (sparse) or row-run chunks (dense).
 __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const LocalEntry& e) {
-  if (seg_dense(a, e.seg)) {
+  if (seg_dense(a, e.seg) || seg_stream(a, e.seg)) {
     const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
     return e.box.rows * per_row;
   }
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
       // below the dense threshold; the others skip the scattered
       // read-modify-writes of records a dense copy would overwrite anyway.
       const int s = a.entries[e].seg;
-      a.fuse_on[s] = a.seg_nnz[s] * 2 <= a.seg_cap[s] ? 1u : 0u;
+      a.fuse_on[s] = a.seg_nnz[s] * kStreamDiv <= a.segs[s].n ? 1u : 0u;
     }
     uint64_t inc = u;
 #pragma unroll
@@ -140,7 +146,8 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
     const LocalEntry& E = a.entries[s_entry];
     const uint64_t lu = u - s_u0;
     __syncthreads();
-    if (!seg_dense(a, E.seg)) {
+    const bool stream = !seg_dense(a, E.seg) && seg_stream(a, E.seg);
+    if (!seg_dense(a, E.seg) && !stream) {
       uint64_t k0, k1;
       warp_tile_records(a, E, lu, threadIdx.x >> 5, &k0, &k1);
       const uint64_t rec = a.seg_rec[E.seg];
@@ -175,7 +182,30 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
       }
       const T* src = next + a.seg_base[E.seg] + so;
       T* dst = serve + E.dst_base + dso;
-      if (B.vec) {
+      if (stream) {  // serve += next - prev where changed (codec.cpp:80-91 over the box)
+        const T* psrc = reinterpret_cast<const T*>(a.train_prev) + a.seg_base[E.seg] + so;
+        if (B.vec) {
+          constexpr int VE = Tr::kVE;
+          const uint4* p4 = reinterpret_cast<const uint4*>(psrc + c0);
+          const uint4* n4 = reinterpret_cast<const uint4*>(src + c0);
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+          for (uint64_t j = threadIdx.x; j < (c1 - c0) / VE; j += blockDim.x) {
+            const uint4 pv = ld_stream(p4 + j), nv = ld_stream(n4 + j);
+            if (!change_mask<DT>(pv, nv)) continue;
+            uint4 sv = d4[j];
+            T* se = reinterpret_cast<T*>(&sv);
+            const T* pe = reinterpret_cast<const T*>(&pv);
+            const T* ne = reinterpret_cast<const T*>(&nv);
+#pragma unroll
+            for (int e = 0; e < VE; ++e)
+              if (Tr::changed(pe[e], ne[e])) se[e] = Tr::add(se[e], Tr::delta(pe[e], ne[e]));
+            d4[j] = sv;
+          }
+        } else {
+          for (uint64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x)
+            if (Tr::changed(psrc[j], src[j])) dst[j] = Tr::add(dst[j], Tr::delta(psrc[j], src[j]));
+        }
+      } else if (B.vec) {
         constexpr int VE = Tr::kVE;
         const uint4* s4 = reinterpret_cast<const uint4*>(src + c0);
         uint4* d4 = reinterpret_cast<uint4*>(dst + c0);

@@ -6,6 +6,12 @@
 namespace wsync {
 
 constexpr uint32_t kTilesPerUnit = 8;    // super-tiles of records per work unit (one per warp)
+// A sparse segment with more than 1/kStreamDiv of its elements changed is
+// cheaper to apply by streaming serve += next - prev over its box (8 B per
+// element) than by scattered read-modify-writes (~100 B of DRAM per record, and
+// partial-sector writes);
+// the same bound decides whether K1 fuses the apply.
+constexpr uint64_t kStreamDiv = 10;  // measured: fused RMW wins at 10%, streaming at 20%
 constexpr uint64_t kCopyChunk = 65536;   // elements per dense-copy work unit
 
 // One (trainer segment -> serving shard) route whose destination is resident
@@ -42,6 +48,9 @@ struct RouteSideArgs {
   const uint32_t* tile_cnt;
   const uint32_t* tile_base;
   uint32_t tile_elems;          // elements per super-tile
+  const SegDev* segs;           // segment sizes
+  int32_t stream_apply;         // local routes: dense-ish sparse segments apply by streaming
+  const void* train_prev;
   const void* train_next;
   void* serve;
   uint64_t* unit_off;           // nentries + 1

@@ -141,9 +141,16 @@ class TransferEngine:
         return self.serve[off:off + n].view(shp)
 
     # ---- sync ----------------------------------------------------------------
-    def generate(self, seed=1, density=0.01):
+    def generate(self, seed=1, density=0.01, expert_zipf=None, perm_seed=0):
+        """Synthetic prev/next in the trainer arenas and prev in the serving
+        arena; expert_zipf=s skews the density of EXPERT tensors per expert
+        (expert_thresholds)."""
         with torch.cuda.device(self.device):
-            check(lib.ws_engine_generate(self.h, seed, density, _stream()))
+            if expert_zipf is None:
+                check(lib.ws_engine_generate(self.h, seed, density, _stream()))
+            else:
+                check(lib.ws_engine_generate_skewed(self.h, seed, density, float(expert_zipf),
+                                                    perm_seed, _stream()))
 
     def sync_step(self, sparse=True, density_threshold=0.20, reverse=False, report=True,
                   stream=None):

@@ -26,11 +26,12 @@ import torch.distributed as dist  # noqa: E402
 import paper_2605_06534_b200 as ws  # noqa: E402
 
 
-def serve_equals_gen(eng, plan, seed, density, which):
+def serve_equals_gen(eng, plan, seed, density, which, tabs=None):
     bad = []
     for i, (p, desc, off, n) in enumerate(plan.serve_shards):
         meta = plan.manifest[p]
-        pv, nx = ws.gen_pair_bf16(seed, meta.name, meta.shape, desc, density, device=eng.device)
+        pv, nx = ws.gen_pair_bf16(seed, meta.name, meta.shape, desc, density, device=eng.device,
+                                  thr_dim0=(tabs or {}).get(p))
         want = (nx if which == "next" else pv).view(torch.int16)
         if not torch.equal(eng.serve_view(i).view(torch.int16), want):
             bad.append(meta.name)
@@ -49,6 +50,24 @@ def bf16_case(rank, world, uid_fn, manifest, density, seed):
     bad += serve_equals_gen(eng, plan, seed, density, "prev")
     eng.sync_step(sparse=False)
     bad += serve_equals_gen(eng, plan, seed, density, "next")
+    return bad, rep
+
+
+def layout_case(rank, world, uid_fn, manifest, train, serve, density, seed, zipf=None):
+    """BASELINE configs 3/4 at this world size: any trainer -> serving layout,
+    optionally with Zipf-skewed per-expert densities; serving == `next`, then
+    a reverse sync restores `prev`."""
+    plan = ws.Plan(manifest, ws.BF16, train, serve, world=world, rank=rank)
+    eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
+    eng.generate(seed=seed, density=density, expert_zipf=zipf, perm_seed=11)
+    tabs = {}
+    if zipf is not None:
+        tabs = {i: ws.expert_thresholds(m.shape[0], density, zipf, 11)
+                for i, m in enumerate(manifest) if m.kind == ws.ModuleKind.EXPERT}
+    rep = eng.sync_step()
+    bad = serve_equals_gen(eng, plan, seed, density, "next", tabs)
+    eng.sync_step(reverse=True)
+    bad += serve_equals_gen(eng, plan, seed, density, "prev", tabs)
     return bad, rep
 
 
@@ -101,6 +120,20 @@ def main():
             bad, rep = bf16_case(rank, world, uid, manifest, density, 3)
             results[f"bf16 {name} d={density}"] = bad or "ok"
             ok &= not bad
+    # BASELINE config 3 (Qwen3-32B TP8 -> TP4 x 2, 0.5%) and config 4
+    # (Qwen3-30B-A3B expert-sharded, Zipf(1.1) per-expert densities around
+    # 1%), on layer subsets, scaled to this world size
+    half = max(1, world // 2)
+    for name, manifest, train, serve, density, zipf in (
+            ("config3 qwen3-32b[0,63]", ws.MODELS["qwen3-32b"]([0, 63]),
+             ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(half, 1, world // half), 0.005,
+             None),
+            ("config4 qwen3-30b-a3b[0,47]", ws.MODELS["qwen3-30b-a3b"]([0, 47]),
+             ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1), 0.01, 1.1)):
+        bad, rep = layout_case(rank, world, uid, manifest, train, serve, density, 5, zipf)
+        results[name] = bad or "ok"
+        results[name + " shards dense/sparse"] = (rep["dense_shards"], rep["sparse_shards"])
+        ok &= not bad
     for dtype in (ws.I32, ws.F32):
         for density, sparse in ((0.05, True), (0.45, True), (0.05, False)):
             bad = ref_case(rank, world, uid, dtype, density, sparse)

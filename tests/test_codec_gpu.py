@@ -235,3 +235,17 @@ def test_generator_matches_oracle(restatement, desc):
     wp, wn = restatement.gen_pair_bf16(3, "layers.0.w", full, desc, 0.05)
     assert to_np(p, BF16).ravel().tobytes() == wp.tobytes()
     assert to_np(n, BF16).ravel().tobytes() == wn.tobytes()
+
+
+@pytest.mark.parametrize("desc", [(-1, 0, 0), (0, 4, 12), (2, 32, 64)])
+def test_skewed_generator_matches_oracle(restatement, desc):
+    """Config 4: per-expert change thresholds along dim 0 of a stacked expert tensor."""
+    import paper_2605_06534_b200 as ws
+    full = (16, 8, 64)
+    thr = ws.expert_thresholds(16, 0.05, 1.1, 5)
+    p, n = ws.gen_pair_bf16(3, "layers.0.mlp.experts.up_proj", full, desc, 0.0, thr_dim0=thr)
+    wp, wn = restatement.gen_pair_bf16(3, "layers.0.mlp.experts.up_proj", full, desc, 0.0,
+                                       thr_dim0=thr)
+    assert to_np(p, BF16).ravel().tobytes() == wp.tobytes()
+    assert to_np(n, BF16).ravel().tobytes() == wn.tobytes()
+    assert (wp != wn).any()

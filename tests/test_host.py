@@ -42,7 +42,9 @@ def test_qwen_manifest_sizes():
 
 
 def _ref_manifest(m):
-    return [p.as_tuple() for p in m]
+    # EXPERT (stacked [E, ...], sliced on dim 0) is expressed to the reference
+    # as its dim-0 kind
+    return [(n, 0 if k == 5 else k, s, l) for (n, k, s, l) in (p.as_tuple() for p in m)]
 
 
 @pytest.mark.parametrize("train,serve", [((2, 1, 1), (4, 1)), ((2, 1, 2), (2, 1)),
@@ -51,7 +53,22 @@ def _ref_manifest(m):
 def test_routes_match_reference_plan_pulls(reference, train, serve):
     """Every serving coordinate pulls exactly the source shards plan_pulls picks."""
     import paper_2605_06534_b200 as ws
-    manifest = ws.toy_transformer_manifest(layers=4, hidden=64, vocab=128)
+    _check_routes(reference, ws.toy_transformer_manifest(layers=4, hidden=64, vocab=128), train,
+                  serve)
+
+
+@pytest.mark.parametrize("model,layers,train,serve", [
+    ("qwen3-32b", [0, 1, 63], (8, 1, 1), (4, 1)),    # BASELINE config 3: TP8 -> TP4 x 2
+    ("qwen3-30b-a3b", [0, 47], (8, 1, 1), (8, 1)),   # config 4: experts 16g..16g+15 on GPU g
+    ("qwen3-8b", [0, 35], (8, 1, 1), (2, 1)),        # config 2's nearest reference layout
+])
+def test_baseline_configs_match_reference_plan_pulls(reference, model, layers, train, serve):
+    import paper_2605_06534_b200 as ws
+    _check_routes(reference, ws.MODELS[model](layers), train, serve)
+
+
+def _check_routes(reference, manifest, train, serve):
+    import paper_2605_06534_b200 as ws
     _, pulls = reference.plan(_ref_manifest(manifest), train, serve)
     want = defaultdict(set)
     for (rank, param, tp_rank, tp_size, stage, dim, start, end) in pulls:
@@ -143,3 +160,21 @@ def test_arena_alignment():
     for (p, desc, off, n) in plan.segments + plan.serve_shards:
         assert off % 64 == 0
     assert plan.info.train_elems == 494_032_768
+
+
+def test_expert_thresholds_match_restatement():
+    """Config 4's skewed per-expert densities: the library's table equals the
+    plain-Python restatement, averages the requested density, and is a
+    permutation of the Zipf profile."""
+    import paper_2605_06534_b200 as ws
+    from oracle.oracle import expert_thresholds
+    for E, d, s, seed in ((128, 0.01, 1.1, 7), (16, 0.05, 0.0, 1), (8, 0.3, 2.0, 3)):
+        got = ws.expert_thresholds(E, d, s, seed)
+        want = expert_thresholds(E, d, s, seed)
+        assert got == want
+        mean = sum(min(t, 1 << 32) for t in got) / E / 4294967296.0
+        if max(got) < (1 << 32):
+            assert abs(mean - d) < 1e-6
+    zipf = ws.expert_thresholds(128, 0.01, 1.1, 7)
+    assert max(zipf) > 0.2 * 4294967296.0  # the hottest expert runs dense (> threshold)
+    assert sorted(zipf) == sorted(ws.expert_thresholds(128, 0.01, 1.1, 8))
