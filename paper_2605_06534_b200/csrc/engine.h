@@ -51,6 +51,11 @@ struct ws_engine {
   wsync::SegDev* d_segs_ = nullptr;
   uint32_t* d_tile0_ = nullptr;
   uint32_t* d_tile_seg_ = nullptr;
+  uint32_t* d_seg_mode_ = nullptr;   // 1: counted only this sync (dense the last one)
+  unsigned long long* d_fill_ = nullptr;
+  uint32_t* d_fix_list_ = nullptr;   // fixup pass super-tiles
+  uint32_t* d_fix_n_ = nullptr;
+  bool count_only_ = true;           // WSYNC_COUNT_ONLY=0 disables the prediction
   void* d_spill_ = nullptr;          // K1 spill scratch (encode_spill_bytes)
   uint32_t spill_blocks_ = 0;
   uint32_t* d_tile_cnt_ = nullptr;   // K1's unordered layout (see EncodeArgs)

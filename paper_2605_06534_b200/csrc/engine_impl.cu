@@ -26,6 +26,10 @@ ws_engine::~ws_engine() {
   cudaFree(d_tile0_);
   cudaFree(d_tile_seg_);
   cudaFree(d_spill_);
+  cudaFree(d_seg_mode_);
+  cudaFree(d_fill_);
+  cudaFree(d_fix_list_);
+  cudaFree(d_fix_n_);
   cudaFree(d_tile_cnt_);
   cudaFree(d_tile_base_);
   cudaFree(d_seq_idx_);
@@ -85,6 +89,12 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   WS_CUDA_TRY(cudaMalloc(&d_status_, std::max<size_t>(1, ntiles_) * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMemset(d_status_, 0, std::max<size_t>(1, ntiles_) * 8), "cudaMemset");
   WS_CUDA_TRY(cudaMalloc(&d_ticket_, 256), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_seg_mode_, ns * 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemset(d_seg_mode_, 0, ns * 4), "cudaMemset");
+  WS_CUDA_TRY(cudaMalloc(&d_fill_, ns * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_fix_list_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&d_fix_n_, 4), "cudaMalloc");
+  if (const char* f = getenv("WSYNC_COUNT_ONLY")) count_only_ = atoi(f) != 0;
   spill_blocks_ = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(), ntiles_));
   WS_CUDA_TRY(cudaMalloc(&d_spill_, encode_spill_bytes(dtype_, spill_blocks_)), "cudaMalloc spill");
   WS_CUDA_TRY(cudaMalloc(&d_tile_cnt_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
@@ -280,6 +290,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   if (o.sparse && ntiles_) {
     // K1 reserves each super-tile's records with an atomic on its segment's count
     WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
+    if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
     EncodeArgs a{};
     a.unordered = 1;
     a.spill = d_spill_;
@@ -304,8 +315,23 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     a.status = d_status_;
     a.epoch = next_epoch();
     a.ticket = d_ticket_;
+    if (count_only_) a.seg_mode = d_seg_mode_;
     WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
     ++launches;
+    if (count_only_) {
+      // super-tiles of predicted-dense segments that came out sparse, then K1
+      // over just those (an empty list costs two near-empty launches)
+      WS_CUDA_TRY(launch_fixup_plan(d_tile0_, nseg_, d_nnz_, d_cap_, d_seg_mode_, d_fix_list_,
+                                    d_fix_n_, s),
+                  "fixup plan");
+      EncodeArgs f = a;
+      f.seg_mode = nullptr;
+      f.tile_list = d_fix_list_;
+      f.ntiles_dev = d_fix_n_;
+      f.fill = d_fill_;
+      WS_CUDA_TRY(launch_encode(dtype_, f, s), "encode fixup");
+      launches += 2;
+    }
   }
   WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
   RouteSideArgs r{};

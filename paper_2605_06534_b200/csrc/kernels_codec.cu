@@ -90,7 +90,8 @@ constexpr int kStagedBar = 2;  // named barriers 2.. : "super-tile staged in buf
 struct StageMeta {
   SegDev sg;
   uint32_t t, s, lt, nsub, cnt, last;
-  uint32_t pad[2];
+  uint32_t count_only;  // segment predicted dense: count, stage nothing
+  uint32_t pad;
 };
 
 #ifndef WS_ENC_SLOTS
@@ -126,7 +127,7 @@ struct EncCfg {
       WORDS * 6 + (size_t)K * kEncConsumers * (sizeof(T) + 2 + (PRE ? 4 : 0));
   static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
                                   (kRing + NB) * sizeof(StageMeta) + NB * 8 +
-                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + 32;
+                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + NB * 4 + 32;
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
   static_assert(SUPER <= 65536, "u16 in-tile index");
   static_assert(WORDS % 128 == 0, "bitmap words per resolver lane in 16-byte loads");
@@ -139,10 +140,22 @@ struct EncCfg {
 template <int DT>
 __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMeta& ti,
                                              const uint32_t* bm, uint16_t* wpre,
-                                             unsigned long long* s_prefix) {
+                                             unsigned long long* s_prefix, uint32_t* s_tcnt) {
   using C = EncCfg<DT>;
   constexpr int PER = C::WORDS / 32;
   const int lane = threadIdx.x & 31;
+  if (ti.count_only) {  // the consumers summed the count; nothing is staged
+    if (lane == 0) {
+      const uint32_t count = *s_tcnt;
+      *s_tcnt = 0;
+      if (count) atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_nnz + ti.s),
+                           (unsigned long long)count);
+      a.tile_cnt[ti.t] = 0;
+      a.tile_base[ti.t] = 0;
+      *s_prefix = ~0ull;
+    }
+    return;
+  }
   const uint4* b4 = reinterpret_cast<const uint4*>(bm + lane * PER);
   uint32_t sum = 0;
 #pragma unroll
@@ -176,8 +189,9 @@ __device__ __forceinline__ void resolve_tile(const EncodeArgs& a, const StageMet
   if (a.unordered) {  // one atomic reserves the super-tile's place in its segment
     if (lane == 0) {
       unsigned long long base = 0;
-      if (count)
-        base = atomicAdd(reinterpret_cast<unsigned long long*>(a.seg_nnz + ti.s),
+      if (count)  // the fixup pass reserves in `fill` (seg_nnz holds the count already)
+        base = atomicAdd(a.fill ? a.fill + ti.s
+                                : reinterpret_cast<unsigned long long*>(a.seg_nnz + ti.s),
                          (unsigned long long)count);
       a.tile_cnt[ti.t] = count;
       a.tile_base[ti.t] = (uint32_t)base;  // <= segment size < 2^32
@@ -384,14 +398,16 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   uint64_t* empty = full + kRing;                                           // [kRing]
   uint64_t* resolved = empty + kRing;                                       // [NB]
   uint32_t* s_ovf = reinterpret_cast<uint32_t*>(resolved + NB);             // [NB][NCW]
+  uint32_t* s_tcnt = s_ovf + NB * NCW;                                      // [NB] count-only
   using SpillRec = typename C::SpillRec;
   SpillRec* spill_blk = reinterpret_cast<SpillRec*>(a.spill) +
                         (size_t)blockIdx.x * NB * NCW * C::SPW;             // [NB][NCW][SPW]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.ntiles_dev && *a.ntiles_dev <= blockIdx.x) return;  // fixup pass: nothing for this block
   for (uint32_t i = tid; i < NB * WORDS; i += blockDim.x)
     buf_bm(i / WORDS)[i % WORDS] = 0;
-  for (uint32_t i = tid; i < NB * NCW; i += blockDim.x) s_ovf[i] = 0;
+  for (uint32_t i = tid; i < NB * NCW + NB; i += blockDim.x) s_ovf[i] = 0;
   if (tid == 0) {
     for (int k = 0; k < kRing; ++k) {
       mbar_init(&full[k], 1);
@@ -414,13 +430,14 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         // Claimed only when the ring can take it: claiming further ahead
         // delays this super-tile's count and lengthens every look-back
         // (measured: 4.29 -> 3.46 TB/s with one-ahead claiming).
-        const uint32_t t = atomicAdd(a.ticket, 1u);
-        if (t >= a.ntiles) {
+        const uint32_t tk = atomicAdd(a.ticket, 1u);
+        if (tk >= (a.ntiles_dev ? *a.ntiles_dev : a.ntiles)) {
           mbar_wait(&empty[k], (ebits >> k) & 1u);
           meta[k].t = END;
           mbar_arrive(&full[k]);
           break;
         }
+        const uint32_t t = a.tile_list ? __ldg(a.tile_list + tk) : tk;
         const int s = a.tile_seg ? (int)__ldg(a.tile_seg + t)
                                  : (a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0);
         const SegDev sg = a.segs ? a.segs[s] : a.seg0;
@@ -441,6 +458,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           m.nsub = nsub;
           m.cnt = cnt;
           m.last = last;
+          m.count_only = a.seg_mode ? __ldg(a.seg_mode + s) : 0u;
           const uint32_t sub_cnt = min(SUB, cnt - g * SUB);
           const uint32_t bytes = (sub_cnt / VE) * 16u;
           mbar_arrive_expect_tx(&full[k], 2 * bytes);
@@ -469,7 +487,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       named_barrier(kStagedBar + b, kEncConsumers + 32);
       const StageMeta ti = tinfo[b];
       if (ti.t == END) break;
-      resolve_tile<DT>(a, ti, buf_bm(b), buf_wpre(b), &s_prefix[b]);
+      resolve_tile<DT>(a, ti, buf_bm(b), buf_wpre(b), &s_prefix[b], s_tcnt + b);
       __syncwarp();
       if (lane == 0) mbar_arrive(&resolved[b]);
     }
@@ -552,7 +570,9 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           memcpy(&pa, ta, 16);
           memcpy(&pb, tb, 16);
         }
-        if (mv) {
+        if (ti.count_only) {
+          mine += __popc(mv);
+        } else if (mv) {
           const uint32_t li = g * SUB + j * VE;
           atomicOr(bm + (li >> 5), mv << (li & 31));
           const T* Pe = reinterpret_cast<const T*>(P) + (size_t)j * VE;
@@ -585,6 +605,13 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       if (lane == 0) mbar_arrive(&empty[kk]);  // this warp is done with the stage
     }
     k = (k + ti.nsub) % kRing;
+    if (ti.count_only) {  // publish the warp's count; nothing to write out later
+      uint32_t w = mine;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(kFullMask, w, o);
+      if (lane == 0 && w) atomicAdd(s_tcnt + b, w);
+      mine = 0;
+    }
     if (C::PRE) cp_async_commit();  // one group per super-tile
     if (tid == 0) tinfo[b] = ti;  // for the resolver only
     __syncwarp();
@@ -833,6 +860,33 @@ int sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+__global__ void fixup_plan_kernel(const uint32_t* tile0, int nseg, const uint64_t* seg_nnz,
+                                  const uint64_t* seg_cap, uint32_t* seg_mode,
+                                  uint32_t* tile_list, uint32_t* ntiles_dev) {
+  __shared__ uint32_t s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
+    const bool dense = seg_nnz[s] > seg_cap[s];
+    if (seg_mode[s] && !dense) {  // counted only, but sparse after all: list its tiles
+      const uint32_t t0 = tile0[s], nt = tile0[s + 1] - t0;
+      const uint32_t o = atomicAdd(&s_n, nt);
+      for (uint32_t k = 0; k < nt; ++k) tile_list[o + k] = t0 + k;
+    }
+    seg_mode[s] = dense ? 1u : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ntiles_dev = s_n;
+}
+
+cudaError_t launch_fixup_plan(const uint32_t* tile0, int nseg, const uint64_t* seg_nnz,
+                              const uint64_t* seg_cap, uint32_t* seg_mode, uint32_t* tile_list,
+                              uint32_t* ntiles_dev, cudaStream_t s) {
+  fixup_plan_kernel<<<1, 1024, 0, s>>>(tile0, nseg, seg_nnz, seg_cap, seg_mode, tile_list,
+                                       ntiles_dev);
+  return cudaGetLastError();
 }
 
 size_t encode_spill_bytes(int dtype, uint32_t blocks) {

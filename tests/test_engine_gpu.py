@@ -219,3 +219,32 @@ def test_single_shard_many_tiles():
     changed = torch.nonzero(p != q).flatten()
     assert torch.equal(d.indices.to(torch.int64) & 0xFFFFFFFF, changed)
     assert torch.equal(d.values.to(torch.int32) & 0xFFFF, (q[changed] - p[changed]) & 0xFFFF)
+
+
+@pytest.mark.parametrize("first", [0.45, 0.0])
+def test_predicted_dense_segments_fixup(restatement, first):
+    """Segments dense in one sync are only counted in the next; when they come
+    out sparse after all, the device-side fixup pass produces their records
+    (and sparse segments predicted sparse that come out dense still fall back)."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.toy_transformer_manifest(layers=3, hidden=64, vocab=384))
+    second = 0.01 if first > 0.2 else 0.45
+    eng.generate(seed=3, density=first)
+    eng.sync_step(sparse=True, density_threshold=0.20)
+    for density in (second, first, second):
+        eng.generate(seed=11, density=density)
+        rep = eng.sync_step(sparse=True, density_threshold=0.20)
+        total = 0
+        for i, (p, desc, off, n) in enumerate(plan.segments):
+            meta = plan.manifest[p]
+            prev, nxt = restatement.gen_pair_bf16(11, meta.name, meta.shape, desc, density)
+            want_i, want_v = restatement.diff_shards(BF16, prev, nxt)
+            delta, codec, nnz = eng.segment_delta(i)
+            assert nnz == want_i.size, meta.name
+            assert codec == ("S" if restatement.is_sparse(nnz, n, 0.20) else "D")
+            if codec == "S":
+                assert delta.indices.cpu().numpy().view(np.uint32).tolist() == want_i.tolist()
+                assert delta.values.cpu().numpy().view(np.uint16).tobytes() == want_v.tobytes()
+            assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
+            total += want_i.size
+        assert rep["nnz"] == total
