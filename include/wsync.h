@@ -178,6 +178,69 @@ ws_status ws_expert_thresholds(int experts, double density, double zipf_s,
                                uint64_t perm_seed, uint64_t* out);
 
 /* ------------------------------------------------------------------------ */
+/* Wire format on the device (codec.cpp:140-263, wire.cpp, key.cpp)          */
+/* ------------------------------------------------------------------------ */
+
+typedef struct ws_payload_info {
+  char codec;             /* 'S' sparse delta, 'D' dense snapshot */
+  int32_t dtype;          /* ws_dtype */
+  int32_t ndims;
+  int32_t index_width;    /* 4 or 8 (sparse), 0 (dense) */
+  int64_t shape[8];
+  uint64_t nnz;           /* sparse records */
+  uint64_t header_bytes;  /* offset of the index (sparse) / value (dense) block */
+  uint64_t total_bytes;
+} ws_payload_info;
+
+/* Bytes of a payload: count = records (codec 'S') or elements ('D'). */
+uint64_t ws_payload_bytes(ws_dtype dtype, int ndims, char codec, int index_width,
+                          uint64_t count);
+
+/* encode_sparse / encode_dense (codec.cpp:145-183) into device memory
+ * (8-byte aligned, ws_payload_bytes long).  F32/I32: "CWS1"/"CWD1"; BF16:
+ * "CWS2"/"CWD2" with 2-byte values.  idx are u32 local indices, written
+ * as index_width (4 or 8) bytes. */
+ws_status ws_encode_sparse_dev(ws_dtype dtype, const int64_t* shape, int ndims,
+                               int index_width, const uint32_t* idx_dev,
+                               const void* val_dev, uint64_t nnz, void* out_dev,
+                               ws_stream_t stream);
+ws_status ws_encode_dense_dev(ws_dtype dtype, const int64_t* shape, int ndims,
+                              const void* data_dev, void* out_dev, ws_stream_t stream);
+
+/* decode_header + size checks of decode_payload (codec.cpp:196-263) on a
+ * payload in device memory: PayloadFormatError exactly where the reference
+ * throws. */
+ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len,
+                              ws_payload_info* info);
+
+/* The records of a sparse payload (after ws_peek_payload_dev): u32 indices
+ * (PayloadFormatError unless strictly ascending, codec.cpp:257) and values.
+ * Synchronises. */
+ws_status ws_decode_sparse_dev(const void* payload_dev, const ws_payload_info* info,
+                               uint32_t* idx_dev, void* val_dev, ws_stream_t stream);
+
+/* frame_crc32 (wire.cpp:9-13, zlib polynomial) of n device byte ranges;
+ * crc_out is host memory.  Synchronises. */
+ws_status ws_crc32_dev(const void* const* data_dev, const uint64_t* len, int n,
+                       uint32_t* crc_out, ws_stream_t stream);
+
+/* The bucket frames of one payload (engine.cpp:136-148 + wire.cpp:35-47):
+ * bucket k = payload[k*bucket_bytes, ...), at least one bucket; frame k =
+ * [key_len u32][keys[k]][len u32][bucket][crc32 u32] at out + frame_off[k]
+ * (frame_off has nbuckets + 1 entries, host).  Synchronises. */
+ws_status ws_encode_bucket_frames_dev(const void* payload_dev, uint64_t payload_len,
+                                      uint64_t bucket_bytes, const char* const* keys,
+                                      const uint64_t* key_lens, int nbuckets,
+                                      void* out_dev, uint64_t out_cap,
+                                      uint64_t* frame_off, ws_stream_t stream);
+
+/* BucketKey::encode (key.cpp:47-69): w|s<step>|p<param>|t<r>.<n>|g<stage>|
+ * d<slice>|c<codec><iw>|q<seq>, '%' and '|' in the name escaped. */
+ws_status ws_bucket_key(uint64_t step, const char* param, int tp_rank, int tp_size,
+                        int pp_stage, ws_shard desc, char codec, int index_width,
+                        uint32_t seq, char* out, uint64_t cap, uint64_t* out_len);
+
+/* ------------------------------------------------------------------------ */
 /* Planner (host, plan.hpp / shard.hpp)                                      */
 /* ------------------------------------------------------------------------ */
 
@@ -241,6 +304,11 @@ ws_status ws_plan_segment(const ws_plan* plan, int i, int32_t* param,
 /* Serving shard i of this rank. */
 ws_status ws_plan_serve_shard(const ws_plan* plan, int i, int32_t* param,
                               ws_shard* desc, uint64_t* offset, uint64_t* n);
+/* The ShardDescriptor fields of segment i that its bucket keys carry
+ * (BucketKey::for_shard, key.hpp:55-67). */
+ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_rank,
+                                     int32_t* tp_size, int32_t* pp_stage);
+
 /* Route i: source segment, destination serving coordinate, number of
  * destination ranks (replicas of that coordinate) and the elements of the
  * box intersection. */
@@ -303,6 +371,13 @@ ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double densit
  * fills it; otherwise it only enqueues (graph-capturable when world == 1). */
 ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts,
                               ws_stream_t stream, ws_report* report);
+
+/* Segment i's payload from the last sync in the reference wire format
+ * (sparse if it was sent sparse, else the dense `next` snapshot), written to
+ * out_dev when non-null (8-byte aligned, info->total_bytes long).
+ * force_wide_index: 8-byte indices (engine.cpp:122).  Synchronises. */
+ws_status ws_engine_payload(ws_engine* eng, int i, int force_wide_index, void* out_dev,
+                            ws_payload_info* info, ws_stream_t stream);
 
 /* Same, with the new snapshot read from HOST memory (pinned for full
  * speed): copies it into the trainer arena that becomes `next` for this

@@ -270,6 +270,13 @@ class Reference:
         L.ref_decode_payload.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int),
                                          C.POINTER(C.c_int), _i64p, _u64p, C.c_void_p,
                                          C.c_void_p]
+        L.ref_bucket_key.argtypes = [C.c_uint64, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.c_int64, C.c_int64, C.c_char, C.c_int, C.c_uint32,
+                                     C.c_char_p, C.c_uint64, _u64p]
+        L.ref_encode_bucket_frame.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                              C.c_void_p, C.c_uint64, _u64p]
+        L.ref_frame_crc32.argtypes = [C.c_void_p, C.c_uint64]
+        L.ref_frame_crc32.restype = C.c_uint32
         L.ref_peek_payload_size.argtypes = [C.c_void_p, C.c_uint64]
         L.ref_peek_payload_size.restype = C.c_int64
         L.ref_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -363,6 +370,47 @@ class Reference:
                                                _ptr(val), idx.size, index_width, _ptr(out),
                                                cap, C.byref(n)))
         return out[:n.value].tobytes()
+
+    def encode_dense(self, dtype, shape, data):
+        data = np.ascontiguousarray(data, NP_DTYPE[dtype])
+        cap = 64 + 8 * len(shape) + data.nbytes
+        out = np.empty(cap, np.uint8)
+        n = C.c_uint64()
+        self._check(self.lib.ref_encode_dense(dtype, _shape(shape), len(shape), _ptr(data),
+                                              _ptr(out), cap, C.byref(n)))
+        return out[:n.value].tobytes()
+
+    def bucket_key(self, step, param, tp_rank, tp_size, pp_stage, desc, codec, iw, seq):
+        """key.cpp:47-69, the reference's own BucketKey::encode."""
+        raw = param.encode("utf-8", "surrogateescape") if isinstance(param, str) else param
+        buf = C.create_string_buffer(8192)
+        n = C.c_uint64()
+        self._check(self.lib.ref_bucket_key(step, raw, tp_rank, tp_size, pp_stage, desc[0],
+                                            desc[1], desc[2], codec.encode(), iw, seq, buf, 8192,
+                                            C.byref(n)))
+        return buf.raw[:n.value]
+
+    def encode_bucket_frame(self, key: bytes, payload: bytes):
+        """wire.cpp:35-47."""
+        out = np.empty(12 + len(key) + len(payload), np.uint8)
+        pl = np.frombuffer(payload, np.uint8) if payload else np.zeros(1, np.uint8)
+        n = C.c_uint64()
+        self._check(self.lib.ref_encode_bucket_frame(key, len(key), _ptr(pl), len(payload),
+                                                     _ptr(out), out.size, C.byref(n)))
+        return out[:n.value].tobytes()
+
+    def decode_payload(self, data: bytes):
+        """codec.cpp:229-263 -> (is_sparse, shape, nnz); raises OracleError."""
+        arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
+        sp, nd, nnz = C.c_int(), C.c_int(), C.c_uint64()
+        shape = (C.c_int64 * 16)()
+        self._check(self.lib.ref_decode_payload(_ptr(arr), len(data), C.byref(sp), C.byref(nd),
+                                                shape, C.byref(nnz), None, None))
+        return bool(sp.value), tuple(shape[:nd.value]), nnz.value
+
+    def frame_crc32(self, data: bytes):
+        arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
+        return int(self.lib.ref_frame_crc32(_ptr(arr), len(data)))
 
     def plan(self, manifest, train, serve):
         """train=(tp,pp,dp), serve=(tp,pp) -> (push list, pull list) of descriptor tuples."""

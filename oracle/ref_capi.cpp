@@ -16,7 +16,9 @@
 #include "coserve/transfer/bench.hpp"
 #include "coserve/transfer/codec.hpp"
 #include "coserve/transfer/engine.hpp"
+#include "coserve/transfer/key.hpp"
 #include "coserve/transfer/plan.hpp"
+#include "coserve/transfer/wire.hpp"
 
 using namespace coserve;
 using namespace coserve::transfer;
@@ -226,6 +228,54 @@ int ref_encode_dense(int dt, const std::int64_t* shape, int nd, const void* data
   } catch (...) {
     return map_exception();
   }
+}
+
+// key.cpp:47-69: BucketKey::encode of one bucket.
+int ref_bucket_key(std::uint64_t step, const char* param, int tp_rank, int tp_size, int pp_stage,
+                   int slice_dim, std::int64_t start, std::int64_t end, char codec, int iw,
+                   std::uint32_t seq, char* out, std::uint64_t cap, std::uint64_t* out_len) {
+  try {
+    BucketKey k;
+    k.step = step;
+    k.param = param;
+    k.tp_rank = tp_rank;
+    k.tp_size = tp_size;
+    k.pp_stage = pp_stage;
+    k.slice_dim = slice_dim;
+    k.start = start;
+    k.end = end;
+    k.codec = codec;
+    k.index_width = iw;
+    k.seq = seq;
+    const std::string e = k.encode();
+    *out_len = e.size();
+    if (e.size() > cap) return 22;
+    std::memcpy(out, e.data(), e.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// wire.cpp:35-47: one bucket frame (lengths, key, payload, zlib crc32).
+int ref_encode_bucket_frame(const char* key, std::uint64_t key_len, const std::uint8_t* payload,
+                            std::uint64_t payload_len, std::uint8_t* out, std::uint64_t cap,
+                            std::uint64_t* out_len) {
+  try {
+    const auto f = encode_bucket_frame(std::string(key, key_len),
+                                       std::vector<std::uint8_t>(payload, payload + payload_len));
+    *out_len = f.size();
+    if (f.size() > cap) return 22;
+    std::memcpy(out, f.data(), f.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// wire.cpp:9-13
+std::uint32_t ref_frame_crc32(const std::uint8_t* data, std::uint64_t len) {
+  return frame_crc32(data, len);
 }
 
 // codec.cpp:196-263: returns 0 and fills is_sparse/ndims/shape/nnz; the

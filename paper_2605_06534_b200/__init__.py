@@ -8,4 +8,5 @@ from .codec import (SparseDelta, apply_delta, copy_overlap, diff_shards,  # noqa
                     extract_shard, expert_thresholds, gen_pair_bf16, reslice_delta,
                     shard_shape)
 from .engine import Plan, ServeConfig, TrainConfig, TransferEngine, nccl_unique_id  # noqa: F401
+from . import wire  # noqa: F401
 from .manifest import MODELS, ModuleKind, ParamMeta, toy_transformer_manifest  # noqa: F401

@@ -130,6 +130,18 @@ class Timing(C.Structure):  # ws_timing
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class PayloadInfo(C.Structure):  # ws_payload_info
+    _fields_ = [("codec", C.c_char), ("dtype", C.c_int32), ("ndims", C.c_int32),
+                ("index_width", C.c_int32), ("shape", C.c_int64 * 8), ("nnz", C.c_uint64),
+                ("header_bytes", C.c_uint64), ("total_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {"codec": self.codec.decode(), "dtype": self.dtype, "ndims": self.ndims,
+                "index_width": self.index_width, "shape": tuple(self.shape[:self.ndims]),
+                "nnz": self.nnz, "header_bytes": self.header_bytes,
+                "total_bytes": self.total_bytes}
+
+
 _vp, _u64, _i64, _i32 = C.c_void_p, C.c_uint64, C.c_int64, C.c_int32
 _SIGS = {
     "ws_status_name": ([C.c_int], C.c_char_p),
@@ -149,6 +161,21 @@ _SIGS = {
     "ws_gen_pair_bf16_dim0": ([_u64, C.c_char_p, C.POINTER(_i64), C.c_int, Shard, _vp, _vp, _vp,
                                _vp], C.c_int),
     "ws_expert_thresholds": ([C.c_int, C.c_double, C.c_double, _u64, C.POINTER(_u64)], C.c_int),
+    "ws_payload_bytes": ([C.c_int, C.c_int, C.c_char, C.c_int, _u64], _u64),
+    "ws_encode_sparse_dev": ([C.c_int, C.POINTER(_i64), C.c_int, C.c_int, _vp, _vp, _u64, _vp,
+                              _vp], C.c_int),
+    "ws_encode_dense_dev": ([C.c_int, C.POINTER(_i64), C.c_int, _vp, _vp, _vp], C.c_int),
+    "ws_peek_payload_dev": ([_vp, _u64, C.POINTER(PayloadInfo)], C.c_int),
+    "ws_decode_sparse_dev": ([_vp, C.POINTER(PayloadInfo), _vp, _vp, _vp], C.c_int),
+    "ws_crc32_dev": ([C.POINTER(_vp), C.POINTER(_u64), C.c_int, C.POINTER(C.c_uint32), _vp],
+                     C.c_int),
+    "ws_encode_bucket_frames_dev": ([_vp, _u64, _u64, C.POINTER(C.c_char_p), C.POINTER(_u64),
+                                     C.c_int, _vp, _u64, C.POINTER(_u64), _vp], C.c_int),
+    "ws_bucket_key": ([_u64, C.c_char_p, C.c_int, C.c_int, C.c_int, Shard, C.c_char, C.c_int,
+                       C.c_uint32, C.c_char_p, _u64, C.POINTER(_u64)], C.c_int),
+    "ws_plan_segment_key_fields": ([_vp, C.c_int, C.POINTER(_i32), C.POINTER(_i32),
+                                    C.POINTER(_i32)], C.c_int),
+    "ws_engine_payload": ([_vp, C.c_int, C.c_int, _vp, C.POINTER(PayloadInfo), _vp], C.c_int),
     "ws_plan_create": ([C.POINTER(Param), C.c_int, C.c_int, C.POINTER(TrainLayout),
                         C.POINTER(ServeLayout), C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "ws_plan_destroy": ([_vp], None),

@@ -115,6 +115,17 @@ ws_status ws_plan_segment(const ws_plan* plan, int i, int32_t* param, ws_shard* 
   return WS_OK;
 }
 
+ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_rank,
+                                     int32_t* tp_size, int32_t* pp_stage) {
+  if (!plan || i < 0 || i >= (int)plan->p->segments().size())
+    return set_error(WS_INVALID_ARGUMENT, "ws_plan_segment_key_fields: index out of range");
+  const Segment& s = plan->p->segments()[i];
+  if (tp_rank) *tp_rank = s.shard.tp_rank;
+  if (tp_size) *tp_size = s.shard.tp_size;
+  if (pp_stage) *pp_stage = s.shard.pp_stage;
+  return WS_OK;
+}
+
 ws_status ws_plan_serve_shard(const ws_plan* plan, int i, int32_t* param, ws_shard* desc,
                               uint64_t* offset, uint64_t* n) {
   if (!plan || i < 0 || i >= (int)plan->p->serve_shards().size())
@@ -185,6 +196,13 @@ ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev, void* train_next_
 ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density, ws_stream_t stream) {
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_generate: null engine");
   return eng->generate(seed, density, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ws_status ws_engine_payload(ws_engine* eng, int i, int force_wide_index, void* out_dev,
+                            ws_payload_info* info, ws_stream_t stream) {
+  if (!eng || !info) return set_error(WS_INVALID_ARGUMENT, "ws_engine_payload: null argument");
+  return eng->payload(i, force_wide_index != 0, out_dev, info,
+                      reinterpret_cast<cudaStream_t>(stream));
 }
 
 ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double density, double zipf_s,

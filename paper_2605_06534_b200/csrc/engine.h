@@ -19,6 +19,7 @@ struct ws_engine {
   ws_status segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
                           char* codec);
   ws_status timing(int reset, ws_timing* out);
+  ws_status payload(int i, bool wide, void* out_dev, ws_payload_info* info, cudaStream_t s);
 
   // caller-owned arenas (ws_engine_bind)
   void* arena[2] = {nullptr, nullptr};
@@ -104,6 +105,7 @@ struct ws_engine {
   uint32_t launch_total_ = 0;
   cudaStream_t last_stream_ = nullptr;
   bool last_sparse_ = true;
+  int last_next_arena_ = 1;
   std::vector<uint64_t> h_nnz_;
   uint64_t* h_nnz_pinned_ = nullptr;
 

@@ -287,6 +287,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   }
   WS_CUDA_TRY(cudaEventRecord(ev_[1], s), "event");
   last_sparse_ = o.sparse != 0;
+  last_next_arena_ = na;
   if (o.sparse && ntiles_) {
     // K1 reserves each super-tile's records with an atomic on its segment's count
     WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
@@ -435,6 +436,46 @@ ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val
   if (val) *val = d_seq_val_;
   if (nnz) *nnz = n;
   if (codec) *codec = sparse ? 'S' : 'D';
+  return WS_OK;
+}
+
+ws_status ws_engine::payload(int i, bool wide, void* out_dev, ws_payload_info* info,
+                             cudaStream_t s) {
+  if (i < 0 || i >= nseg_) return set_error(WS_INVALID_ARGUMENT, "segment index out of range");
+  const uint32_t* idx = nullptr;
+  const void* val = nullptr;
+  uint64_t nnz = 0;
+  char codec = 'D';
+  ws_status st = segment_delta(i, &idx, &val, &nnz, &codec);  // ascending stream
+  if (st != WS_OK) return st;
+  const Segment& sg = plan_.segments()[i];
+  const ParamMeta& p = plan_.manifest()[sg.shard.param];
+  int64_t shape[8];
+  const int nd = (int)p.shape.size();
+  for (int d = 0; d < nd; ++d) shape[d] = p.shape[d];
+  if (sg.shard.d.slice_dim >= 0) shape[sg.shard.d.slice_dim] = sg.shard.d.end - sg.shard.d.start;
+  // pick_index_width (codec.cpp:140-143): local indices of a shard < 2^32 -> 4
+  const int iw = codec == 'S' ? (wide ? 8 : 4) : 0;
+  std::memset(info, 0, sizeof(*info));
+  info->codec = codec;
+  info->dtype = dtype_;
+  info->ndims = nd;
+  info->index_width = iw;
+  for (int d = 0; d < nd; ++d) info->shape[d] = shape[d];
+  info->nnz = codec == 'S' ? nnz : 0;
+  info->header_bytes = 8 + 8 * (uint64_t)nd + (codec == 'S' ? 8 : 0);
+  info->total_bytes = ws_payload_bytes((ws_dtype)dtype_, nd, codec, iw,
+                                       codec == 'S' ? nnz : sg.n);
+  if (!out_dev) return WS_OK;
+  const ws_stream_t ss = reinterpret_cast<ws_stream_t>(s);
+  if (codec == 'S')
+    st = ws_encode_sparse_dev((ws_dtype)dtype_, shape, nd, iw, idx, val, nnz, out_dev, ss);
+  else
+    st = ws_encode_dense_dev((ws_dtype)dtype_, shape, nd,
+                             (const char*)arena[last_next_arena_] + sg.offset * dtype_size(dtype_),
+                             out_dev, ss);
+  if (st != WS_OK) return st;
+  WS_CUDA_TRY(cudaStreamSynchronize(s), "payload");
   return WS_OK;
 }
 

@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from ._lib import BF16, F32, I32, check, lib
-from .codec import SparseDelta, shard_shape
+from .codec import SparseDelta, _ptr, shard_shape
 from .manifest import ParamMeta
 
 TORCH_DTYPE = {BF16: torch.bfloat16, I32: torch.int32, F32: torch.float32}
@@ -86,6 +86,12 @@ class Plan:
             s, c, r, ov = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
             check(lib.ws_plan_route(h, i, C.byref(s), C.byref(c), C.byref(r), C.byref(ov)))
             self.routes.append((s.value, c.value, r.value, ov.value))
+
+    def segment_key_fields(self, i):
+        """(tp_rank, tp_size, pp_stage) of segment i's ShardDescriptor."""
+        r, n, g = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib.ws_plan_segment_key_fields(self.h, i, C.byref(r), C.byref(n), C.byref(g)))
+        return r.value, n.value, g.value
 
     def __del__(self):
         try:
@@ -181,6 +187,34 @@ class TransferEngine:
         with torch.cuda.device(self.device):
             check(lib.ws_engine_timing(self.h, int(reset), C.byref(t)))
         return t.as_dict()
+
+    def segment_payload(self, i, force_wide_index=False):
+        """Segment i's payload from the last sync in the reference wire format
+        (what engine.cpp:116-128 puts on the relay): (uint8 device tensor, info)."""
+        info = _lib.PayloadInfo()
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_payload(self.h, i, int(force_wide_index), None, C.byref(info),
+                                        _stream()))
+            out = torch.empty(max(8, info.total_bytes), dtype=torch.uint8, device=self.device)
+            check(lib.ws_engine_payload(self.h, i, int(force_wide_index), _ptr(out),
+                                        C.byref(info), _stream()))
+        return out[:info.total_bytes], info.as_dict()
+
+    def segment_frames(self, i, step, bucket_bytes=None, force_wide_index=False):
+        """The relay frames of segment i for `step` (engine.cpp:136-148 +
+        wire.cpp:35-47): (uint8 device tensor, keys, frame offsets)."""
+        from . import wire
+        bucket_bytes = bucket_bytes or wire.DEFAULT_BUCKET_BYTES
+        payload, info = self.segment_payload(i, force_wide_index)
+        p, desc, off, n = self.plan.segments[i]
+        r, size, stage = self.plan.segment_key_fields(i)
+        name = self.plan.manifest[p].name
+        nb = wire.num_buckets(info["total_bytes"], bucket_bytes)
+        keys = [wire.bucket_key(step, name, r, size, stage, desc, info["codec"],
+                                info["index_width"], q) for q in range(nb)]
+        with torch.cuda.device(self.device):
+            frames, offs = wire.encode_bucket_frames(payload, bucket_bytes, keys)
+        return frames, keys, offs
 
     def segment_delta(self, i) -> tuple:
         """(SparseDelta of segment i from the last sync, codec 'S'/'D')."""
