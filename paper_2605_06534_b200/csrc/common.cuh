@@ -199,6 +199,14 @@ __device__ __forceinline__ void named_arrive(int id, int threads) {
 }
 
 // ---- system-scope flags (peer GPUs over NVLink) -----------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -212,7 +220,7 @@ __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned l
 }
 // Spins until *p >= want; false after ~`cycles` (a dead peer must not hang us).
 __device__ __forceinline__ bool wait_geq_sys(const unsigned long long* p, unsigned long long want,
-                                             long long cycles = 60ll * 2000000000ll) {
+                                             long long cycles = 10ll * 2000000000ll) {
   const long long t0 = clock64();
   while (ld_acquire_sys(p) < want) {
     if (clock64() - t0 > cycles) return false;

@@ -67,6 +67,11 @@ struct ws_engine::Comm {
   std::vector<void*> peer_serve_map;             // mapped serving allocations (null: me)
   P2PArgs pargs{};
   uint32_t epoch = 0;
+  EntryDest* d_edest = nullptr;
+  unsigned int* d_ent_cnt = nullptr;
+  RecvEntry* d_rentries = nullptr;
+  uint64_t* d_recv_units = nullptr;
+  int nsend_entries = 0;
 
   ~Comm() {
     for (void* p : peer)
@@ -74,6 +79,10 @@ struct ws_engine::Comm {
     for (void* p : peer_serve_map)
       if (p) cudaIpcCloseMemHandle(p);
     cudaFree(d_p2p);
+    cudaFree(d_edest);
+    cudaFree(d_ent_cnt);
+    cudaFree(d_rentries);
+    cudaFree(d_recv_units);
     cudaFree(d_entries);
     cudaFree(d_unit_off);
     cudaFree(d_region_off);
@@ -179,26 +188,59 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
   return size_recv(recv_full_total ? std::max<uint64_t>(4096, (uint64_t)(frac * recv_full_total)) : 0);
 }
 
-// Peer-memory exchange: every rank exports [mailbox | receive buffer] with
-// CUDA IPC; the layouts of all ranks follow from the static plan (no data
-// exchange needed beyond the 64-byte handles, all-gathered over NCCL).
+// Peer-memory exchange: every rank exports [mailbox | counts | records] with
+// CUDA IPC.  The records area holds one region per (source rank, remote
+// entry of that source) whose coordinate is this rank's, sized by the route's
+// overlap; the layouts of all ranks follow from the static plan (no data
+// exchange beyond the 64-byte handles, all-gathered over NCCL).
+namespace {
+// Remote entries of rank g, in the order rank g builds them (init_comm).
+std::vector<int> remote_routes(const Plan& plan, int g) {
+  std::vector<int> out;
+  const auto& rs = plan.routes_of(g);
+  for (int i = 0; i < (int)rs.size(); ++i)
+    if (plan.replicas() > 1 || rs[i].coord != plan.coord_of_rank(g)) out.push_back(i);
+  return out;
+}
+struct RecvLayout {
+  std::vector<std::pair<int, int>> entries;  // (source rank, its remote-entry index)
+  std::vector<uint64_t> off, cap;            // records
+  uint64_t records = 0;
+  size_t head = 0;                           // mailbox + count slots, bytes
+};
+RecvLayout recv_layout(const Plan& plan, int q) {
+  RecvLayout L;
+  const int k = plan.coord_of_rank(q);
+  for (int g = 0; g < plan.world(); ++g) {
+    if (g == q) continue;
+    const std::vector<int> rr = remote_routes(plan, g);
+    for (int e = 0; e < (int)rr.size(); ++e) {
+      const Route& r = plan.routes_of(g)[rr[e]];
+      if (r.coord != k) continue;
+      L.entries.emplace_back(g, e);
+      L.off.push_back(L.records);
+      L.cap.push_back(r.overlap);
+      L.records += r.overlap;
+    }
+  }
+  L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
+  return L;
+}
+}  // namespace
+
 ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
                               const std::vector<uint64_t>& recv_full) {
   Comm* c = comm_;
-  const int me = c->rank, W = c->world, C = c->coords;
+  const int me = c->rank, W = c->world;
   const size_t wb = wire_bytes(dtype_);
-  // receive layout of every rank: one region per source, worst-case sized
-  std::vector<std::vector<uint64_t>> off(W, std::vector<uint64_t>(W + 1, 0));
-  std::vector<std::vector<uint64_t>> cap(W);
-  for (int g = 0; g < W; ++g) {
-    std::vector<uint64_t> s_unused;
-    exchange_caps(plan_, g, &s_unused, &cap[g]);
-    for (int s = 0; s < W; ++s) off[g][s + 1] = off[g][s] + cap[g][s];
-  }
-  const size_t bytes = kMailboxBytes + std::max<uint64_t>(1, off[me][W]) * wb;
+  (void)send_full;
+  (void)recv_full;
+  std::vector<RecvLayout> lay(W);
+  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q);
+  const size_t bytes = lay[me].head + std::max<uint64_t>(1, lay[me].records) * wb;
   if (cudaMalloc(&c->d_p2p, bytes) != cudaSuccess)
     return set_error(WS_CUDA, "p2p: receive buffer allocation failed");
-  WS_CUDA_TRY(cudaMemset(c->d_p2p, 0, kMailboxBytes), "memset mailbox");
+  WS_CUDA_TRY(cudaMemset(c->d_p2p, 0, lay[me].head), "memset mailbox");
   cudaIpcMemHandle_t h;
   if (cudaIpcGetMemHandle(&h, c->d_p2p) != cudaSuccess) {
     cudaGetLastError();
@@ -253,28 +295,61 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
       P.dest[k][r] = nullptr;
       P.dest_rank[k][r] = -1;
     }
-  std::vector<uint64_t> region_cap(C, 0);
-  for (int k = 0; k < C; ++k) {
-    if (!send_full[k]) continue;
+  // sender: where each of my remote entries goes at each replica; only the
+  // coordinates I send to get destinations (their ranks ack exactly the
+  // sources they expect)
+  const std::vector<int> mine = remote_routes(plan_, me);
+  std::vector<char> sends_to(c->coords, 0);
+  for (int e : mine) sends_to[plan_.routes_of(me)[e].coord] = 1;
+  for (int k = 0; k < c->coords; ++k) {
+    if (!sends_to[k]) continue;
     int r = 0;
-    for (int g : c->dests[k]) {
-      P.dest[k][r] = static_cast<char*>(c->peer[g]) + kMailboxBytes + off[g][me] * wb;
-      P.dest_rank[k][r] = g;
-      region_cap[k] = cap[g][me];
+    for (int g : c->dests[k]) P.dest_rank[k][r++] = g;
+  }
+  std::vector<EntryDest> ed(std::max<size_t>(1, mine.size()));
+  for (int e = 0; e < (int)mine.size(); ++e) {
+    EntryDest& D = ed[e];
+    std::memset(&D, 0, sizeof(D));
+    const Route& rt = plan_.routes_of(me)[mine[e]];
+    D.cap = rt.overlap;
+    int r = 0;
+    for (int q : c->dests[rt.coord]) {
+      const RecvLayout& L = lay[q];
+      int pos = -1;
+      for (int j = 0; j < (int)L.entries.size(); ++j)
+        if (L.entries[j].first == me && L.entries[j].second == e) pos = j;
+      if (pos < 0) return set_error(WS_TRANSFER_ERROR, "p2p: entry missing from a receiver layout");
+      char* base = static_cast<char*>(c->peer[q]);
+      D.rec[r] = base + L.head + L.off[pos] * wb;
+      D.cnt[r] = reinterpret_cast<uint32_t*>(base + kMailboxBytes) + pos;
       ++r;
     }
   }
-  P.recv = static_cast<char*>(c->d_p2p) + kMailboxBytes;
-  for (int s = 0; s < W; ++s) {
-    P.recv_off[s] = off[me][s];
-    if (s != me && recv_full[s]) P.expect_mask |= 1u << s;
+  WS_CUDA_TRY(cudaMalloc(&c->d_edest, ed.size() * sizeof(EntryDest)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(c->d_edest, ed.data(), ed.size() * sizeof(EntryDest),
+                         cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMalloc(&c->d_ent_cnt, std::max<size_t>(1, mine.size()) * 4), "cudaMalloc");
+  // receiver: my regions
+  const RecvLayout& L = lay[me];
+  std::vector<RecvEntry> re(std::max<size_t>(1, L.entries.size()));
+  for (int j = 0; j < (int)L.entries.size(); ++j) {
+    re[j] = RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first};
+    P.expect_mask |= 1u << L.entries[j].first;
   }
+  WS_CUDA_TRY(cudaMalloc(&c->d_rentries, re.size() * sizeof(RecvEntry)), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemcpy(c->d_rentries, re.data(), re.size() * sizeof(RecvEntry),
+                         cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMalloc(&c->d_recv_units, (L.entries.size() + 1) * 8), "cudaMalloc");
+  P.edest = c->d_edest;
+  P.ent_cnt = c->d_ent_cnt;
+  P.recv = static_cast<char*>(c->d_p2p) + L.head;
+  P.rentries = c->d_rentries;
+  P.nrecv = (int)L.entries.size();
+  P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_p2p) + kMailboxBytes);
+  P.recv_units = c->d_recv_units;
   P.err = c->d_err;
-  c->region_cap = region_cap;
-  c->region_off.assign(C, 0);
-  WS_CUDA_TRY(cudaMemcpy(c->d_region_off, c->region_off.data(), C * 8, cudaMemcpyHostToDevice),
-              "H2D");
-  WS_CUDA_TRY(cudaMemcpy(c->d_region_cap, region_cap.data(), C * 8, cudaMemcpyHostToDevice), "H2D");
+  if (const char* d = getenv("WSYNC_P2P_DEBUG")) P.debug = atoi(d);
+  c->nsend_entries = (int)mine.size();
   WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "memset");
   c->p2p = true;
   return WS_OK;
@@ -438,7 +513,8 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     // buffers over NVLink; the receiving kernel waits on its own mailbox.
     // No host synchronisation, no collective launch.
     c->pargs.epoch = ++c->epoch;
-    WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
+    if (c->nsend_entries)
+      WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt, 0, c->nsend_entries * 4, s), "memset");
     PackArgs pa{};
     pa.r.entries = c->d_entries;
     pa.r.nentries = c->nentries;
@@ -462,9 +538,8 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (p2p)");
     if (c->nentries) *launches += 2;
     if (c->pargs.expect_mask) {
-      WS_CUDA_TRY(launch_apply_p2p(dtype_, c->pargs, nullptr, serve, sm_count() * 4, s),
-                  "apply (p2p)");
-      *launches += 1;
+      WS_CUDA_TRY(launch_apply_p2p(dtype_, c->pargs, serve, sm_count() * 4, s), "apply (p2p)");
+      *launches += 2;
     }
     pulled_bytes_ = 0;  // filled by exchange_report() when a report is asked for
     return WS_OK;

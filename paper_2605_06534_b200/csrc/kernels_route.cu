@@ -246,17 +246,22 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
       s_u0 = a.unit_off[e];
     }
     __syncthreads();
-    const LocalEntry& E = a.entries[s_entry];
+    const int ei = s_entry;  // s_entry is rewritten for the next unit after the barrier
+    const LocalEntry& E = a.entries[ei];
     const uint64_t lu = u - s_u0;
     __syncthreads();
     const int c = E.coord;
-    const uint64_t roff = P.on ? 0 : pa.region_off[c], rcap = pa.region_cap[c];
+    // P2P: this entry's own region at every replica; NCCL: the coordinate's send region
+    const EntryDest* ED = P.on ? P.edest + ei : nullptr;
+    const uint64_t roff = P.on ? 0 : pa.region_off[c], rcap = P.on ? ED->cap : pa.region_cap[c];
     // emits one record per lane with `valid`, reserving slots warp-wide
     auto emit = [&](bool valid, uint64_t idx, T v, bool set) {
       const unsigned bal = __ballot_sync(kFullMask, valid);
       if (!bal) return;
       unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(pa.region_cnt + c, (unsigned long long)__popc(bal));
+      if (lane == 0)
+        base = P.on ? atomicAdd(P.ent_cnt + ei, (unsigned)__popc(bal))
+                    : atomicAdd(pa.region_cnt + c, (unsigned long long)__popc(bal));
       base = __shfl_sync(kFullMask, base, 0);
       if (!valid) return;
       const uint64_t slot = base + __popc(bal & ((1u << lane) - 1u));
@@ -269,8 +274,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
         if (!P.on) {
           reinterpret_cast<uint64_t*>(pa.send)[roff + slot] = w;
         } else {  // straight into every replica's receive buffer over NVLink
-          for (int r = 0; r < kMaxReplicas && P.dest[c][r]; ++r)
-            reinterpret_cast<uint64_t*>(P.dest[c][r])[slot] = w;
+          for (int r = 0; r < kMaxReplicas && ED->rec[r]; ++r)
+            reinterpret_cast<uint64_t*>(ED->rec[r])[slot] = w;
         }
       } else {
         ulonglong2 w;
@@ -279,14 +284,15 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
         if (!P.on) {
           reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
         } else {
-          for (int r = 0; r < kMaxReplicas && P.dest[c][r]; ++r)
-            reinterpret_cast<ulonglong2*>(P.dest[c][r])[slot] = w;
+          for (int r = 0; r < kMaxReplicas && ED->rec[r]; ++r)
+            reinterpret_cast<ulonglong2*>(ED->rec[r])[slot] = w;
         }
       }
     };
     if (!seg_dense(a, E.seg)) {
       uint64_t k0, k1;
       warp_tile_records(a, E, lu, warp, &k0, &k1);
+      if (P.debug & 2) k1 = k0;
       const uint64_t rec = a.seg_rec[E.seg];
       for (uint64_t kb = k0; kb < k1; kb += 32) {
         const uint64_t k = kb + lane;
@@ -358,22 +364,27 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     }
   }
   if (P.on) {
-    // The last block to finish publishes, per destination, how many records
-    // it now holds from us and this step's flag (after a system fence, so the
-    // records are visible before the flag).
+    // The last block to finish publishes every entry's record count at each
+    // replica (0 for a dense segment whose box went direct: records emitted
+    // for it must not be applied) and then, after a system fence, this step's
+    // flag, so the records are visible before the flag.
+    __shared__ int s_last;
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned long long prev = atomicAdd(P.mailbox + 3 * W, 1ull);
-      if (prev == gridDim.x - 1) {
-        __threadfence();
-        for (int c = 0; c < kMaxWorld; ++c) {
-          const unsigned long long n =
-              *reinterpret_cast<volatile unsigned long long*>(pa.region_cnt + c);
-          for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
-            st_relaxed_sys(P.peer_mailbox[P.dest_rank[c][r]] + P.rank, n);
-        }
-        __threadfence_system();
+    if (threadIdx.x == 0) s_last = atomicAdd(P.mailbox + 3 * W, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int e = threadIdx.x; e < a.nentries; e += blockDim.x) {
+        const EntryDest& D = P.edest[e];
+        const unsigned c0 = *reinterpret_cast<volatile unsigned*>(P.ent_cnt + e);
+        const uint32_t n = (P.dense_direct && seg_dense(a, a.entries[e].seg))
+                               ? 0u : (uint32_t)(c0 < D.cap ? c0 : D.cap);
+        for (int r = 0; r < kMaxReplicas && D.rec[r]; ++r) st_relaxed_sys_u32(D.cnt[r], n);
+      }
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0) {
         for (int c = 0; c < kMaxWorld; ++c)
           for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
             st_release_sys(P.peer_mailbox[P.dest_rank[c][r]] + W + P.rank, P.epoch);
@@ -384,30 +395,56 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
 }
 
 template <int DT>
-__device__ __forceinline__ void apply_record(const void* recv, uint64_t k,
-                                             typename Traits<DT>::T* serve) {
-  using Tr = Traits<DT>;
-  using T = typename Tr::T;
+__device__ __forceinline__ void decode_wire(const void* recv, uint64_t k, uint64_t* i,
+                                            typename Traits<DT>::T* v, bool* set) {
+  using T = typename Traits<DT>::T;
   uint64_t key;
-  T v;
   if constexpr (DT == WS_BF16) {
     const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(recv) + k);
     key = (w & kWireSet) | ((w & ~kWireSet) >> 16);
-    v = (T)(w & 0xffffu);
+    *v = (T)(w & 0xffffu);
   } else {
     const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(recv) + k);
     key = w.x;
-    v = (T)w.y;
+    *v = (T)w.y;
   }
-  const uint64_t i = key & ~kWireSet;
-  serve[i] = (key & kWireSet) ? v : Tr::add(serve[i], v);
+  *i = key & ~kWireSet;
+  *set = (key & kWireSet) != 0;
+}
+
+// Applies the records at positions pos(k) for this thread's k = k0 + j *
+// stride (j < AB) of [0, total): all serving-element loads of the batch are
+// issued before any store, so a thread keeps AB scattered reads in flight.
+constexpr int kApplyBatch = 4;
+template <int DT, typename Pos>
+__device__ __forceinline__ void apply_records(const void* recv, uint64_t total, Pos pos,
+                                              typename Traits<DT>::T* serve) {
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k0 < total;
+       k0 += stride * kApplyBatch) {
+    uint64_t ix[kApplyBatch];
+    T v[kApplyBatch], o[kApplyBatch];
+    bool ok[kApplyBatch], st[kApplyBatch];
+#pragma unroll
+    for (int j = 0; j < kApplyBatch; ++j) {
+      const uint64_t k = k0 + j * stride;
+      ok[j] = k < total;
+      if (ok[j]) decode_wire<DT>(recv, pos(k), &ix[j], &v[j], &st[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kApplyBatch; ++j)
+      if (ok[j] && !st[j]) o[j] = serve[ix[j]];
+#pragma unroll
+    for (int j = 0; j < kApplyBatch; ++j)
+      if (ok[j]) serve[ix[j]] = st[j] ? v[j] : Tr::add(o[j], v[j]);
+  }
 }
 
 template <int DT>
 __global__ void apply_wire_kernel(const void* recv, uint64_t nrec, typename Traits<DT>::T* serve) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nrec;
-       k += (uint64_t)gridDim.x * blockDim.x)
-    apply_record<DT>(recv, k, serve);
+  apply_records<DT>(recv, nrec, [](uint64_t k) { return k; }, serve);
 }
 
 // P2P receiver: every block waits (on its own HBM) for the step flags of the
@@ -422,28 +459,93 @@ __global__ void p2p_ready_kernel(P2PArgs P) {
   }
 }
 
+// P2P receiver, step 1 (one block): wait (acquire) for the step flag of
+// every expected source, then turn the published per-entry counts into a
+// prefix of apply units (kApplyUnit records each).
+constexpr uint64_t kApplyUnit = 8192;
+__global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
+  __shared__ uint64_t s_warp[32];
+  __shared__ uint64_t s_carry;
+  const int W = P.world, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < W && (P.expect_mask & (1u << tid)))
+    if (!wait_geq_sys(P.mailbox + W + tid, P.epoch)) atomicOr(P.err, kErrBitTimeout);
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < P.nrecv; base += 1024) {
+    const int e = base + tid;
+    const uint64_t u = e < P.nrecv
+        ? ((uint64_t)ld_acquire_sys_u32(P.recv_cnt + P.rentries[e].cnt_idx) + kApplyUnit - 1) /
+              kApplyUnit
+        : 0;
+    uint64_t inc = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t w = s_warp[lane];
+      uint64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFullMask, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint64_t excl = s_carry + s_warp[warp] + inc - u;
+    if (e < P.nrecv) P.recv_units[e] = excl;
+    __syncthreads();
+    if (tid == 1023) s_carry = excl + u;
+    __syncthreads();
+  }
+  if (tid == 0) P.recv_units[P.nrecv] = s_carry;
+}
+
+// Step 2: the grid applies unit after unit (one region slice each), then the
+// last block acks the sources so they may refill their regions next step.
 template <int DT>
 __global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
   const int W = P.world;
-  __shared__ unsigned long long s_cnt[kMaxWorld];
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < W; ++s) {
-      s_cnt[s] = 0;
-      if (!(P.expect_mask & (1u << s))) continue;
-      if (!wait_geq_sys(P.mailbox + W + s, P.epoch)) atomicOr(P.err, kErrBitTimeout);
-      s_cnt[s] = *reinterpret_cast<volatile unsigned long long*>(P.mailbox + s);
+  __shared__ int s_e;
+  __shared__ uint64_t s_k0, s_k1;
+  const uint64_t total = (P.debug & 1) ? 0 : P.recv_units[P.nrecv];
+  for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const int e = find_entry(P.recv_units, P.nrecv, u);
+      const RecvEntry R = P.rentries[e];
+      const uint64_t n = P.recv_cnt[R.cnt_idx];
+      const uint64_t lo = (u - P.recv_units[e]) * kApplyUnit;
+      s_e = e;
+      s_k0 = R.off + lo;
+      s_k1 = R.off + (n < lo + kApplyUnit ? n : lo + kApplyUnit);
     }
-  }
-  __syncthreads();
-  uint64_t off[kMaxWorld + 1];
-  off[0] = 0;
-  for (int s = 0; s < W; ++s) off[s + 1] = off[s] + s_cnt[s];
-  const uint64_t total = off[W];
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    int s = 0;
-    while (k >= off[s + 1]) ++s;
-    apply_record<DT>(P.recv, P.recv_off[s] + (k - off[s]), serve);
+    __syncthreads();
+    const uint64_t k0 = s_k0, k1 = s_k1;
+    __syncthreads();
+    // block-local strided apply of [k0, k1)
+    using Tr = Traits<DT>;
+    using T = typename Tr::T;
+    for (uint64_t kb = k0 + threadIdx.x; kb < k1; kb += (uint64_t)blockDim.x * kApplyBatch) {
+      uint64_t ix[kApplyBatch];
+      T v[kApplyBatch], o[kApplyBatch];
+      bool ok[kApplyBatch], st[kApplyBatch];
+#pragma unroll
+      for (int j = 0; j < kApplyBatch; ++j) {
+        const uint64_t k = kb + (uint64_t)j * blockDim.x;
+        ok[j] = k < k1;
+        if (ok[j]) decode_wire<DT>(P.recv, k, &ix[j], &v[j], &st[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kApplyBatch; ++j)
+        if (ok[j] && !st[j]) o[j] = serve[ix[j]];
+#pragma unroll
+      for (int j = 0; j < kApplyBatch; ++j)
+        if (ok[j]) serve[ix[j]] = st[j] ? v[j] : Tr::add(o[j], v[j]);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -476,8 +578,8 @@ cudaError_t launch_p2p_ready(const P2PArgs& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, const uint64_t*, void* serve, int grid,
-                            cudaStream_t s) {
+cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, void* serve, int grid, cudaStream_t s) {
+  p2p_recv_plan_kernel<<<1, 1024, 0, s>>>(p);
   switch (dtype) {
     case WS_BF16: apply_p2p_kernel<WS_BF16><<<grid, 256, 0, s>>>(p, (uint16_t*)serve); break;
     case WS_I32: apply_p2p_kernel<WS_I32><<<grid, 256, 0, s>>>(p, (uint32_t*)serve); break;

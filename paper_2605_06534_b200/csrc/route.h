@@ -84,6 +84,7 @@ constexpr int kMaxReplicas = 8;
 // receiver's own stream did to its serving arena before the sync.
 struct P2PArgs {
   int32_t on;                       // 0: NCCL mode (send region + host exchange)
+  int32_t debug;                    // perf experiments (WSYNC_P2P_DEBUG): 1 no scatter, 2 no records
   int32_t world, rank;
   uint32_t epoch;                   // this step's number (>= 1), equal on every rank
   unsigned long long* mailbox;                        // local
@@ -95,11 +96,32 @@ struct P2PArgs {
   // arena, 2 bytes per bf16 element over NVLink instead of an 8-byte record.
   int32_t dense_direct;
   void* serve_dst[kMaxWorld][kMaxReplicas];           // per coordinate: replica serving arenas
-  // receiver side
-  const void* recv;                                   // local records, partitioned by source
-  uint64_t recv_off[kMaxWorld];                       // per source, records
+  // sender side: one record region per (remote entry, replica) at the
+  // replica, filled through per-entry counters; counts published at the end
+  const struct EntryDest* edest;                      // per remote entry
+  unsigned int* ent_cnt;                              // per remote entry, zeroed each step
+  // receiver side: one region per (source, entry) that sends here
+  const void* recv;                                   // local record area
+  const struct RecvEntry* rentries;
+  int32_t nrecv;
+  const uint32_t* recv_cnt;                           // local count slots (written by the sources)
+  uint64_t* recv_units;                               // nrecv + 1: apply units, prefix
   uint32_t expect_mask;                               // sources that send to this rank
   uint32_t* err;                                      // WS_ERRBIT_* (timeouts, capacity)
+};
+
+// Where one remote entry's records go at each replica of its coordinate.
+struct EntryDest {
+  void* rec[kMaxReplicas];      // record region at replica r (null-terminated)
+  uint32_t* cnt[kMaxReplicas];  // its count slot at replica r
+  uint64_t cap;                 // region capacity, records (the route's overlap)
+};
+// A region of this rank's receive area: records [off, off + count) where
+// count is the source's published count for it.
+struct RecvEntry {
+  uint64_t off;                 // records from the start of the record area
+  uint32_t cnt_idx;
+  uint32_t src;
 };
 constexpr uint32_t kErrBitTimeout = 0x4u;
 constexpr size_t kMailboxBytes = 4096;
@@ -123,10 +145,9 @@ cudaError_t launch_apply_wire(int dtype, const void* recv, uint64_t nrec, void* 
 // this rank's serving arena for step p.epoch.
 cudaError_t launch_p2p_ready(const P2PArgs& p, cudaStream_t s);
 
-// P2P receiver: waits for every expected source's step flag, applies all
-// records that arrived in the local receive buffer, acks the sources.
-cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, const uint64_t* region_cnt_unused,
-                            void* serve, int grid, cudaStream_t s);
+// P2P receiver: waits for every expected source's step flag, applies the
+// records of every (source, entry) region (its published count), acks.
+cudaError_t launch_apply_p2p(int dtype, const P2PArgs& p, void* serve, int grid, cudaStream_t s);
 
 // Fills a LocalEntry for the route src -> dst of a tensor of `full`.
 LocalEntry make_local_entry(int dtype, const int64_t* full, int nd, int seg, const ws_shard& src,
