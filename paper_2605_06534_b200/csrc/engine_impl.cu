@@ -317,6 +317,10 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     a.epoch = next_epoch();
     a.ticket = d_ticket_;
     if (count_only_) a.seg_mode = d_seg_mode_;
+    if (plan_.world() > 1) {
+      st = exchange_fuse_k1(a, s);
+      if (st != WS_OK) return st;
+    }
     WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
     ++launches;
     if (count_only_) {

@@ -67,6 +67,9 @@ struct ws_engine::Comm {
   std::vector<void*> peer_serve_map;             // mapped serving allocations (null: me)
   P2PArgs pargs{};
   uint32_t epoch = 0;
+  RemoteMap* d_rmaps = nullptr;                  // my remote routes grouped by segment (K1)
+  uint32_t* d_rseg_first = nullptr;
+  bool k1_emit = false;                          // this sync's records went out from K1
   EntryDest* d_edest = nullptr;
   unsigned int* d_ent_cnt = nullptr;
   RecvEntry* d_rentries = nullptr;
@@ -80,6 +83,8 @@ struct ws_engine::Comm {
       if (p) cudaIpcCloseMemHandle(p);
     cudaFree(d_p2p);
     cudaFree(d_edest);
+    cudaFree(d_rmaps);
+    cudaFree(d_rseg_first);
     cudaFree(d_ent_cnt);
     cudaFree(d_rentries);
     cudaFree(d_recv_units);
@@ -329,6 +334,43 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
   WS_CUDA_TRY(cudaMemcpy(c->d_edest, ed.data(), ed.size() * sizeof(EntryDest),
                          cudaMemcpyHostToDevice), "H2D");
   WS_CUDA_TRY(cudaMalloc(&c->d_ent_cnt, std::max<size_t>(1, mine.size()) * 4), "cudaMalloc");
+  {  // the same routes as K1 sees them, grouped by segment
+    const auto& segs = plan_.segments();
+    std::vector<std::vector<RemoteMap>> by_seg(segs.size());
+    for (int e = 0; e < (int)mine.size(); ++e) {
+      const Route& rt = plan_.routes_of(me)[mine[e]];
+      const ParamMeta& p = plan_.manifest()[rt.dst.param];
+      const LocalEntry le = make_local_entry(dtype_, p.shape.data(), (int)p.shape.size(), rt.seg,
+                                             segs[rt.seg].shard.d, rt.dst.d, rt.dst_offset);
+      RemoteMap m;
+      std::memset(&m, 0, sizeof(m));
+      m.identity = le.identity;
+      m.keep_lo = le.keep_lo;
+      m.keep_hi = le.keep_hi;
+      m.shift = le.shift;
+      m.dst_base = le.dst_base;
+      m.map = le.map;
+      m.cap = ed[e].cap;
+      m.cnt = c->d_ent_cnt + e;
+      for (int r = 0; r < kMaxReplicas && r < 8; ++r) m.rec[r] = ed[e].rec[r];
+      by_seg[rt.seg].push_back(m);
+    }
+    std::vector<RemoteMap> flat;
+    std::vector<uint32_t> first(segs.size() + 1, 0);
+    for (size_t sg = 0; sg < segs.size(); ++sg) {
+      first[sg] = (uint32_t)flat.size();
+      flat.insert(flat.end(), by_seg[sg].begin(), by_seg[sg].end());
+    }
+    first[segs.size()] = (uint32_t)flat.size();
+    WS_CUDA_TRY(cudaMalloc(&c->d_rmaps, std::max<size_t>(1, flat.size()) * sizeof(RemoteMap)),
+                "cudaMalloc");
+    if (!flat.empty())
+      WS_CUDA_TRY(cudaMemcpy(c->d_rmaps, flat.data(), flat.size() * sizeof(RemoteMap),
+                             cudaMemcpyHostToDevice), "H2D");
+    WS_CUDA_TRY(cudaMalloc(&c->d_rseg_first, first.size() * 4), "cudaMalloc");
+    WS_CUDA_TRY(cudaMemcpy(c->d_rseg_first, first.data(), first.size() * 4,
+                           cudaMemcpyHostToDevice), "H2D");
+  }
   // receiver: my regions
   const RecvLayout& L = lay[me];
   std::vector<RecvEntry> re(std::max<size_t>(1, L.entries.size()));
@@ -495,11 +537,42 @@ void ws_engine::destroy_comm() {
 
 ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
   Comm* c = comm_;
+  if (c) c->k1_emit = false;  // set again by exchange_fuse_k1 when K1 emits this sync
   if (!c || !c->p2p || !c->pargs.dense_direct || !c->pargs.expect_mask) return WS_OK;
   P2PArgs p = c->pargs;
   p.epoch = c->epoch + 1;  // the number exchange() gives this sync
   WS_CUDA_TRY(launch_p2p_ready(p, s), "p2p ready");
   *launches += 1;
+  return WS_OK;
+}
+
+ws_status ws_engine::exchange_fuse_k1(EncodeArgs& a, cudaStream_t s) {
+  Comm* c = comm_;
+  if (c) c->k1_emit = false;
+  // Opt-in (WSYNC_FUSED_REMOTE=1).  Measured on 2 and 4 B200s it is slower
+  // than the separate pack: the ballots, counters and NVLink stores sit on
+  // K1's issue-bound critical path (+0.4 ms at 1%), and waiting for the
+  // previous step's acks inside K1 couples the ranks' start times; the pack
+  // it replaces costs 0.2-0.5 ms.  See DESIGN.md §6.
+  static const bool enabled = [] {
+    const char* e = getenv("WSYNC_FUSED_REMOTE");
+    return e && e[0] == '1';
+  }();
+  // Only with direct dense boxes: a segment that comes out dense after K1
+  // emitted some of its records then reports 0 of them (pack_kernel).
+  if (!c || !c->p2p || !c->pargs.dense_direct || dtype_ != WS_BF16 || !enabled ||
+      !c->nsend_entries)
+    return WS_OK;
+  WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt, 0, c->nsend_entries * 4, s), "memset");
+  a.remote.maps = c->d_rmaps;
+  a.remote.seg_first = c->d_rseg_first;
+  a.remote.ack = c->pargs.mailbox + 2 * c->world;
+  a.remote.ack_mask = 0;
+  for (int k = 0; k < kMaxWorld; ++k)
+    for (int r = 0; r < kMaxReplicas && c->pargs.dest_rank[k][r] >= 0; ++r)
+      a.remote.ack_mask |= 1u << c->pargs.dest_rank[k][r];
+  a.remote.epoch = c->epoch + 1;  // the number exchange() gives this sync
+  c->k1_emit = true;
   return WS_OK;
 }
 
@@ -513,12 +586,13 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     // buffers over NVLink; the receiving kernel waits on its own mailbox.
     // No host synchronisation, no collective launch.
     c->pargs.epoch = ++c->epoch;
-    if (c->nsend_entries)
+    if (c->nsend_entries && !c->k1_emit)
       WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt, 0, c->nsend_entries * 4, s), "memset");
     PackArgs pa{};
     pa.r.entries = c->d_entries;
     pa.r.nentries = c->nentries;
     pa.r.sparse = o.sparse ? 1 : 0;
+    pa.r.k1_emitted = c->k1_emit && o.sparse ? 1 : 0;
     pa.r.seg_nnz = d_nnz_;
     pa.r.seg_cap = d_cap_;
     pa.r.seg_rec = d_rec_;

@@ -59,6 +59,28 @@ struct FuseEntry {
   Remap map;
 };
 
+// A route of a segment to another GPU as K1 sees it (engine, P2P, bf16):
+// K1's flush re-indexes each record into the destination shard and stores it
+// as a wire record straight into every replica's receive region over NVLink,
+// so the transfer overlaps the encode tile by tile.
+struct RemoteMap {
+  int32_t identity;
+  uint32_t keep_lo, keep_hi;     // identity: keep segment-local i in [keep_lo, keep_hi)
+  int64_t shift;                 // identity: destination-local = i + shift
+  uint64_t dst_base;             // destination shard offset in the serving arena
+  Remap map;                     // general box re-index
+  uint64_t cap;                  // region capacity (records)
+  unsigned int* cnt;             // the route's slot counter (zeroed per sync)
+  void* rec[8];                  // region at each replica (null-terminated)
+};
+struct RemoteEmit {
+  const RemoteMap* maps;         // grouped by segment
+  const uint32_t* seg_first;     // nseg + 1
+  const unsigned long long* ack; // this rank's mailbox ack words (per peer)
+  uint32_t ack_mask;             // peers whose ack of the previous step must be seen first
+  uint32_t epoch;                // this step
+};
+
 struct EncodeArgs {
   const void* prev;
   const void* next;
@@ -99,6 +121,7 @@ struct EncodeArgs {
   const uint32_t* tile_list;
   const uint32_t* ntiles_dev;
   unsigned long long* fill;
+  RemoteEmit remote;             // maps == null: no fused remote emission
 };
 
 // Between the two K1 launches of an engine sync: lists the super-tiles of

@@ -127,7 +127,7 @@ struct EncCfg {
       WORDS * 6 + (size_t)K * kEncConsumers * (sizeof(T) + 2 + (PRE ? 4 : 0));
   static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
                                   (kRing + NB) * sizeof(StageMeta) + NB * 8 +
-                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + NB * 4 + 32;
+                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + NB * 4 + 4 + 32;
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
   static_assert(SUPER <= 65536, "u16 in-tile index");
   static_assert(WORDS % 128 == 0, "bitmap words per resolver lane in 16-byte loads");
@@ -244,6 +244,36 @@ __device__ __forceinline__ typename Traits<DT>::T* fuse_target(const FuseEntry* 
 #define WS_FLUSH_BATCH 2
 #endif
 
+// Fused remote emission (bf16): the record (segment-local i, value v) of a
+// lane with `valid`, re-indexed into route M's destination shard, stored as a
+// wire record (serving index << 16 | value) into every replica's region.
+// Warp-collective: every lane calls it.
+__device__ __forceinline__ void emit_remote(const RemoteMap& M, bool valid, uint32_t i,
+                                            uint16_t v) {
+  uint64_t d = 0;
+  if (valid) {
+    if (M.identity) {
+      valid = i >= M.keep_lo && i < M.keep_hi;
+      d = (uint64_t)((int64_t)i + M.shift);
+    } else {
+      d = remap_index(M.map, i);
+      valid = d != ~0ull;
+    }
+  }
+  const unsigned bal = __ballot_sync(kFullMask, valid);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(M.cnt, (unsigned)__popc(bal));
+  base = __shfl_sync(kFullMask, base, 0);
+  if (!valid) return;
+  const uint64_t slot = (uint64_t)base + __popc(bal & ((1u << lane) - 1u));
+  if (slot >= M.cap) return;  // cannot happen: the capacity is the route's overlap
+  const uint64_t w = ((M.dst_base + d) << 16) | (uint64_t)v;
+#pragma unroll 1
+  for (int r = 0; r < 8 && M.rec[r]; ++r) reinterpret_cast<uint64_t*>(M.rec[r])[slot] = w;
+}
+
 // Ascending rank of in-tile element li among the super-tile's changes.
 __device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint16_t* wpre, uint32_t li) {
   const uint32_t w = li >> 5;
@@ -260,7 +290,8 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
                                             const uint16_t* sidx,
                                             const typename Traits<DT>::T* sval,
                                             const uint32_t* spre, uint32_t* ovf,
-                                            const typename EncCfg<DT>::SpillRec* spill) {
+                                            const typename EncCfg<DT>::SpillRec* spill,
+                                            const uint32_t* s_acks) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
@@ -275,6 +306,14 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
     // identity-mapped fused segments had their serving words fetched at staging
     const bool pre = C::PRE && fz && fz->mode == 1;
+    // routes of this segment to other GPUs (bf16 engine, P2P): emitted here
+    uint32_t rm0 = 0, rm1 = 0;
+    if (DT == WS_BF16 && a.remote.maps) {
+      rm0 = a.remote.seg_first[ti.seg];
+      rm1 = a.remote.seg_first[ti.seg + 1];
+      if (rm1 > rm0)
+        while (!ld_acquire_cta_u32(s_acks)) __nanosleep(256);
+    }
     T* serve = reinterpret_cast<T*>(a.serve);
     const uint32_t mine = ti.mine < (uint32_t)K ? ti.mine : (uint32_t)K;
     uint32_t start = mine;
@@ -331,33 +370,44 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         out_val[ti.rec + pos[j]] = vv[j];
         if (tp[j]) *tp[j] = Tr::add(old[j], vv[j]);
       }
+      if constexpr (DT == WS_BF16)
+        for (uint32_t q = rm0; q < rm1; ++q)
+#pragma unroll
+          for (int j = 0; j < FB; ++j)
+            emit_remote(a.remote.maps[q], pos[j] != ~0ull, ii[j], (uint16_t)vv[j]);
     }
     // changes past the slots: from this warp's spill region (written at
     // staging, still in L2), in any order -- the bitmap gives their ranks
     const uint32_t nov = *ovf;
-    for (uint32_t r0 = 0; r0 < nov; r0 += 32) {
+    for (uint32_t r0 = 0; r0 < nov; r0 += 32) {  // warp-uniform trip count
       const uint32_t r = r0 + lane;
-      if (r >= nov) continue;
-      uint32_t li;
-      T dv;
-      if constexpr (sizeof(T) == 2) {
-        const uint32_t x = spill[r];
-        li = x & 0xffffu;
-        dv = (T)(x >> 16);
-      } else {
-        const uint2 x = spill[r];
-        li = x.x;
-        dv = (T)x.y;
-      }
-      const uint64_t pos = prefix + tile_rank(bm, wpre, li);
-      if (pos < ti.cap) {
-        a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li);
-        out_val[ti.rec + pos] = dv;
-        if (fz) {
-          T* p = fuse_target<DT>(fz, serve, (uint32_t)(e0 + li));
-          if (p) *p = Tr::add(*p, dv);
+      bool ok = r < nov;
+      uint32_t li = 0;
+      T dv = 0;
+      if (ok) {
+        if constexpr (sizeof(T) == 2) {
+          const uint32_t x = spill[r];
+          li = x & 0xffffu;
+          dv = (T)(x >> 16);
+        } else {
+          const uint2 x = spill[r];
+          li = x.x;
+          dv = (T)x.y;
+        }
+        const uint64_t pos = prefix + tile_rank(bm, wpre, li);
+        ok = pos < ti.cap;
+        if (ok) {
+          a.out_idx[ti.rec + pos] = (uint32_t)(e0 + li);
+          out_val[ti.rec + pos] = dv;
+          if (fz) {
+            T* p = fuse_target<DT>(fz, serve, (uint32_t)(e0 + li));
+            if (p) *p = Tr::add(*p, dv);
+          }
         }
       }
+      if constexpr (DT == WS_BF16)
+        for (uint32_t q = rm0; q < rm1; ++q)
+          emit_remote(a.remote.maps[q], ok, (uint32_t)(e0 + li), (uint16_t)dv);
     }
   }
   __syncwarp();  // every lane of the warp is done reading the bitmap
@@ -399,6 +449,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   uint64_t* resolved = empty + kRing;                                       // [NB]
   uint32_t* s_ovf = reinterpret_cast<uint32_t*>(resolved + NB);             // [NB][NCW]
   uint32_t* s_tcnt = s_ovf + NB * NCW;                                      // [NB] count-only
+  uint32_t* s_acks = s_tcnt + NB;                                           // remote acks seen
   using SpillRec = typename C::SpillRec;
   SpillRec* spill_blk = reinterpret_cast<SpillRec*>(a.spill) +
                         (size_t)blockIdx.x * NB * NCW * C::SPW;             // [NB][NCW][SPW]
@@ -407,7 +458,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   if (a.ntiles_dev && *a.ntiles_dev <= blockIdx.x) return;  // fixup pass: nothing for this block
   for (uint32_t i = tid; i < NB * WORDS; i += blockDim.x)
     buf_bm(i / WORDS)[i % WORDS] = 0;
-  for (uint32_t i = tid; i < NB * NCW + NB; i += blockDim.x) s_ovf[i] = 0;
+  for (uint32_t i = tid; i < NB * NCW + NB + 1; i += blockDim.x) s_ovf[i] = 0;
   if (tid == 0) {
     for (int k = 0; k < kRing; ++k) {
       mbar_init(&full[k], 1);
@@ -425,14 +476,37 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (lane == 0) {
       uint32_t ebits = (1u << kRing) - 1u;  // the first wait on each empty barrier passes
       const uint64_t pol = policy_evict_first();
+      // fused remote emission: the receivers must have consumed last step's
+      // records before this step's reach their regions.  Polled between
+      // super-tiles (never blocking the stream); emitting warps wait on the flag.
+      uint32_t pending = a.remote.maps ? a.remote.ack_mask : 0u;
+      auto poll_acks = [&] {
+        for (uint32_t m = pending; m; m &= m - 1) {
+          const int q = __ffs(m) - 1;
+          if (ld_acquire_sys(a.remote.ack + q) >= a.remote.epoch - 1) pending &= ~(1u << q);
+        }
+        if (!pending) st_release_cta_u32(s_acks, 1u);
+      };
+      if (!a.remote.maps) *s_acks = 1u;
+      // waiting for a free stage keeps polling the acks: emitting consumers
+      // hold their stages until the flag is up
+      auto wait_empty = [&](int kk) {
+        while (pending) {
+          if (mbar_try_wait(&empty[kk], (ebits >> kk) & 1u)) return;
+          poll_acks();
+        }
+        mbar_wait(&empty[kk], (ebits >> kk) & 1u);
+      };
       int k = 0;
       while (true) {
         // Claimed only when the ring can take it: claiming further ahead
         // delays this super-tile's count and lengthens every look-back
         // (measured: 4.29 -> 3.46 TB/s with one-ahead claiming).
+        if (pending) poll_acks();
         const uint32_t tk = atomicAdd(a.ticket, 1u);
         if (tk >= (a.ntiles_dev ? *a.ntiles_dev : a.ntiles)) {
-          mbar_wait(&empty[k], (ebits >> k) & 1u);
+          while (pending) poll_acks();
+          wait_empty(k);
           meta[k].t = END;
           mbar_arrive(&full[k]);
           break;
@@ -448,7 +522,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         const uint32_t nsub = (cnt + SUB - 1) / SUB;
         const uint32_t last = (a.tile0 ? __ldg(a.tile0 + s + 1) : a.ntiles) == t + 1;
         for (uint32_t g = 0; g < nsub; ++g) {
-          mbar_wait(&empty[k], (ebits >> k) & 1u);
+          wait_empty(k);
           ebits ^= 1u << k;
           StageMeta& m = meta[k];
           m.sg = sg;
@@ -511,7 +585,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     rbits ^= 1u << pb;
     flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
                     buf_pre(pb), s_ovf + pb * NCW + warp,
-                    spill_blk + ((size_t)pb * NCW + warp) * C::SPW);
+                    spill_blk + ((size_t)pb * NCW + warp) * C::SPW, s_acks);
   };
   PendingSlice pend0{}, pend1{};  // super-tiles i-2 and i-1 of this thread
   const uint64_t pol_keep = policy_evict_last();

@@ -53,6 +53,7 @@ __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const Lo
     return e.box.rows * per_row;
   }
   if (a.fused && a.fuse_on[e.seg]) return 0;  // K1 applied the sparse records as it wrote them
+  if (a.k1_emitted) return 0;                  // K1 stored them into the receivers' regions
   if (a.seg_nnz[e.seg] == 0) return 0;
   uint32_t ta, tb;
   entry_tiles(a, e, &ta, &tb);

@@ -50,6 +50,7 @@ struct RouteSideArgs {
   uint32_t tile_elems;          // elements per super-tile
   const SegDev* segs;           // segment sizes
   int32_t stream_apply;         // local routes: dense-ish sparse segments apply by streaming
+  int32_t k1_emitted;           // pack: K1 already stored the sparse records remotely
   const void* train_prev;
   const void* train_next;
   void* serve;
