@@ -284,7 +284,7 @@ __device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint16_t
 // super-tile (warp-cooperative: record r of the warp is slot r - start(l)
 // of the lane l owning it), then the spilled ones, then clears its bitmap
 // words for the buffer's next super-tile.
-template <int DT>
+template <int DT, bool REMOTE>
 __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
                                             uint64_t prefix, uint32_t* bm, const uint16_t* wpre,
                                             const uint16_t* sidx,
@@ -308,7 +308,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
     const bool pre = C::PRE && fz && fz->mode == 1;
     // routes of this segment to other GPUs (bf16 engine, P2P): emitted here
     uint32_t rm0 = 0, rm1 = 0;
-    if (DT == WS_BF16 && a.remote.maps) {
+    if (REMOTE) {
       rm0 = a.remote.seg_first[ti.seg];
       rm1 = a.remote.seg_first[ti.seg + 1];
       if (rm1 > rm0)
@@ -370,7 +370,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         out_val[ti.rec + pos[j]] = vv[j];
         if (tp[j]) *tp[j] = Tr::add(old[j], vv[j]);
       }
-      if constexpr (DT == WS_BF16)
+      if constexpr (REMOTE)
         for (uint32_t q = rm0; q < rm1; ++q)
 #pragma unroll
           for (int j = 0; j < FB; ++j)
@@ -405,7 +405,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
           }
         }
       }
-      if constexpr (DT == WS_BF16)
+      if constexpr (REMOTE)
         for (uint32_t q = rm0; q < rm1; ++q)
           emit_remote(a.remote.maps[q], ok, (uint32_t)(e0 + li), (uint16_t)dv);
     }
@@ -419,7 +419,7 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         bm[(g * SUB + (v * kEncConsumers + threadIdx.x) * VE) >> 5] = 0;
 }
 
-template <int DT>
+template <int DT, bool REMOTE>
 __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   using C = EncCfg<DT>;
   using Tr = Traits<DT>;
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       // fused remote emission: the receivers must have consumed last step's
       // records before this step's reach their regions.  Polled between
       // super-tiles (never blocking the stream); emitting warps wait on the flag.
-      uint32_t pending = a.remote.maps ? a.remote.ack_mask : 0u;
+      uint32_t pending = REMOTE ? a.remote.ack_mask : 0u;
       auto poll_acks = [&] {
         for (uint32_t m = pending; m; m &= m - 1) {
           const int q = __ffs(m) - 1;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         }
         if (!pending) st_release_cta_u32(s_acks, 1u);
       };
-      if (!a.remote.maps) *s_acks = 1u;
+      if (!REMOTE) *s_acks = 1u;
       // waiting for a free stage keeps polling the acks: emitting consumers
       // hold their stages until the flag is up
       auto wait_empty = [&](int kk) {
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     }
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
-    flush_slice<DT>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
+    flush_slice<DT, REMOTE>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
                     buf_pre(pb), s_ovf + pb * NCW + warp,
                     spill_blk + ((size_t)pb * NCW + warp) * C::SPW, s_acks);
   };
@@ -976,11 +976,13 @@ size_t encode_spill_bytes(int dtype, uint32_t blocks) {
 cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(encode_kernel<WS_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(encode_kernel<WS_BF16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)EncCfg<WS_BF16>::kSmem);
-    cudaFuncSetAttribute(encode_kernel<WS_I32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(encode_kernel<WS_BF16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)EncCfg<WS_BF16>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_I32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)EncCfg<WS_I32>::kSmem);
-    cudaFuncSetAttribute(encode_kernel<WS_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(encode_kernel<WS_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)EncCfg<WS_F32>::kSmem);
     attr_done = true;
   }
@@ -996,9 +998,14 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
   cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   switch (dtype) {
-    case WS_BF16: encode_kernel<WS_BF16><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2); break;
-    case WS_I32: encode_kernel<WS_I32><<<grid, kEncodeBlock, EncCfg<WS_I32>::kSmem, s>>>(a2); break;
-    case WS_F32: encode_kernel<WS_F32><<<grid, kEncodeBlock, EncCfg<WS_F32>::kSmem, s>>>(a2); break;
+    case WS_BF16:
+      if (a2.remote.maps)
+        encode_kernel<WS_BF16, true><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
+      else
+        encode_kernel<WS_BF16, false><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
+      break;
+    case WS_I32: encode_kernel<WS_I32, false><<<grid, kEncodeBlock, EncCfg<WS_I32>::kSmem, s>>>(a2); break;
+    case WS_F32: encode_kernel<WS_F32, false><<<grid, kEncodeBlock, EncCfg<WS_F32>::kSmem, s>>>(a2); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
