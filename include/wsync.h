@@ -372,6 +372,49 @@ ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double densit
 ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts,
                               ws_stream_t stream, ws_report* report);
 
+/* A relay (relay.hpp:27-35) seen through C callbacks: the binding of the
+ * reference's Relay / RelayFactory.  get_any returns the
+ * length of the payload of the first of the n keys present (its index in
+ * *hit), copying it to out when it fits in cap (call again with a larger
+ * buffer otherwise); -1 = RelayTimeout, other negatives = errors. */
+typedef struct ws_relay {
+  void* ctx;
+  int (*put)(void* ctx, const char* key, uint64_t key_len, const uint8_t* data,
+             uint64_t len);
+  int64_t (*get_any)(void* ctx, const char* const* keys, const uint64_t* key_lens, int n,
+                     int timeout_ms, int* hit, uint8_t* out, uint64_t cap);
+} ws_relay;
+
+typedef struct ws_relay_options {
+  uint64_t bucket_bytes;       /* SyncOptions::bucket_bytes (64 MiB) */
+  uint64_t pull_batch_bytes;   /* SyncOptions::pull_batch_bytes */
+  double push_bytes_per_s;     /* TokenBucket pacing per direction, 0 = unlimited */
+  double pull_bytes_per_s;
+  double burst_bytes;
+  int32_t timeout_ms;          /* SyncOptions::relay_timeout_ms */
+  int32_t async;               /* SyncMode::Async (1) or Batch (0) */
+  int32_t force_wide_index;
+  int32_t staging_buffers;     /* pinned staging depth per direction (>= 2) */
+} ws_relay_options;
+
+typedef struct ws_relay_report { /* TransferReport (engine.hpp:34-42) */
+  double wall_s, push_s, pull_s, encode_s, apply_s;
+  uint64_t pushed_bytes, pulled_bytes, push_buckets, pull_buckets;
+  uint32_t dense_shards, sparse_shards;
+} ws_relay_report;
+
+/* TransferEngine::sync_step across clusters (engine.cpp:66-254) with this
+ * GPU as both sides: the pusher encodes on the GPU (K1 + payloads) and puts
+ * every shard's buckets (BucketKey keys, bucket_bytes) through pinned
+ * double-buffered staging; the puller fetches the buckets of every source of
+ * its serving shards (plan_pulls; codec probed from the first key as
+ * engine.cpp:164-171), stages them to the GPU, decodes, reslices and applies
+ * there.  Async runs both sides concurrently, Batch pushes first.  world ==
+ * 1 plans only. */
+ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step, const ws_sync_options* opts,
+                               const ws_relay_options* relay_opts, const ws_relay* relay,
+                               ws_relay_report* report);
+
 /* Segment i's payload from the last sync in the reference wire format
  * (sparse if it was sent sparse, else the dense `next` snapshot), written to
  * out_dev when non-null (8-byte aligned, info->total_bytes long).

@@ -275,6 +275,14 @@ class Reference:
                                      C.c_char_p, C.c_uint64, _u64p]
         L.ref_encode_bucket_frame.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                               C.c_void_p, C.c_uint64, _u64p]
+        L.ref_memrelay_create.restype = C.c_void_p
+        L.ref_memrelay_destroy.argtypes = [C.c_void_p]
+        L.ref_memrelay_size.argtypes = [C.c_void_p]
+        L.ref_memrelay_size.restype = C.c_uint64
+        L.ref_memrelay_list.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_uint64]
+        L.ref_memrelay_list.restype = C.c_uint64
+        L.ref_memrelay_get.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint64]
+        L.ref_memrelay_get.restype = C.c_int64
         L.ref_frame_crc32.argtypes = [C.c_void_p, C.c_uint64]
         L.ref_frame_crc32.restype = C.c_uint32
         L.ref_peek_payload_size.argtypes = [C.c_void_p, C.c_uint64]
@@ -408,6 +416,11 @@ class Reference:
                                                 shape, C.byref(nnz), None, None))
         return bool(sp.value), tuple(shape[:nd.value]), nnz.value
 
+    def memory_relay(self):
+        """The reference's MemoryRelay (relay.cpp:7-59) as a ws_relay
+        (ctx, put, get_any) triple of raw pointers, plus helpers."""
+        return RefMemoryRelay(self.lib)
+
     def frame_crc32(self, data: bytes):
         arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
         return int(self.lib.ref_frame_crc32(_ptr(arr), len(data)))
@@ -496,3 +509,38 @@ class RefState:
             c = self.ref.lib.ref_state_codec(self.h, k, d)
             out.append((tuple(d[:7]), chr(c)))
         return out
+
+
+class RefMemoryRelay:
+    """The compiled reference MemoryRelay; `callbacks` are the C function
+    pointers ws_engine_sync_relay calls (no Python on the data path)."""
+
+    def __init__(self, lib):
+        self.lib = lib
+        self.ctx = lib.ref_memrelay_create()
+        self.callbacks = (self.ctx, C.cast(lib.ref_memrelay_put, C.c_void_p).value,
+                          C.cast(lib.ref_memrelay_get_any, C.c_void_p).value)
+
+    def size(self):
+        return int(self.lib.ref_memrelay_size(self.ctx))
+
+    def keys(self, prefix=""):
+        n = self.lib.ref_memrelay_list(self.ctx, prefix.encode(), None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self.lib.ref_memrelay_list(self.ctx, prefix.encode(), buf, n)
+        return [k for k in buf.raw[:n].decode("utf-8", "surrogateescape").split("\n") if k]
+
+    def get(self, key: str) -> bytes:
+        kb = key.encode("utf-8", "surrogateescape")
+        n = self.lib.ref_memrelay_get(self.ctx, kb, len(kb), None, 0)
+        if n < 0:
+            raise KeyError(key)
+        out = np.empty(max(1, n), np.uint8)
+        self.lib.ref_memrelay_get(self.ctx, kb, len(kb), out.ctypes.data, n)
+        return out[:n].tobytes()
+
+    def __del__(self):
+        try:
+            self.lib.ref_memrelay_destroy(self.ctx)
+        except Exception:
+            pass

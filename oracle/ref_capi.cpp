@@ -18,6 +18,7 @@
 #include "coserve/transfer/engine.hpp"
 #include "coserve/transfer/key.hpp"
 #include "coserve/transfer/plan.hpp"
+#include "coserve/transfer/relay.hpp"
 #include "coserve/transfer/wire.hpp"
 
 using namespace coserve;
@@ -270,6 +271,60 @@ int ref_encode_bucket_frame(const char* key, std::uint64_t key_len, const std::u
     return 0;
   } catch (...) {
     return map_exception();
+  }
+}
+
+// relay.cpp:7-59: the reference's MemoryRelay behind the ws_relay callbacks
+// (test harness for ws_engine_sync_relay).
+void* ref_memrelay_create() { return new MemoryRelay(); }
+void ref_memrelay_destroy(void* r) { delete static_cast<MemoryRelay*>(r); }
+std::uint64_t ref_memrelay_size(void* r) { return static_cast<MemoryRelay*>(r)->size(); }
+
+int ref_memrelay_put(void* ctx, const char* key, std::uint64_t klen, const std::uint8_t* data,
+                     std::uint64_t len) {
+  try {
+    static_cast<MemoryRelay*>(ctx)->put(std::string(key, klen),
+                                        std::vector<std::uint8_t>(data, data + len));
+    return 0;
+  } catch (...) {
+    return -2;
+  }
+}
+
+std::int64_t ref_memrelay_get_any(void* ctx, const char* const* keys, const std::uint64_t* lens,
+                                  int n, int timeout_ms, int* hit, std::uint8_t* out,
+                                  std::uint64_t cap) {
+  try {
+    std::vector<std::string> ks;
+    for (int i = 0; i < n; ++i) ks.emplace_back(keys[i], lens[i]);
+    auto kv = static_cast<MemoryRelay*>(ctx)->get_any(ks, timeout_ms);
+    for (int i = 0; i < n; ++i)
+      if (ks[i] == kv.first) *hit = i;
+    if (kv.second.size() <= cap) std::memcpy(out, kv.second.data(), kv.second.size());
+    return static_cast<std::int64_t>(kv.second.size());
+  } catch (const RelayTimeout&) {
+    return -1;
+  } catch (...) {
+    return -2;
+  }
+}
+
+// keys under `prefix`, '\n'-separated; returns the bytes needed
+std::uint64_t ref_memrelay_list(void* ctx, const char* prefix, char* out, std::uint64_t cap) {
+  std::string all;
+  for (const auto& k : static_cast<MemoryRelay*>(ctx)->list(prefix)) all += k + "\n";
+  if (all.size() <= cap) std::memcpy(out, all.data(), all.size());
+  return all.size();
+}
+
+std::int64_t ref_memrelay_get(void* ctx, const char* key, std::uint64_t klen, std::uint8_t* out,
+                              std::uint64_t cap) {
+  try {
+    auto v = static_cast<MemoryRelay*>(ctx)->get(std::string(key, klen), 0);
+    if (v.size() <= cap) std::memcpy(out, v.data(), v.size());
+    return static_cast<std::int64_t>(v.size());
+  } catch (...) {
+    return -1;
   }
 }
 

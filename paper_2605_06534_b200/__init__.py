@@ -3,7 +3,8 @@ transfer engine, arXiv 2605.06534) -- sm_100a kernels behind a C-ABI
 (include/wsync.h) with a Python mirror of the reference's transfer API."""
 from ._lib import (BF16, F32, I32, CapacityError, CudaError, IncompleteCoverage,  # noqa: F401
                    IndexOutOfShard, IndivisibleShape, InvalidArgument, NcclError,
-                   PayloadFormatError, ShapeMismatch, TransferError, UnknownModuleKind)
+                   IntegrityError, KeyFormatError, PayloadFormatError, RelayTimeout, ShapeMismatch,
+                   TransferError, UnknownModuleKind)
 from .codec import (SparseDelta, apply_delta, copy_overlap, diff_shards,  # noqa: F401
                     extract_shard, expert_thresholds, gen_pair_bf16, reslice_delta,
                     shard_shape)

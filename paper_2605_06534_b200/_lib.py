@@ -142,6 +142,28 @@ class PayloadInfo(C.Structure):  # ws_payload_info
                 "total_bytes": self.total_bytes}
 
 
+class Relay(C.Structure):  # ws_relay (function pointers passed as raw addresses)
+    _fields_ = [("ctx", C.c_void_p), ("put", C.c_void_p), ("get_any", C.c_void_p)]
+
+
+class RelayOptions(C.Structure):  # ws_relay_options
+    _fields_ = [("bucket_bytes", C.c_uint64), ("pull_batch_bytes", C.c_uint64),
+                ("push_bytes_per_s", C.c_double), ("pull_bytes_per_s", C.c_double),
+                ("burst_bytes", C.c_double), ("timeout_ms", C.c_int32), ("async_", C.c_int32),
+                ("force_wide_index", C.c_int32), ("staging_buffers", C.c_int32)]
+
+
+class RelayReport(C.Structure):  # ws_relay_report
+    _fields_ = [("wall_s", C.c_double), ("push_s", C.c_double), ("pull_s", C.c_double),
+                ("encode_s", C.c_double), ("apply_s", C.c_double), ("pushed_bytes", C.c_uint64),
+                ("pulled_bytes", C.c_uint64), ("push_buckets", C.c_uint64),
+                ("pull_buckets", C.c_uint64), ("dense_shards", C.c_uint32),
+                ("sparse_shards", C.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _vp, _u64, _i64, _i32 = C.c_void_p, C.c_uint64, C.c_int64, C.c_int32
 _SIGS = {
     "ws_status_name": ([C.c_int], C.c_char_p),
@@ -175,6 +197,8 @@ _SIGS = {
                        C.c_uint32, C.c_char_p, _u64, C.POINTER(_u64)], C.c_int),
     "ws_plan_segment_key_fields": ([_vp, C.c_int, C.POINTER(_i32), C.POINTER(_i32),
                                     C.POINTER(_i32)], C.c_int),
+    "ws_engine_sync_relay": ([_vp, _u64, C.POINTER(SyncOptions), C.POINTER(RelayOptions),
+                              C.POINTER(Relay), C.POINTER(RelayReport)], C.c_int),
     "ws_engine_payload": ([_vp, C.c_int, C.c_int, _vp, C.POINTER(PayloadInfo), _vp], C.c_int),
     "ws_plan_create": ([C.POINTER(Param), C.c_int, C.c_int, C.POINTER(TrainLayout),
                         C.POINTER(ServeLayout), C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),

@@ -20,6 +20,10 @@ struct ws_engine {
                           char* codec);
   ws_status timing(int reset, ws_timing* out);
   ws_status payload(int i, bool wide, void* out_dev, ws_payload_info* info, cudaStream_t s);
+  // cross-cluster sync through a relay (relay.cpp)
+  ws_status sync_relay(uint64_t step, const ws_sync_options& o, const ws_relay_options& ro,
+                       const ws_relay& relay, ws_relay_report* rep);
+  bool encode_only_ = false;  // sync_step: K1 only (no fused apply, no routes)
 
   // caller-owned arenas (ws_engine_bind)
   void* arena[2] = {nullptr, nullptr};

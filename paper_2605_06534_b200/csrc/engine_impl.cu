@@ -303,7 +303,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     a.segs = d_segs_;
     a.tile0 = d_tile0_;
     a.tile_seg = d_tile_seg_;
-    if (fuse_apply_) {
+    if (fuse_apply_ && !encode_only_) {
       a.fuse = d_fuse_;
       a.fuse_on = d_fuse_on_;
       a.serve = serve;
@@ -339,6 +339,13 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
     }
   }
   WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
+  if (encode_only_) {  // relay pusher: the serving side applies what it pulls
+    WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
+    WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
+    WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
+    launch_total_ += launches;
+    return WS_OK;
+  }
   RouteSideArgs r{};
   r.entries = d_local_;
   r.nentries = nlocal_;

@@ -1,0 +1,377 @@
+// relay.cpp -- the engine's cross-cluster sync through a relay (SURVEY.md
+// 8(f) rank 4): TransferEngine::sync_step's pusher and puller
+// (engine.cpp:109-238) with the encode, payloads, decode, reslice and apply on
+// the GPU, and the relay reached through the C callbacks of ws_relay (the
+// binding of the reference's Relay, relay.hpp:27-35).
+//   pusher  K1 (encode only) -> per shard: device payload -> bucket D2H into
+//           pinned staging on a copy stream, bucket k+1 in flight while bucket
+//           k is paced (TokenBucket, relay.cpp:69-84) and put;
+//   puller  per source of every serving shard (plan_pulls): probe the codec
+//           with get_any over the D0/S4/S8 keys (engine.cpp:164-171), fetch
+//           the remaining buckets, stage the payload to the GPU, decode,
+//           reslice and apply (or copy the dense overlap) there.
+//   modes   Async runs both sides concurrently, Batch pushes first
+//           (engine.cpp:231-238).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "capi_util.h"
+#include "engine.h"
+
+using namespace wsync;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+// TokenBucket (relay.cpp:69-84): a byte stream paced at `rate` against the
+// wall clock; callers may overdraw and sleep the debt off.
+class Pacer {
+ public:
+  Pacer(double rate, double burst) : rate_(rate), burst_(burst), tokens_(burst), last_(Clock::now()) {}
+  void acquire(uint64_t bytes) {
+    if (rate_ <= 0.0 || bytes == 0) return;
+    double wait = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      const auto now = Clock::now();
+      tokens_ = std::min(burst_, tokens_ + secs(last_, now) * rate_);
+      last_ = now;
+      tokens_ -= (double)bytes;
+      if (tokens_ < 0) wait = -tokens_ / rate_;
+    }
+    if (wait > 0) std::this_thread::sleep_for(std::chrono::duration<double>(wait));
+  }
+
+ private:
+  double rate_, burst_, tokens_;
+  Clock::time_point last_;
+  std::mutex mu_;
+};
+
+// peek_payload_size (codec.cpp:219-227) on the first bucket, host side.
+bool payload_total(const uint8_t* d, uint64_t n, uint64_t* total) {
+  if (n < 8) return false;
+  uint32_t magic;
+  std::memcpy(&magic, d, 4);
+  const bool sparse = magic == 0x31535743u || magic == 0x32535743u;
+  const bool dense = magic == 0x31445743u || magic == 0x32445743u;
+  if (!sparse && !dense) return false;
+  const uint64_t esz = (magic >> 24) == '2' ? 2 : 4;
+  const int nd = d[5], iw = d[6];
+  uint64_t pos = 8 + 8 * (uint64_t)nd, elems = 1;
+  if (n < pos) return false;
+  for (int k = 0; k < nd; ++k) {
+    int64_t v;
+    std::memcpy(&v, d + 8 + 8 * k, 8);
+    if (v <= 0) return false;
+    elems *= (uint64_t)v;
+  }
+  if (dense) {
+    *total = pos + elems * esz;
+    return true;
+  }
+  if (n < pos + 8) return false;
+  uint64_t nnz;
+  std::memcpy(&nnz, d + pos, 8);
+  *total = pos + 8 + nnz * ((uint64_t)iw + esz);
+  return true;
+}
+
+std::string key_of(uint64_t step, const std::string& param, const ShardDesc& d, char codec,
+                   int iw, uint32_t seq) {
+  char buf[8192];
+  uint64_t n = 0;
+  if (ws_bucket_key(step, param.c_str(), d.tp_rank, d.tp_size, d.pp_stage, d.d, codec, iw, seq,
+                    buf, sizeof(buf), &n) != WS_OK)
+    return std::string();
+  return std::string(buf, n);
+}
+
+struct RelayError {
+  ws_status st;
+  std::string msg;
+};
+
+}  // namespace
+
+ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
+                                const ws_relay_options& ro, const ws_relay& relay,
+                                ws_relay_report* rep) {
+  if (plan_.world() != 1)
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: single-GPU plans only");
+  if (!relay.put || !relay.get_any)
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: relay callbacks missing");
+  if (ro.bucket_bytes == 0) return set_error(WS_INVALID_ARGUMENT, "bucket_bytes must be > 0");
+  if (cudaSetDevice(device_) != cudaSuccess) return set_error(WS_CUDA, "cudaSetDevice");
+  const int esz = dtype_size(dtype_);
+  const int depth = std::max(2, ro.staging_buffers);
+  const int timeout = ro.timeout_ms > 0 ? ro.timeout_ms : 10000;
+  cudaStream_t s_enc = nullptr, s_push = nullptr, s_pull = nullptr;
+  cudaStreamCreateWithFlags(&s_enc, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s_push, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s_pull, cudaStreamNonBlocking);
+  std::vector<void*> host_bufs, dev_bufs;
+  auto cleanup = [&] {
+    for (void* p : host_bufs) cudaFreeHost(p);
+    for (void* p : dev_bufs) cudaFree(p);
+    cudaStreamDestroy(s_enc);
+    cudaStreamDestroy(s_push);
+    cudaStreamDestroy(s_pull);
+  };
+  auto dev_alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(16, bytes)) != cudaSuccess) return nullptr;
+    dev_bufs.push_back(p);
+    return p;
+  };
+  auto host_alloc = [&](size_t bytes) -> uint8_t* {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, std::max<size_t>(16, bytes)) != cudaSuccess) return nullptr;
+    host_bufs.push_back(p);
+    return static_cast<uint8_t*>(p);
+  };
+
+  std::memset(rep, 0, sizeof(*rep));
+  const auto wall0 = Clock::now();
+
+  // ---- encode (K1 only: no fused apply, no routes) ------------------------
+  encode_only_ = true;
+  ws_status st = sync_step(o, s_enc, nullptr, nullptr, nullptr);
+  encode_only_ = false;
+  if (st != WS_OK) {
+    cleanup();
+    return st;
+  }
+  if (cudaStreamSynchronize(s_enc) != cudaSuccess) {
+    cleanup();
+    return set_error(WS_CUDA, "sync_relay: encode");
+  }
+  rep->encode_s = secs(wall0, Clock::now());
+
+  // sizes: the largest payload (dense bound) and record count of a segment
+  const auto& segs = plan_.segments();
+  uint64_t max_payload = 64, max_n = 1, max_cap = 1;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    const int nd = (int)plan_.manifest()[segs[i].shard.param].shape.size();
+    max_payload = std::max<uint64_t>(
+        max_payload, std::max(ws_payload_bytes((ws_dtype)dtype_, nd, 'D', 0, segs[i].n),
+                              ws_payload_bytes((ws_dtype)dtype_, nd, 'S', 8, segs_[i].cap)));
+    max_n = std::max<uint64_t>(max_n, segs[i].n);
+    max_cap = std::max<uint64_t>(max_cap, segs_[i].cap);
+  }
+  const uint64_t B = ro.bucket_bytes;
+
+  Pacer push_pacer(ro.push_bytes_per_s, ro.burst_bytes > 0 ? ro.burst_bytes : (double)B);
+  Pacer pull_pacer(ro.pull_bytes_per_s, ro.burst_bytes > 0 ? ro.burst_bytes : (double)B);
+  std::mutex err_mu;
+  RelayError first_err{WS_OK, ""};
+  auto fail = [&](ws_status e, const std::string& m) {
+    std::lock_guard<std::mutex> lk(err_mu);
+    if (first_err.st == WS_OK) first_err = RelayError{e, m};
+  };
+  std::atomic<uint64_t> pushed{0}, pulled{0}, pbk{0}, lbk{0};
+  std::atomic<uint32_t> dense_n{0}, sparse_n{0};
+  double push_s = 0, pull_s = 0, apply_s = 0;
+
+  // ---- pusher --------------------------------------------------------------
+  void* d_payload = dev_alloc(max_payload);
+  std::vector<uint8_t*> stage(depth);
+  for (auto& p : stage) p = host_alloc(std::min<uint64_t>(B, max_payload));
+  std::vector<cudaEvent_t> ev(depth);
+  for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  auto pusher = [&] {
+    const auto t0 = Clock::now();
+    for (size_t i = 0; i < segs.size() && first_err.st == WS_OK; ++i) {
+      ws_payload_info info;
+      ws_status e = payload((int)i, ro.force_wide_index != 0, d_payload, &info, s_push);
+      if (e != WS_OK) {
+        fail(e, "sync_relay: payload");
+        return;
+      }
+      (info.codec == 'S' ? sparse_n : dense_n)++;
+      const std::string& name = plan_.manifest()[segs[i].shard.param].name;
+      const uint64_t total = info.total_bytes;
+      const uint64_t nb = total ? (total + B - 1) / B : 1;  // engine.cpp:139
+      auto issue = [&](uint64_t k) {
+        const uint64_t n = std::min(B, total - std::min(total, k * B));
+        cudaMemcpyAsync(stage[k % depth], static_cast<char*>(d_payload) + k * B, n,
+                        cudaMemcpyDeviceToHost, s_push);
+        cudaEventRecord(ev[k % depth], s_push);
+      };
+      for (uint64_t k = 0; k < std::min<uint64_t>(nb, depth - 1); ++k) issue(k);
+      for (uint64_t k = 0; k < nb; ++k) {
+        if (k + depth - 1 < nb) issue(k + depth - 1);  // overlaps this bucket's put
+        cudaEventSynchronize(ev[k % depth]);
+        const uint64_t n = std::min(B, total - std::min(total, k * B));
+        push_pacer.acquire(n);
+        const std::string key = key_of(step, name, segs[i].shard, info.codec, info.index_width,
+                                       (uint32_t)k);
+        if (relay.put(relay.ctx, key.data(), key.size(), stage[k % depth], n) != 0) {
+          fail(WS_TRANSFER_ERROR, "relay put failed for '" + key + "'");
+          return;
+        }
+        pushed += n;
+        ++pbk;
+      }
+    }
+    push_s = secs(t0, Clock::now());
+  };
+
+  // ---- puller --------------------------------------------------------------
+  uint8_t* h_payload = host_alloc(max_payload);
+  void* d_in = dev_alloc(max_payload);
+  uint32_t* d_idx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
+  void* d_val = dev_alloc(max_cap * 4);
+  uint32_t* d_ridx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
+  void* d_rval = dev_alloc(max_cap * 4);
+  uint64_t* d_rnnz = static_cast<uint64_t*>(dev_alloc(8));
+  uint32_t* d_err = static_cast<uint32_t*>(dev_alloc(4));
+  const size_t ws_bytes = ws_diff_workspace_bytes(max_cap);
+  void* d_ws = dev_alloc(ws_bytes);
+  auto puller = [&] {
+    const auto t0 = Clock::now();
+    double apply_acc = 0;
+    for (const Route& r : plan_.routes()) {
+      if (first_err.st != WS_OK) return;
+      const Segment& src = segs[r.seg];
+      const ParamMeta& p = plan_.manifest()[src.shard.param];
+      std::string cand[3] = {key_of(step, p.name, src.shard, 'D', 0, 0),
+                             key_of(step, p.name, src.shard, 'S', 4, 0),
+                             key_of(step, p.name, src.shard, 'S', 8, 0)};
+      const char* kp[3] = {cand[0].data(), cand[1].data(), cand[2].data()};
+      const uint64_t kl[3] = {cand[0].size(), cand[1].size(), cand[2].size()};
+      int hit = -1;
+      int64_t n0 = relay.get_any(relay.ctx, kp, kl, 3, timeout, &hit, h_payload, max_payload);
+      if (n0 < 0 || hit < 0) {
+        fail(n0 == -1 ? WS_RELAY_TIMEOUT : WS_TRANSFER_ERROR,
+             "relay get_any for '" + cand[1] + "' failed");
+        return;
+      }
+      pull_pacer.acquire((uint64_t)n0);
+      uint64_t total = 0;
+      if (!payload_total(h_payload, (uint64_t)n0, &total) || total > max_payload) {
+        fail(WS_PAYLOAD_FORMAT, "bad first bucket for '" + cand[hit] + "'");
+        return;
+      }
+      if ((uint64_t)n0 != std::min(total, B)) {
+        fail(WS_PAYLOAD_FORMAT, "bucket 0 of '" + cand[hit] + "' has a wrong size");
+        return;
+      }
+      const char codec = hit == 0 ? 'D' : 'S';
+      const int iw = hit == 0 ? 0 : (hit == 1 ? 4 : 8);
+      const uint64_t nb = total ? (total + B - 1) / B : 1;
+      uint64_t have = (uint64_t)n0;
+      pulled += have;
+      ++lbk;
+      for (uint64_t k = 1; k < nb; ++k) {
+        const std::string kk = key_of(step, p.name, src.shard, codec, iw, (uint32_t)k);
+        const char* kkp = kk.data();
+        const uint64_t kkl = kk.size();
+        int h = -1;
+        const int64_t nk = relay.get_any(relay.ctx, &kkp, &kkl, 1, timeout, &h, h_payload + have,
+                                         max_payload - have);
+        if (nk < 0 || have + (uint64_t)nk > total) {
+          fail(nk == -1 ? WS_RELAY_TIMEOUT : WS_PAYLOAD_FORMAT, "relay get for '" + kk + "' failed");
+          return;
+        }
+        pull_pacer.acquire((uint64_t)nk);
+        have += (uint64_t)nk;
+        pulled += (uint64_t)nk;
+        ++lbk;
+      }
+      if (have != total) {
+        fail(WS_PAYLOAD_FORMAT, "reassembled payload has the wrong size");
+        return;
+      }
+      const auto ta = Clock::now();
+      cudaMemcpyAsync(d_in, h_payload, total, cudaMemcpyHostToDevice, s_pull);
+      cudaStreamSynchronize(s_pull);
+      ws_payload_info info;
+      ws_status e = ws_peek_payload_dev(d_in, total, &info);
+      if (e != WS_OK) {
+        fail(e, std::string(ws_last_error()));
+        return;
+      }
+      const int nd = (int)p.shape.size();
+      const ws_stream_t ps = reinterpret_cast<ws_stream_t>(s_pull);
+      char* tgt = static_cast<char*>(serve) + r.dst_offset * esz;
+      if (info.codec == 'S') {
+        e = ws_decode_sparse_dev(d_in, &info, d_idx, d_val, ps);
+        if (e == WS_OK)
+          e = ws_reslice_delta((ws_dtype)dtype_, p.shape.data(), nd, src.shard.d, r.dst.d, 1,
+                               d_idx, d_val, info.nnz, nullptr, d_ridx, d_rval, d_rnnz, d_err,
+                               d_ws, ws_bytes, ps);
+        uint64_t dn = 1;
+        for (int dd = 0; dd < nd; ++dd)
+          dn *= (uint64_t)(r.dst.d.slice_dim == dd ? r.dst.d.end - r.dst.d.start : p.shape[dd]);
+        if (e == WS_OK)
+          e = ws_apply_delta((ws_dtype)dtype_, tgt, dn, d_ridx, d_rval, 0, d_rnnz, d_err, ps);
+        uint32_t herr = 0;
+        cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s_pull);
+        cudaStreamSynchronize(s_pull);
+        if (e == WS_OK && herr) e = set_error(WS_INDEX_OUT_OF_SHARD, "sync_relay: apply");
+      } else {
+        int64_t copied = 0;
+        e = ws_copy_overlap((ws_dtype)dtype_, p.shape.data(), nd, r.dst.d, tgt, src.shard.d,
+                            static_cast<char*>(d_in) + info.header_bytes, &copied, ps);
+        cudaStreamSynchronize(s_pull);
+      }
+      if (e != WS_OK) {
+        fail(e, std::string(ws_last_error()));
+        return;
+      }
+      apply_acc += secs(ta, Clock::now());
+    }
+    pull_s = secs(t0, Clock::now());
+    apply_s = apply_acc;
+  };
+
+  const auto t_net = Clock::now();
+  if (ro.async) {
+    std::thread pt(pusher);
+    puller();
+    pt.join();
+  } else {
+    pusher();
+    if (first_err.st == WS_OK) puller();
+  }
+  (void)t_net;
+  for (auto& e : ev) cudaEventDestroy(e);
+  cleanup();
+  rep->wall_s = secs(wall0, Clock::now());
+  rep->push_s = push_s;
+  rep->pull_s = pull_s;
+  rep->apply_s = apply_s;
+  rep->pushed_bytes = pushed;
+  rep->pulled_bytes = pulled;
+  rep->push_buckets = pbk;
+  rep->pull_buckets = lbk;
+  rep->dense_shards = dense_n;
+  rep->sparse_shards = sparse_n;
+  if (first_err.st != WS_OK) return set_error(first_err.st, first_err.msg);
+  return WS_OK;
+}
+
+extern "C" ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step,
+                                          const ws_sync_options* opts,
+                                          const ws_relay_options* relay_opts,
+                                          const ws_relay* relay, ws_relay_report* report) {
+  if (!eng || !opts || !relay_opts || !relay || !report)
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: null argument");
+  try {
+    return eng->sync_relay(step, *opts, *relay_opts, *relay, report);
+  } catch (const std::exception& e) {
+    return set_error(WS_TRANSFER_ERROR, e.what());
+  }
+}

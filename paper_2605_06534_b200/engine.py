@@ -200,6 +200,26 @@ class TransferEngine:
                                         C.byref(info), _stream()))
         return out[:info.total_bytes], info.as_dict()
 
+    def sync_relay(self, relay, step=1, sparse=True, density_threshold=0.20, reverse=False,
+                   bucket_bytes=64 << 20, mode="async", push_bytes_per_s=0.0,
+                   pull_bytes_per_s=0.0, burst_bytes=0.0, timeout_ms=10000,
+                   force_wide_index=False, staging_buffers=2):
+        """TransferEngine::sync_step across clusters (engine.cpp:66-254): this
+        GPU pushes its trainer shards through `relay` -- a (ctx, put, get_any)
+        triple of C pointers implementing ws_relay -- and pulls them into its
+        serving shards; mode "async" or "batch" (SyncMode)."""
+        o = _lib.SyncOptions(int(sparse), density_threshold, int(reverse))
+        ro = _lib.RelayOptions(bucket_bytes, 256 << 20, push_bytes_per_s, pull_bytes_per_s,
+                               burst_bytes, timeout_ms, int(mode == "async"),
+                               int(force_wide_index), staging_buffers)
+        rl = _lib.Relay(*relay)
+        rep = _lib.RelayReport()
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            check(lib.ws_engine_sync_relay(self.h, step, C.byref(o), C.byref(ro), C.byref(rl),
+                                           C.byref(rep)))
+        return rep.as_dict()
+
     def segment_frames(self, i, step, bucket_bytes=None, force_wide_index=False):
         """The relay frames of segment i for `step` (engine.cpp:136-148 +
         wire.cpp:35-47): (uint8 device tensor, keys, frame offsets)."""
