@@ -18,7 +18,7 @@ namespace wsync {
 #define WS_ENC_CONSUMERS 512
 #endif
 #ifndef WS_ENC_BUFFERS
-#define WS_ENC_BUFFERS 3
+#define WS_ENC_BUFFERS 2
 #endif
 #ifndef WS_ENC_CAPDIV
 #define WS_ENC_CAPDIV 16  // staged records per super-tile buffer: 3/CAPDIV of its elements

@@ -95,7 +95,7 @@ struct StageMeta {
 };
 
 #ifndef WS_ENC_SLOTS
-#define WS_ENC_SLOTS 4
+#define WS_ENC_SLOTS 6
 #endif
 #ifndef WS_ENC_PREFETCH
 #define WS_ENC_PREFETCH 1
@@ -575,10 +575,10 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   }
   // Super-tile i is staged in buffer i % NB and written out after super-tile
   // i + NB - 1 is staged, so its placement has NB - 1 periods to complete.
-  static_assert(NB == 3, "two pending super-tiles are kept in registers");
+  static_assert(NB == 2 || NB == 3, "one or two pending super-tiles are kept in registers");
   auto flush_tile = [&](int pb, const PendingSlice& p, uint32_t& rbits, bool drain) {
     if (C::PRE) {  // this super-tile's serving words are in (the two later groups may not be)
-      if (drain) cp_async_wait<0>(); else cp_async_wait<2>();
+      if (drain) cp_async_wait<0>(); else cp_async_wait<NB - 1>();
       __syncwarp();
     }
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
@@ -690,12 +690,18 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (tid == 0) tinfo[b] = ti;  // for the resolver only
     __syncwarp();
     named_arrive(kStagedBar + b, kEncConsumers + 32);
-    if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, false);  // super-tile i-2
-    pend0 = pend1;
-    pend1 = PendingSlice{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, ti.s, mine};
+    const PendingSlice cur{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, ti.s, mine};
+    if constexpr (NB == 3) {
+      if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, false);  // super-tile i-2
+      pend0 = pend1;
+      pend1 = cur;
+    } else {
+      if (i >= 1) flush_tile((int)((i - 1) % NB), pend1, rbits, false);  // super-tile i-1
+      pend1 = cur;
+    }
   }
   // ---- drain: write out the pending super-tiles, then stop the resolvers
-  if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, true);
+  if (NB == 3 && i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, true);
   if (i >= 1) flush_tile((int)((i - 1) % NB), pend1, rbits, true);
   named_barrier(1, kEncConsumers);  // every warp is past its last use of tinfo
   if (tid == 0)
