@@ -120,6 +120,22 @@ def main():
             bad, rep = bf16_case(rank, world, uid, manifest, density, 3)
             results[f"bf16 {name} d={density}"] = bad or "ok"
             ok &= not bad
+    # many alternating syncs (the bench's pattern), P2P epochs/acks wrapping
+    # through several steps: an even count must leave serving == prev
+    manifest = ws.MODELS["qwen2.5-0.5b"]([0, 23])
+    tp = 1 if world == 1 else 2
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+                   world=world, rank=rank)
+    eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid())
+    eng.generate(seed=8, density=0.02)
+    for k in range(10):
+        eng.sync_step(reverse=bool(k % 2), report=False, sparse=(k % 3 != 2))
+    torch.cuda.synchronize()
+    bad = serve_equals_gen(eng, plan, 8, 0.02, "prev")
+    results["10 alternating syncs"] = bad or "ok"
+    ok &= not bad
+    del eng
+
     # BASELINE config 3 (Qwen3-32B TP8 -> TP4 x 2, 0.5%) and config 4
     # (Qwen3-30B-A3B expert-sharded, Zipf(1.1) per-expert densities around
     # 1%), on layer subsets, scaled to this world size
