@@ -41,6 +41,7 @@ struct ws_engine {
   ws_status size_recv(uint64_t records);
   void destroy_comm();
   ws_status exchange_begin(cudaStream_t s, uint32_t* launches);  // P2P "reached step" flags
+  ws_status exchange_status() const;                             // faults seen by the kernels
   // P2P + bf16 + direct dense: K1 stores the remote records itself (fills a.remote)
   ws_status exchange_fuse_k1(wsync::EncodeArgs& a, cudaStream_t s);
   ws_status exchange(const ws_sync_options& o, int next_arena, cudaStream_t s, uint32_t* launches);

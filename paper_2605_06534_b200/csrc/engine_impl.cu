@@ -380,6 +380,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   launch_total_ += launches;
   if (!nnz_host && !report) return WS_OK;
   WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  if ((st = exchange_status()) != WS_OK) return st;
   std::memcpy(h_nnz_.data(), h_nnz_pinned_, nseg_ * 8);
   if (nnz_host) std::memcpy(nnz_host, h_nnz_.data(), nseg_ * 8);
   if (report) {
@@ -494,6 +495,8 @@ ws_status ws_engine::timing(int reset, ws_timing* out) {
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
   if (last_stream_) WS_CUDA_TRY(cudaStreamSynchronize(last_stream_), "sync");
   WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  ws_status st = exchange_status();  // timed syncs must not hide an exchange fault
+  if (st != WS_OK) return st;
   ws_timing t{};
   t.steps = ring_steps_;
   t.kernel_launches = launch_total_;

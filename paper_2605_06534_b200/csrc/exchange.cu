@@ -56,6 +56,7 @@ struct ws_engine::Comm {
   uint64_t* d_allcnt = nullptr;                  // [world][coords]
   uint64_t* h_allcnt = nullptr;                  // pinned copy
   uint32_t* d_err = nullptr;
+  uint32_t* h_err = nullptr;                     // pinned copy, refreshed every sync
   void* d_send = nullptr;
   void* d_recv = nullptr;
   uint64_t send_cap = 0, recv_cap = 0;           // records
@@ -95,6 +96,7 @@ struct ws_engine::Comm {
     cudaFree(d_region_cnt);
     cudaFree(d_allcnt);
     cudaFree(d_err);
+    if (h_err) cudaFreeHost(h_err);
     cudaFree(d_send);
     cudaFree(d_recv);
     if (h_allcnt) cudaFreeHost(h_allcnt);
@@ -178,6 +180,9 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
   WS_CUDA_TRY(cudaMalloc(&c->d_region_cnt, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_allcnt, (size_t)c->world * c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_err, 4), "cudaMalloc");
+  WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "cudaMemset");
+  WS_CUDA_TRY(cudaMallocHost(&c->h_err, 4), "cudaMallocHost");
+  *c->h_err = 0;
   WS_CUDA_TRY(cudaMallocHost(&c->h_allcnt, (size_t)c->world * c->coords * 8), "cudaMallocHost");
   const char* mode = getenv("WSYNC_EXCHANGE");
   const bool want_p2p = !(mode && std::string(mode) == "nccl") && c->world <= kMaxWorld &&
@@ -616,6 +621,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
       *launches += 2;
     }
     pulled_bytes_ = 0;  // filled by exchange_report() when a report is asked for
+    WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
     return WS_OK;
   }
   // 1. pack
@@ -707,6 +713,19 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   if (recv_total) *launches += 1;
   pulled_bytes_ = recv_total * wb;
   pushed_wire_bytes_ = sent;
+  WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
+  return WS_OK;
+}
+
+// Device-side exchange faults of the syncs so far (sticky in P2P mode), read
+// after a synchronising call.
+ws_status ws_engine::exchange_status() const {
+  const Comm* c = comm_;
+  if (!c || !c->h_err) return WS_OK;
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(c->h_err);
+  if (e & kErrBitTimeout)
+    return set_error(WS_RELAY_TIMEOUT, "exchange: a peer did not reach, send or ack a step in time");
+  if (e & WS_ERRBIT_CAPACITY) return set_error(WS_CAPACITY, "exchange: region capacity exceeded");
   return WS_OK;
 }
 
