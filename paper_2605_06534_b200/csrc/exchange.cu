@@ -678,6 +678,8 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
     if (st != WS_OK) return st;
     pa.send = c->d_send;
     WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
+    // the first pack's overflow was the signal to grow, not a fault
+    WS_CUDA_TRY(cudaMemsetAsync(c->d_err, 0, 4, s), "memset");
     WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (grown)");
     *launches += 2;
   }
