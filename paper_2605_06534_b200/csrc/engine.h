@@ -42,6 +42,19 @@ struct ws_engine {
   void destroy_comm();
   ws_status exchange_begin(cudaStream_t s, uint32_t* launches);  // P2P "reached step" flags
   ws_status exchange_status() const;                             // faults seen by the kernels
+  int exchange_rounds() const;
+  // R > 1 (P2P): K1 round by round on a high-priority stream, round r's
+  // exchange on a low-priority stream overlapping the encode of round r + 1
+  ws_status sync_rounds(const ws_sync_options& o, int pa, int na, cudaStream_t s,
+                        uint32_t* launches, cudaEvent_t* ev);
+  wsync::EncodeArgs encode_args(int pa, int na);
+  ws_status launch_fixup(const wsync::EncodeArgs& a, int seg_begin, int seg_end, cudaStream_t s,
+                         uint32_t* launches);
+  ws_status local_route(const ws_sync_options& o, int pa, int na, cudaStream_t s,
+                        uint32_t* launches);
+  bool overlap_ = true;  // WSYNC_OVERLAP=0 runs the rounds back to back
+  ws_status exchange_round(const ws_sync_options& o, int next_arena, int round, cudaStream_t s,
+                           uint32_t* launches);
   // P2P + bf16 + direct dense: K1 stores the remote records itself (fills a.remote)
   ws_status exchange_fuse_k1(wsync::EncodeArgs& a, cudaStream_t s);
   ws_status exchange(const ws_sync_options& o, int next_arena, cudaStream_t s, uint32_t* launches);

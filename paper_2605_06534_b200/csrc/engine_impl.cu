@@ -261,6 +261,81 @@ ws_status ws_engine::generate(uint64_t seed, double density, cudaStream_t s, dou
   return st;
 }
 
+EncodeArgs ws_engine::encode_args(int pa, int na) {
+  EncodeArgs a{};
+  a.unordered = 1;
+  a.spill = d_spill_;
+  a.spill_blocks = spill_blocks_;
+  a.tile_cnt = d_tile_cnt_;
+  a.tile_base = d_tile_base_;
+  a.prev = arena[pa];
+  a.next = arena[na];
+  a.segs = d_segs_;
+  a.tile0 = d_tile0_;
+  a.tile_seg = d_tile_seg_;
+  if (fuse_apply_ && !encode_only_) {
+    a.fuse = d_fuse_;
+    a.fuse_on = d_fuse_on_;
+    a.serve = serve;
+  }
+  a.nseg = nseg_;
+  a.ntiles = ntiles_;
+  a.out_idx = d_idx_;
+  a.out_val = d_val_;
+  a.seg_nnz = d_nnz_;
+  a.status = d_status_;
+  a.epoch = next_epoch();
+  a.ticket = d_ticket_;
+  if (count_only_) a.seg_mode = d_seg_mode_;
+  return a;
+}
+
+// Super-tiles of predicted-dense segments in [seg_begin, seg_end) that came
+// out sparse, then K1 over just those (an empty list costs two near-empty
+// launches).
+ws_status ws_engine::launch_fixup(const EncodeArgs& a, int seg_begin, int seg_end, cudaStream_t s,
+                                  uint32_t* launches) {
+  WS_CUDA_TRY(launch_fixup_plan(d_tile0_, seg_begin, seg_end, d_nnz_, d_cap_, d_seg_mode_,
+                                d_fix_list_, d_fix_n_, s),
+              "fixup plan");
+  EncodeArgs f = a;
+  f.seg_mode = nullptr;
+  f.tile_list = d_fix_list_;
+  f.ntiles_dev = d_fix_n_;
+  f.tile_offset = 0;
+  f.ntiles = ntiles_;
+  f.fill = d_fill_;
+  WS_CUDA_TRY(launch_encode(dtype_, f, s), "encode fixup");
+  *launches += 2;
+  return WS_OK;
+}
+
+ws_status ws_engine::local_route(const ws_sync_options& o, int pa, int na, cudaStream_t s,
+                                 uint32_t* launches) {
+  RouteSideArgs r{};
+  r.entries = d_local_;
+  r.nentries = nlocal_;
+  r.sparse = o.sparse ? 1 : 0;
+  r.seg_nnz = d_nnz_;
+  r.seg_cap = d_cap_;
+  r.seg_rec = d_rec_;
+  r.seg_base = d_base_;
+  r.rec_idx = d_idx_;
+  r.rec_val = d_val_;
+  fill_tiles(r);
+  r.segs = d_segs_;
+  r.stream_apply = 1;
+  r.train_prev = arena[pa];
+  r.train_next = arena[na];
+  r.serve = serve;
+  r.unit_off = d_unit_off_;
+  r.fused = (fuse_apply_ && o.sparse && ntiles_) ? 1 : 0;
+  r.fuse_on = d_fuse_on_;
+  WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
+  if (nlocal_) *launches += 2;
+  return WS_OK;
+}
+
 ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
                                uint64_t* nnz_host, ws_report* report) {
   if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "sync: unbound");
@@ -288,89 +363,43 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   WS_CUDA_TRY(cudaEventRecord(ev_[1], s), "event");
   last_sparse_ = o.sparse != 0;
   last_next_arena_ = na;
-  if (o.sparse && ntiles_) {
-    // K1 reserves each super-tile's records with an atomic on its segment's count
-    WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
-    if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
-    EncodeArgs a{};
-    a.unordered = 1;
-    a.spill = d_spill_;
-    a.spill_blocks = spill_blocks_;
-    a.tile_cnt = d_tile_cnt_;
-    a.tile_base = d_tile_base_;
-    a.prev = arena[pa];
-    a.next = arena[na];
-    a.segs = d_segs_;
-    a.tile0 = d_tile0_;
-    a.tile_seg = d_tile_seg_;
-    if (fuse_apply_ && !encode_only_) {
-      a.fuse = d_fuse_;
-      a.fuse_on = d_fuse_on_;
-      a.serve = serve;
+  const bool rounds = plan_.world() > 1 && o.sparse && ntiles_ && !encode_only_ &&
+                      exchange_rounds() > 1;
+  if (rounds) {
+    st = sync_rounds(o, pa, na, s, &launches, ev_);
+    if (st != WS_OK) return st;
+  } else {
+    if (o.sparse && ntiles_) {
+      // K1 reserves each super-tile's records with an atomic on its segment's count
+      WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
+      if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
+      EncodeArgs a = encode_args(pa, na);
+      if (plan_.world() > 1) {
+        st = exchange_fuse_k1(a, s);
+        if (st != WS_OK) return st;
+      }
+      WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
+      ++launches;
+      if (count_only_) {
+        st = launch_fixup(a, 0, nseg_, s, &launches);
+        if (st != WS_OK) return st;
+      }
     }
-    a.nseg = nseg_;
-    a.ntiles = ntiles_;
-    a.out_idx = d_idx_;
-    a.out_val = d_val_;
-    a.seg_nnz = d_nnz_;
-    a.status = d_status_;
-    a.epoch = next_epoch();
-    a.ticket = d_ticket_;
-    if (count_only_) a.seg_mode = d_seg_mode_;
+    WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
+    if (encode_only_) {  // relay pusher: the serving side applies what it pulls
+      WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
+      WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
+      WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
+      launch_total_ += launches;
+      return WS_OK;
+    }
+    st = local_route(o, pa, na, s, &launches);
+    if (st != WS_OK) return st;
+    WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
     if (plan_.world() > 1) {
-      st = exchange_fuse_k1(a, s);
+      st = exchange(o, na, s, &launches);
       if (st != WS_OK) return st;
     }
-    WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
-    ++launches;
-    if (count_only_) {
-      // super-tiles of predicted-dense segments that came out sparse, then K1
-      // over just those (an empty list costs two near-empty launches)
-      WS_CUDA_TRY(launch_fixup_plan(d_tile0_, nseg_, d_nnz_, d_cap_, d_seg_mode_, d_fix_list_,
-                                    d_fix_n_, s),
-                  "fixup plan");
-      EncodeArgs f = a;
-      f.seg_mode = nullptr;
-      f.tile_list = d_fix_list_;
-      f.ntiles_dev = d_fix_n_;
-      f.fill = d_fill_;
-      WS_CUDA_TRY(launch_encode(dtype_, f, s), "encode fixup");
-      launches += 2;
-    }
-  }
-  WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
-  if (encode_only_) {  // relay pusher: the serving side applies what it pulls
-    WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
-    WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
-    WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
-    launch_total_ += launches;
-    return WS_OK;
-  }
-  RouteSideArgs r{};
-  r.entries = d_local_;
-  r.nentries = nlocal_;
-  r.sparse = o.sparse ? 1 : 0;
-  r.seg_nnz = d_nnz_;
-  r.seg_cap = d_cap_;
-  r.seg_rec = d_rec_;
-  r.seg_base = d_base_;
-  r.rec_idx = d_idx_;
-  r.rec_val = d_val_;
-  fill_tiles(r);
-  r.segs = d_segs_;
-  r.stream_apply = 1;
-  r.train_prev = arena[pa];
-  r.train_next = arena[na];
-  r.serve = serve;
-  r.unit_off = d_unit_off_;
-  r.fused = (fuse_apply_ && o.sparse && ntiles_) ? 1 : 0;
-  r.fuse_on = d_fuse_on_;
-  WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
-  if (nlocal_) launches += 2;
-  WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
-  if (plan_.world() > 1) {
-    st = exchange(o, na, s, &launches);
-    if (st != WS_OK) return st;
   }
   WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
   if ((nnz_host || report) && nseg_)

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -76,6 +77,24 @@ struct ws_engine::Comm {
   RecvEntry* d_rentries = nullptr;
   uint64_t* d_recv_units = nullptr;
   int nsend_entries = 0;
+  // exchange rounds (P2P): K1 encodes segment runs round by round and round
+  // r's pack/apply overlap the encode of round r + 1
+  int R = 1;
+  uint64_t step = 0;                             // syncs so far (epochs derive from it)
+  std::vector<int> ent_first;                    // R + 1: my remote entries per round
+  std::vector<int> seg_first;                    // R + 1: my segments per round
+  std::vector<uint32_t> tile_first;              // R + 1: my super-tiles per round
+  struct RoundRecv {
+    RecvEntry* d_rentries = nullptr;
+    uint64_t* d_units = nullptr;
+    int n = 0;
+    uint32_t mask = 0;                           // sources with entries in this round
+    int32_t dest_rank[kMaxWorld][kMaxReplicas];  // where my round-r entries go
+  };
+  std::vector<RoundRecv> rr;
+  cudaStream_t s_enc = nullptr, s_xchg = nullptr;  // high / low priority (R > 1)
+  std::vector<cudaEvent_t> ev_round;               // K1 round r done
+  cudaEvent_t ev_start = nullptr, ev_xdone = nullptr, ev_encdone = nullptr;
 
   ~Comm() {
     for (void* p : peer)
@@ -89,6 +108,16 @@ struct ws_engine::Comm {
     cudaFree(d_ent_cnt);
     cudaFree(d_rentries);
     cudaFree(d_recv_units);
+    for (auto& x : rr) {
+      cudaFree(x.d_rentries);
+      cudaFree(x.d_units);
+    }
+    for (auto& e : ev_round) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_xdone) cudaEventDestroy(ev_xdone);
+    if (ev_encdone) cudaEventDestroy(ev_encdone);
+    if (s_enc) cudaStreamDestroy(s_enc);
+    if (s_xchg) cudaStreamDestroy(s_xchg);
     cudaFree(d_entries);
     cudaFree(d_unit_off);
     cudaFree(d_region_off);
@@ -126,6 +155,59 @@ void exchange_caps(const Plan& plan, int me, std::vector<uint64_t>* send_cap,
 
 }  // namespace wsync
 
+namespace {
+// Remote routes of rank g (their coordinate has a replica other than g),
+// ordered by segment: the order of g's remote entries on every rank.
+std::vector<int> remote_routes(const Plan& plan, int g) {
+  std::vector<int> out;
+  const auto& rs = plan.routes_of(g);
+  for (int i = 0; i < (int)rs.size(); ++i)
+    if (plan.replicas() > 1 || rs[i].coord != plan.coord_of_rank(g)) out.push_back(i);
+  std::stable_sort(out.begin(), out.end(), [&](int x, int y) { return rs[x].seg < rs[y].seg; });
+  return out;
+}
+// Exchange round of each of rank g's segments: R contiguous runs of segments
+// with about equal super-tile counts (K1 encodes them round by round).
+std::vector<int> segment_rounds(const Plan& plan, int g, int R, uint32_t tile) {
+  const auto& segs = plan.segments_of(g);
+  uint64_t total = 0, acc = 0;
+  for (const Segment& sg : segs) total += (sg.n + tile - 1) / tile;
+  std::vector<int> out(segs.size(), 0);
+  for (size_t i = 0; i < segs.size(); ++i) {
+    out[i] = (int)std::min<uint64_t>(R - 1, acc * R / std::max<uint64_t>(1, total));
+    acc += (segs[i].n + tile - 1) / tile;
+  }
+  return out;
+}
+struct RecvLayout {
+  std::vector<std::pair<int, int>> entries;  // (source rank, its remote-entry index)
+  std::vector<uint64_t> off, cap;            // records
+  std::vector<int> round;
+  uint64_t records = 0;
+  size_t head = 0;                           // mailbox + count slots, bytes
+};
+RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
+  RecvLayout L;
+  const int k = plan.coord_of_rank(q);
+  for (int g = 0; g < plan.world(); ++g) {
+    if (g == q) continue;
+    const std::vector<int> rr = remote_routes(plan, g);
+    const std::vector<int> sr = segment_rounds(plan, g, R, tile);
+    for (int e = 0; e < (int)rr.size(); ++e) {
+      const Route& r = plan.routes_of(g)[rr[e]];
+      if (r.coord != k) continue;
+      L.entries.emplace_back(g, e);
+      L.off.push_back(L.records);
+      L.cap.push_back(r.overlap);
+      L.round.push_back(sr[r.seg]);
+      L.records += r.overlap;
+    }
+  }
+  L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
+  return L;
+}
+}  // namespace
+
 ws_status ws_engine::init_comm(const uint8_t* unique_id) {
   if (plan_.world() == 1) return WS_OK;
   if (!unique_id) return set_error(WS_INVALID_ARGUMENT, "multi-GPU engine needs an NCCL unique id");
@@ -140,10 +222,11 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
 
   // remote routes: every route whose coordinate has a replica other than me
   const int me = plan_.rank(), my_coord = plan_.my_coord();
+  (void)my_coord;
   std::vector<LocalEntry> remote;
   const auto& segs = plan_.segments();
-  for (const Route& r : plan_.routes()) {
-    if (plan_.replicas() == 1 && r.coord == my_coord) continue;
+  for (int ri : remote_routes(plan_, me)) {
+    const Route& r = plan_.routes()[ri];
     const ParamMeta& p = plan_.manifest()[r.dst.param];
     LocalEntry e = make_local_entry(dtype_, p.shape.data(), (int)p.shape.size(), r.seg,
                                     segs[r.seg].shard.d, r.dst.d, r.dst_offset);
@@ -157,7 +240,7 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
     WS_CUDA_TRY(cudaMemcpy(c->d_entries, remote.data(), remote.size() * sizeof(LocalEntry),
                            cudaMemcpyHostToDevice),
                 "H2D");
-  WS_CUDA_TRY(cudaMalloc(&c->d_unit_off, (remote.size() + 1) * 8), "cudaMalloc");
+  WS_CUDA_TRY(cudaMalloc(&c->d_unit_off, (remote.size() + kMaxRounds + 1) * 8), "cudaMalloc");
 
   // Buffers start at a fraction of the worst case (every routed element sent
   // dense) and grow on demand: the all-gathered counts tell every rank what
@@ -203,40 +286,6 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
 // entry of that source) whose coordinate is this rank's, sized by the route's
 // overlap; the layouts of all ranks follow from the static plan (no data
 // exchange beyond the 64-byte handles, all-gathered over NCCL).
-namespace {
-// Remote entries of rank g, in the order rank g builds them (init_comm).
-std::vector<int> remote_routes(const Plan& plan, int g) {
-  std::vector<int> out;
-  const auto& rs = plan.routes_of(g);
-  for (int i = 0; i < (int)rs.size(); ++i)
-    if (plan.replicas() > 1 || rs[i].coord != plan.coord_of_rank(g)) out.push_back(i);
-  return out;
-}
-struct RecvLayout {
-  std::vector<std::pair<int, int>> entries;  // (source rank, its remote-entry index)
-  std::vector<uint64_t> off, cap;            // records
-  uint64_t records = 0;
-  size_t head = 0;                           // mailbox + count slots, bytes
-};
-RecvLayout recv_layout(const Plan& plan, int q) {
-  RecvLayout L;
-  const int k = plan.coord_of_rank(q);
-  for (int g = 0; g < plan.world(); ++g) {
-    if (g == q) continue;
-    const std::vector<int> rr = remote_routes(plan, g);
-    for (int e = 0; e < (int)rr.size(); ++e) {
-      const Route& r = plan.routes_of(g)[rr[e]];
-      if (r.coord != k) continue;
-      L.entries.emplace_back(g, e);
-      L.off.push_back(L.records);
-      L.cap.push_back(r.overlap);
-      L.records += r.overlap;
-    }
-  }
-  L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
-  return L;
-}
-}  // namespace
 
 ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
                               const std::vector<uint64_t>& recv_full) {
@@ -245,8 +294,14 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
   const size_t wb = wire_bytes(dtype_);
   (void)send_full;
   (void)recv_full;
+  // rounds: WSYNC_ROUNDS (1..kMaxRounds).  Measured (Qwen3-8B, 1%): 3 rounds
+  // take N = 4 from 4.10 to 3.74 ms; at N = 2 the 0.46 ms exchange gains
+  // nothing from the split, so one round there.
+  int R = W >= 4 ? 3 : 1;
+  if (const char* e = getenv("WSYNC_ROUNDS")) R = std::max(1, std::min(kMaxRounds, atoi(e)));
+  const uint32_t tile = encode_tile_elems(dtype_);
   std::vector<RecvLayout> lay(W);
-  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q);
+  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q, R, tile);
   const size_t bytes = lay[me].head + std::max<uint64_t>(1, lay[me].records) * wb;
   if (cudaMalloc(&c->d_p2p, bytes) != cudaSuccess)
     return set_error(WS_CUDA, "p2p: receive buffer allocation failed");
@@ -376,24 +431,74 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
     WS_CUDA_TRY(cudaMemcpy(c->d_rseg_first, first.data(), first.size() * 4,
                            cudaMemcpyHostToDevice), "H2D");
   }
-  // receiver: my regions
-  const RecvLayout& L = lay[me];
-  std::vector<RecvEntry> re(std::max<size_t>(1, L.entries.size()));
-  for (int j = 0; j < (int)L.entries.size(); ++j) {
-    re[j] = RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first};
-    P.expect_mask |= 1u << L.entries[j].first;
+  // rounds of my segments / entries (sender side)
+  c->R = R;
+  {
+    const std::vector<int> sr = segment_rounds(plan_, me, R, tile);
+    const auto& segs = plan_.segments();
+    c->seg_first.assign(R + 1, (int)segs.size());
+    c->tile_first.assign(R + 1, 0);
+    c->ent_first.assign(R + 1, (int)mine.size());
+    uint32_t t = 0;
+    for (int r = R - 1; r >= 0; --r)
+      for (int i = (int)segs.size() - 1; i >= 0; --i)
+        if (sr[i] >= r) c->seg_first[r] = i;
+    for (size_t i = 0; i < segs.size(); ++i) {
+      for (int r = 0; r <= R; ++r)
+        if (c->seg_first[r] == (int)i) c->tile_first[r] = t;
+      t += (uint32_t)((segs[i].n + tile - 1) / tile);
+    }
+    for (int r = 0; r <= R; ++r)
+      if (c->seg_first[r] == (int)segs.size()) c->tile_first[r] = t;
+    for (int r = R - 1; r >= 0; --r)
+      for (int e = (int)mine.size() - 1; e >= 0; --e)
+        if (sr[plan_.routes_of(me)[mine[e]].seg] >= r) c->ent_first[r] = e;
   }
-  WS_CUDA_TRY(cudaMalloc(&c->d_rentries, re.size() * sizeof(RecvEntry)), "cudaMalloc");
-  WS_CUDA_TRY(cudaMemcpy(c->d_rentries, re.data(), re.size() * sizeof(RecvEntry),
-                         cudaMemcpyHostToDevice), "H2D");
-  WS_CUDA_TRY(cudaMalloc(&c->d_recv_units, (L.entries.size() + 1) * 8), "cudaMalloc");
+  // receiver: my regions, per round
+  const RecvLayout& L = lay[me];
+  c->rr.assign(R, Comm::RoundRecv{});
+  for (int r = 0; r < R; ++r) {
+    Comm::RoundRecv& X = c->rr[r];
+    for (int k = 0; k < kMaxWorld; ++k)
+      for (int q = 0; q < kMaxReplicas; ++q) X.dest_rank[k][q] = -1;
+    std::vector<char> to(c->coords, 0);
+    for (int e = c->ent_first[r]; e < c->ent_first[r + 1]; ++e)
+      to[plan_.routes_of(me)[mine[e]].coord] = 1;
+    for (int k = 0; k < c->coords; ++k) {
+      if (!to[k]) continue;
+      int q = 0;
+      for (int g : c->dests[k]) X.dest_rank[k][q++] = g;
+    }
+    std::vector<RecvEntry> re;
+    for (int j = 0; j < (int)L.entries.size(); ++j)
+      if (L.round[j] == r) {
+        re.push_back(RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first});
+        X.mask |= 1u << L.entries[j].first;
+      }
+    X.n = (int)re.size();
+    P.expect_mask |= X.mask;
+    WS_CUDA_TRY(cudaMalloc(&X.d_rentries, std::max<size_t>(1, re.size()) * sizeof(RecvEntry)),
+                "cudaMalloc");
+    if (!re.empty())
+      WS_CUDA_TRY(cudaMemcpy(X.d_rentries, re.data(), re.size() * sizeof(RecvEntry),
+                             cudaMemcpyHostToDevice), "H2D");
+    WS_CUDA_TRY(cudaMalloc(&X.d_units, (re.size() + 1) * 8), "cudaMalloc");
+  }
+  if (R > 1) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    WS_CUDA_TRY(cudaStreamCreateWithPriority(&c->s_enc, cudaStreamNonBlocking, hi), "stream");
+    WS_CUDA_TRY(cudaStreamCreateWithPriority(&c->s_xchg, cudaStreamNonBlocking, lo), "stream");
+    c->ev_round.resize(R);
+    for (auto& e : c->ev_round) WS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
+    WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming), "ev");
+    WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming), "ev");
+    WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_encdone, cudaEventDisableTiming), "ev");
+  }
   P.edest = c->d_edest;
   P.ent_cnt = c->d_ent_cnt;
   P.recv = static_cast<char*>(c->d_p2p) + L.head;
-  P.rentries = c->d_rentries;
-  P.nrecv = (int)L.entries.size();
   P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_p2p) + kMailboxBytes);
-  P.recv_units = c->d_recv_units;
   P.err = c->d_err;
   if (const char* d = getenv("WSYNC_P2P_DEBUG")) P.debug = atoi(d);
   c->nsend_entries = (int)mine.size();
@@ -542,42 +647,163 @@ void ws_engine::destroy_comm() {
 
 ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
   Comm* c = comm_;
-  if (c) c->k1_emit = false;  // set again by exchange_fuse_k1 when K1 emits this sync
-  if (!c || !c->p2p || !c->pargs.dense_direct || !c->pargs.expect_mask) return WS_OK;
+  if (!c) return WS_OK;
+  c->k1_emit = false;  // set again by exchange_fuse_k1 when K1 emits this sync
+  if (!c->p2p) return WS_OK;
+  ++c->step;  // this sync's rounds carry epochs R * step + r
+  if (!c->pargs.dense_direct || !c->pargs.expect_mask) return WS_OK;
   P2PArgs p = c->pargs;
-  p.epoch = c->epoch + 1;  // the number exchange() gives this sync
+  p.epoch = (uint32_t)(c->R * c->step + c->R - 1);  // reached every round of this step
   WS_CUDA_TRY(launch_p2p_ready(p, s), "p2p ready");
   *launches += 1;
   return WS_OK;
 }
 
+int ws_engine::exchange_rounds() const {
+  return comm_ && comm_->p2p ? comm_->R : 1;
+}
+
 ws_status ws_engine::exchange_fuse_k1(EncodeArgs& a, cudaStream_t s) {
   Comm* c = comm_;
   if (c) c->k1_emit = false;
-  // Opt-in (WSYNC_FUSED_REMOTE=1).  Measured on 2 and 4 B200s it is slower
-  // than the separate pack: the ballots, counters and NVLink stores sit on
-  // K1's issue-bound critical path (+0.4 ms at 1%), and waiting for the
-  // previous step's acks inside K1 couples the ranks' start times; the pack
-  // it replaces costs 0.2-0.5 ms.  See DESIGN.md §6.
+  // Opt-in (WSYNC_FUSED_REMOTE=1, single round).  Measured on 2 and 4 B200s
+  // it is slower than the separate pack: the ballots, counters and NVLink
+  // stores sit on K1's issue-bound critical path (+0.4 ms at 1%), and
+  // waiting for the previous step's acks inside K1 couples the ranks' start
+  // times; the pack it replaces costs 0.2-0.5 ms.  See DESIGN.md §6.
   static const bool enabled = [] {
     const char* e = getenv("WSYNC_FUSED_REMOTE");
     return e && e[0] == '1';
   }();
   // Only with direct dense boxes: a segment that comes out dense after K1
   // emitted some of its records then reports 0 of them (pack_kernel).
-  if (!c || !c->p2p || !c->pargs.dense_direct || dtype_ != WS_BF16 || !enabled ||
+  if (!c || !c->p2p || c->R != 1 || !c->pargs.dense_direct || dtype_ != WS_BF16 || !enabled ||
       !c->nsend_entries)
     return WS_OK;
   WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt, 0, c->nsend_entries * 4, s), "memset");
   a.remote.maps = c->d_rmaps;
   a.remote.seg_first = c->d_rseg_first;
-  a.remote.ack = c->pargs.mailbox + 2 * c->world;
+  a.remote.ack = c->pargs.mailbox + mb_ack(c->world, 0, 0);
   a.remote.ack_mask = 0;
   for (int k = 0; k < kMaxWorld; ++k)
-    for (int r = 0; r < kMaxReplicas && c->pargs.dest_rank[k][r] >= 0; ++r)
-      a.remote.ack_mask |= 1u << c->pargs.dest_rank[k][r];
-  a.remote.epoch = c->epoch + 1;  // the number exchange() gives this sync
+    for (int r = 0; r < kMaxReplicas && c->rr[0].dest_rank[k][r] >= 0; ++r)
+      a.remote.ack_mask |= 1u << c->rr[0].dest_rank[k][r];
+  a.remote.epoch = (uint32_t)c->step;  // waits for acks >= epoch - 1 (the previous step)
   c->k1_emit = true;
+  return WS_OK;
+}
+
+// One P2P exchange round: pack this round's remote entries (records into the
+// replicas' regions, dense boxes into their serving arenas), publish, and
+// apply what the sources sent for this round.  No host synchronisation.
+ws_status ws_engine::exchange_round(const ws_sync_options& o, int next_arena, int round,
+                                    cudaStream_t s, uint32_t* launches) {
+  Comm* c = comm_;
+  const Comm::RoundRecv& X = c->rr[round];
+  const int e0 = c->ent_first[round], ne = c->ent_first[round + 1] - e0;
+  P2PArgs P = c->pargs;
+  P.round = round;
+  P.epoch = (uint32_t)(c->R * c->step + round);
+  P.prev_epoch = c->step > 1 ? (uint32_t)(c->R * (c->step - 1) + round) : 0u;
+  for (int k = 0; k < kMaxWorld; ++k)
+    for (int q = 0; q < kMaxReplicas; ++q) P.dest_rank[k][q] = X.dest_rank[k][q];
+  P.edest = c->d_edest + e0;
+  P.ent_cnt = c->d_ent_cnt + e0;
+  P.rentries = X.d_rentries;
+  P.nrecv = X.n;
+  P.recv_units = X.d_units;
+  P.expect_mask = X.mask;
+  if (ne && !c->k1_emit)
+    WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt + e0, 0, ne * 4, s), "memset");
+  PackArgs pa{};
+  pa.r.entries = c->d_entries + e0;
+  pa.r.nentries = ne;
+  pa.r.sparse = o.sparse ? 1 : 0;
+  pa.r.k1_emitted = c->k1_emit && o.sparse ? 1 : 0;
+  pa.r.seg_nnz = d_nnz_;
+  pa.r.seg_cap = d_cap_;
+  pa.r.seg_rec = d_rec_;
+  pa.r.seg_base = d_base_;
+  pa.r.rec_idx = d_idx_;
+  pa.r.rec_val = d_val_;
+  fill_tiles(pa.r);
+  pa.r.segs = d_segs_;
+  pa.r.train_next = arena[next_arena];
+  pa.r.serve = serve;
+  pa.r.unit_off = c->d_unit_off + e0 + round;
+  pa.region_off = c->d_region_off;
+  pa.region_cap = c->d_region_cap;
+  pa.region_cnt = c->d_region_cnt;
+  pa.err = c->d_err;
+  pa.p2p = P;
+  WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (p2p)");
+  if (ne) *launches += 2;
+  if (X.mask) {
+    WS_CUDA_TRY(launch_apply_p2p(dtype_, P, serve, sm_count() * 4, s), "apply (p2p)");
+    *launches += 2;
+  }
+  return WS_OK;
+}
+
+// A sync whose exchange is split in R rounds (P2P): round r's segments are
+// encoded on a high-priority stream; their pack/apply run on a low-priority
+// stream while K1 encodes round r + 1 on all but kOverlapSMs SMs (which the
+// exchange kernels then occupy).  The last round's exchange follows the local
+// route on the encode stream; the caller's stream joins both at the end.
+ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaStream_t s,
+                                 uint32_t* launches, cudaEvent_t* ev) {
+  Comm* c = comm_;
+  const int R = c->R;
+  static const int overlap_sms = [] {
+    const char* e = getenv("WSYNC_OVERLAP_SMS");
+    return e ? std::max(0, atoi(e)) : 28;
+  }();
+  static const bool overlap = [] {
+    const char* e = getenv("WSYNC_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  cudaStream_t ks = c->s_enc, xs = overlap ? c->s_xchg : c->s_enc;
+  WS_CUDA_TRY(cudaEventRecord(c->ev_start, s), "event");
+  WS_CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_start, 0), "wait");
+  if (xs != ks) WS_CUDA_TRY(cudaStreamWaitEvent(xs, c->ev_start, 0), "wait");
+  WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, ks), "memset counts");
+  if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, ks), "memset fill");
+  const EncodeArgs a = encode_args(pa, na);
+  const int sms = sm_count();
+  for (int r = 0; r < R; ++r) {
+    EncodeArgs ar = a;
+    ar.tile_offset = c->tile_first[r];
+    ar.ntiles = c->tile_first[r + 1] - c->tile_first[r];
+    if (overlap && r > 0 && sms > overlap_sms + 8) ar.max_grid = (uint32_t)(sms - overlap_sms);
+    if (ar.ntiles) {
+      WS_CUDA_TRY(launch_encode(dtype_, ar, ks), "encode (round)");
+      ++*launches;
+    }
+    if (count_only_) {
+      ws_status st = launch_fixup(a, c->seg_first[r], c->seg_first[r + 1], ks, launches);
+      if (st != WS_OK) return st;
+    }
+    if (r < R - 1) {
+      WS_CUDA_TRY(cudaEventRecord(c->ev_round[r], ks), "event");
+      if (xs != ks) WS_CUDA_TRY(cudaStreamWaitEvent(xs, c->ev_round[r], 0), "wait");
+      ws_status st = exchange_round(o, na, r, xs, launches);
+      if (st != WS_OK) return st;
+    }
+  }
+  WS_CUDA_TRY(cudaEventRecord(ev[2], ks), "event");
+  ws_status st = local_route(o, pa, na, ks, launches);
+  if (st != WS_OK) return st;
+  WS_CUDA_TRY(cudaEventRecord(ev[3], ks), "event");
+  st = exchange_round(o, na, R - 1, ks, launches);
+  if (st != WS_OK) return st;
+  if (xs != ks) {
+    WS_CUDA_TRY(cudaEventRecord(c->ev_xdone, xs), "event");
+    WS_CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_xdone, 0), "wait");
+  }
+  pulled_bytes_ = 0;
+  WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, ks), "D2H err");
+  WS_CUDA_TRY(cudaEventRecord(c->ev_encdone, ks), "event");
+  WS_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_encdone, 0), "wait");
   return WS_OK;
 }
 
@@ -587,40 +813,11 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   if (!c) return set_error(WS_INVALID_ARGUMENT, "exchange without a communicator");
   const size_t wb = wire_bytes(dtype_);
   if (c->p2p) {
-    // One kernel packs AND moves the records into the peers' receive
-    // buffers over NVLink; the receiving kernel waits on its own mailbox.
-    // No host synchronisation, no collective launch.
-    c->pargs.epoch = ++c->epoch;
-    if (c->nsend_entries && !c->k1_emit)
-      WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt, 0, c->nsend_entries * 4, s), "memset");
-    PackArgs pa{};
-    pa.r.entries = c->d_entries;
-    pa.r.nentries = c->nentries;
-    pa.r.sparse = o.sparse ? 1 : 0;
-    pa.r.k1_emitted = c->k1_emit && o.sparse ? 1 : 0;
-    pa.r.seg_nnz = d_nnz_;
-    pa.r.seg_cap = d_cap_;
-    pa.r.seg_rec = d_rec_;
-    pa.r.seg_base = d_base_;
-    pa.r.rec_idx = d_idx_;
-    pa.r.rec_val = d_val_;
-    fill_tiles(pa.r);
-    pa.r.segs = d_segs_;
-    pa.r.train_next = arena[next_arena];
-    pa.r.serve = serve;
-    pa.r.unit_off = c->d_unit_off;
-    pa.region_off = c->d_region_off;
-    pa.region_cap = c->d_region_cap;
-    pa.region_cnt = c->d_region_cnt;
-    pa.err = c->d_err;
-    pa.p2p = c->pargs;
-    WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (p2p)");
-    if (c->nentries) *launches += 2;
-    if (c->pargs.expect_mask) {
-      WS_CUDA_TRY(launch_apply_p2p(dtype_, c->pargs, serve, sm_count() * 4, s), "apply (p2p)");
-      *launches += 2;
+    for (int r = 0; r < c->R; ++r) {
+      ws_status st = exchange_round(o, next_arena, r, s, launches);
+      if (st != WS_OK) return st;
     }
-    pulled_bytes_ = 0;  // filled by exchange_report() when a report is asked for
+    pulled_bytes_ = 0;
     WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
     return WS_OK;
   }

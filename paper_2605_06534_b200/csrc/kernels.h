@@ -117,6 +117,8 @@ struct EncodeArgs {
   // = 1, from the previous sync) are only counted.  A second launch then
   // processes the tiles of those that turned out sparse: tile_list /
   // ntiles_dev give its super-tiles and `fill` (zeroed) their reservations.
+  uint32_t tile_offset;           // this launch claims super-tiles [tile_offset, + ntiles)
+  uint32_t max_grid;              // 0: one block per SM; else at most this many (SMs left free)
   const uint32_t* seg_mode;
   const uint32_t* tile_list;
   const uint32_t* ntiles_dev;
@@ -127,9 +129,9 @@ struct EncodeArgs {
 // Between the two K1 launches of an engine sync: lists the super-tiles of
 // the count-only segments that came out sparse, and sets every segment's
 // mode for the next sync (dense now -> count-only next).
-cudaError_t launch_fixup_plan(const uint32_t* tile0, int nseg, const uint64_t* seg_nnz,
-                              const uint64_t* seg_cap, uint32_t* seg_mode, uint32_t* tile_list,
-                              uint32_t* ntiles_dev, cudaStream_t s);
+cudaError_t launch_fixup_plan(const uint32_t* tile0, int seg_begin, int seg_end,
+                              const uint64_t* seg_nnz, const uint64_t* seg_cap, uint32_t* seg_mode,
+                              uint32_t* tile_list, uint32_t* ntiles_dev, cudaStream_t s);
 
 constexpr uint32_t kMaxEncodeGrid = 160;  // >= SMs of a B200 (148)
 size_t encode_spill_bytes(int dtype, uint32_t blocks);

@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           mbar_arrive(&full[k]);
           break;
         }
-        const uint32_t t = a.tile_list ? __ldg(a.tile_list + tk) : tk;
+        const uint32_t t = a.tile_list ? __ldg(a.tile_list + tk) : tk + a.tile_offset;
         const int s = a.tile_seg ? (int)__ldg(a.tile_seg + t)
                                  : (a.tile0 ? find_segment(a.tile0, a.nseg, t) : 0);
         const SegDev sg = a.segs ? a.segs[s] : a.seg0;
@@ -942,13 +942,13 @@ int sm_count() {
   return n;
 }
 
-__global__ void fixup_plan_kernel(const uint32_t* tile0, int nseg, const uint64_t* seg_nnz,
-                                  const uint64_t* seg_cap, uint32_t* seg_mode,
-                                  uint32_t* tile_list, uint32_t* ntiles_dev) {
+__global__ void fixup_plan_kernel(const uint32_t* tile0, int seg_begin, int seg_end,
+                                  const uint64_t* seg_nnz, const uint64_t* seg_cap,
+                                  uint32_t* seg_mode, uint32_t* tile_list, uint32_t* ntiles_dev) {
   __shared__ uint32_t s_n;
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
+  for (int s = seg_begin + threadIdx.x; s < seg_end; s += blockDim.x) {
     const bool dense = seg_nnz[s] > seg_cap[s];
     if (seg_mode[s] && !dense) {  // counted only, but sparse after all: list its tiles
       const uint32_t t0 = tile0[s], nt = tile0[s + 1] - t0;
@@ -961,11 +961,11 @@ __global__ void fixup_plan_kernel(const uint32_t* tile0, int nseg, const uint64_
   if (threadIdx.x == 0) *ntiles_dev = s_n;
 }
 
-cudaError_t launch_fixup_plan(const uint32_t* tile0, int nseg, const uint64_t* seg_nnz,
-                              const uint64_t* seg_cap, uint32_t* seg_mode, uint32_t* tile_list,
-                              uint32_t* ntiles_dev, cudaStream_t s) {
-  fixup_plan_kernel<<<1, 1024, 0, s>>>(tile0, nseg, seg_nnz, seg_cap, seg_mode, tile_list,
-                                       ntiles_dev);
+cudaError_t launch_fixup_plan(const uint32_t* tile0, int seg_begin, int seg_end,
+                              const uint64_t* seg_nnz, const uint64_t* seg_cap, uint32_t* seg_mode,
+                              uint32_t* tile_list, uint32_t* ntiles_dev, cudaStream_t s) {
+  fixup_plan_kernel<<<1, 256, 0, s>>>(tile0, seg_begin, seg_end, seg_nnz, seg_cap, seg_mode,
+                                      tile_list, ntiles_dev);
   return cudaGetLastError();
 }
 
@@ -996,6 +996,7 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
   int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(),
                                                            std::max(a.ntiles, 1u)));
   if (const char* g = getenv("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
+  if (a.max_grid) grid = std::min<int>(grid, (int)a.max_grid);
   if (!a.spill || a.spill_blocks == 0) return cudaErrorInvalidValue;
   grid = std::min<int>(grid, (int)a.spill_blocks);
   if (grid_out) *grid_out = grid;

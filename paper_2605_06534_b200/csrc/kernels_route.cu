@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     // every destination must have consumed our previous step's records
     for (int c = 0; c < kMaxWorld; ++c)
       for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
-        if (!wait_geq_sys(P.mailbox + 2 * W + P.dest_rank[c][r], P.epoch - 1) ||
-            (P.dense_direct && !wait_geq_sys(P.mailbox + 4 * W + P.dest_rank[c][r], P.epoch)))
+        if (!wait_geq_sys(P.mailbox + mb_ack(W, P.round, P.dest_rank[c][r]), P.prev_epoch) ||
+            (P.dense_direct &&
+             !wait_geq_sys(P.mailbox + mb_ready(W, P.dest_rank[c][r]), P.epoch)))
           atomicOr(P.err, kErrBitTimeout);
   }
   __syncthreads();
@@ -372,7 +373,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     __shared__ int s_last;
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(P.mailbox + 3 * W, 1ull) == gridDim.x - 1;
+    if (threadIdx.x == 0)
+      s_last = atomicAdd(P.mailbox + mb_pack_ctr(W, P.round), 1ull) == gridDim.x - 1;
     __syncthreads();
     if (s_last) {
       __threadfence();
@@ -388,8 +390,9 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
       if (threadIdx.x == 0) {
         for (int c = 0; c < kMaxWorld; ++c)
           for (int r = 0; r < kMaxReplicas && P.dest_rank[c][r] >= 0; ++r)
-            st_release_sys(P.peer_mailbox[P.dest_rank[c][r]] + W + P.rank, P.epoch);
-        P.mailbox[3 * W] = 0;
+            st_release_sys(P.peer_mailbox[P.dest_rank[c][r]] + mb_flag(W, P.round, P.rank),
+                           P.epoch);
+        P.mailbox[mb_pack_ctr(W, P.round)] = 0;
       }
     }
   }
@@ -456,7 +459,7 @@ __global__ void p2p_ready_kernel(P2PArgs P) {
   const int s = threadIdx.x;
   if (s < P.world && (P.expect_mask & (1u << s))) {
     __threadfence_system();
-    st_release_sys(P.peer_mailbox[s] + 4 * P.world + P.rank, P.epoch);
+    st_release_sys(P.peer_mailbox[s] + mb_ready(P.world, P.rank), P.epoch);
   }
 }
 
@@ -469,7 +472,8 @@ __global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
   __shared__ uint64_t s_carry;
   const int W = P.world, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < W && (P.expect_mask & (1u << tid)))
-    if (!wait_geq_sys(P.mailbox + W + tid, P.epoch)) atomicOr(P.err, kErrBitTimeout);
+    if (!wait_geq_sys(P.mailbox + mb_flag(W, P.round, tid), P.epoch))
+      atomicOr(P.err, kErrBitTimeout);
   if (tid == 0) s_carry = 0;
   __syncthreads();
   for (int base = 0; base < P.nrecv; base += 1024) {
@@ -550,12 +554,13 @@ __global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Trai
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned long long prev = atomicAdd(P.mailbox + 3 * W + 1, 1ull);
+    const unsigned long long prev = atomicAdd(P.mailbox + mb_apply_ctr(W, P.round), 1ull);
     if (prev == gridDim.x - 1) {
       __threadfence_system();
       for (int s = 0; s < W; ++s)
-        if (P.expect_mask & (1u << s)) st_release_sys(P.peer_mailbox[s] + 2 * W + P.rank, P.epoch);
-      P.mailbox[3 * W + 1] = 0;
+        if (P.expect_mask & (1u << s))
+          st_release_sys(P.peer_mailbox[s] + mb_ack(W, P.round, P.rank), P.epoch);
+      P.mailbox[mb_apply_ctr(W, P.round)] = 0;
     }
   }
 }

@@ -76,6 +76,21 @@ inline size_t wire_bytes(int dtype) { return dtype == WS_BF16 ? 8 : 16; }
 constexpr int kMaxWorld = 8;      // GPUs of one box
 constexpr int kMaxReplicas = 8;
 
+// Mailbox words (u64, in every rank's own HBM, written by its peers) for a
+// world of W ranks and R exchange rounds per sync:
+//   [0, W)                      ready[g]: rank g reached step e (posted at the sync's start)
+//   per round r, b = W + r(2W+2):
+//     [b, b+W)                  flag[g]: source g published round r of step e
+//     [b+W, b+2W)               ack[g]: destination g applied round r of step e
+//     b+2W, b+2W+1              pack / apply blocks done (last-block detection)
+// Round r of step e carries epoch R*e + r; ready[g] = R*e + R - 1.
+constexpr int kMaxRounds = 4;
+__host__ __device__ inline size_t mb_ready(int, int g) { return (size_t)g; }
+__host__ __device__ inline size_t mb_flag(int W, int r, int g) { return (size_t)(W + r * (2 * W + 2) + g); }
+__host__ __device__ inline size_t mb_ack(int W, int r, int g) { return (size_t)(W + r * (2 * W + 2) + W + g); }
+__host__ __device__ inline size_t mb_pack_ctr(int W, int r) { return (size_t)(W + r * (2 * W + 2) + 2 * W); }
+__host__ __device__ inline size_t mb_apply_ctr(int W, int r) { return mb_pack_ctr(W, r) + 1; }
+
 // Peer-memory (P2P) exchange state shared by the pack and apply kernels.
 // Mailbox of every rank (u64 words, in its own HBM, mapped by all peers):
 //   [0, W) records sent by rank s this step   [W, 2W) step flag from s
@@ -87,7 +102,9 @@ struct P2PArgs {
   int32_t on;                       // 0: NCCL mode (send region + host exchange)
   int32_t debug;                    // perf experiments (WSYNC_P2P_DEBUG): 1 no scatter, 2 no records
   int32_t world, rank;
-  uint32_t epoch;                   // this step's number (>= 1), equal on every rank
+  int32_t round;                    // exchange round of this launch (< kMaxRounds)
+  uint32_t epoch;                   // R * step + round, equal on every rank
+  uint32_t prev_epoch;              // the same round's epoch of the previous step (0: none)
   unsigned long long* mailbox;                        // local
   unsigned long long* peer_mailbox[kMaxWorld];        // mapped peers' mailboxes
   void* dest[kMaxWorld][kMaxReplicas];                // per coordinate: my region at each replica
