@@ -309,6 +309,11 @@ ws_status ws_plan_serve_shard(const ws_plan* plan, int i, int32_t* param,
 ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_rank,
                                      int32_t* tp_size, int32_t* pp_stage);
 
+/* Checks, on the host, the peer-memory exchange layouts every rank of this
+ * plan would build with `rounds` exchange rounds (entries, rounds,
+ * destinations vs expectations, mailbox size): WS_OK when consistent. */
+ws_status ws_plan_check_exchange(const ws_plan* plan, int rounds);
+
 /* Route i: source segment, destination serving coordinate, number of
  * destination ranks (replicas of that coordinate) and the elements of the
  * box intersection. */

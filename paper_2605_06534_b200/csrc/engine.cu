@@ -45,9 +45,6 @@ LocalEntry make_local_entry(int dtype, const int64_t* full, int nd, int seg, con
 
 }  // namespace wsync
 
-struct ws_plan {
-  std::unique_ptr<Plan> p;
-};
 
 static ws_status plan_guard(const std::function<void()>& f) {
   try {

@@ -7,6 +7,12 @@
 #include "plan.h"
 #include "route.h"
 
+#include <memory>
+
+struct ws_plan {  // the C-ABI plan handle
+  std::unique_ptr<wsync::Plan> p;
+};
+
 struct ws_engine {
   ws_engine(const wsync::Plan& plan, int device);
   ~ws_engine();

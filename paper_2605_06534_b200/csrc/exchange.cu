@@ -928,6 +928,61 @@ ws_status ws_engine::exchange_status() const {
   return WS_OK;
 }
 
+// Host-only consistency check of the P2P exchange layouts of every rank of
+// a plan (what init_p2p builds per rank): each remote entry of every sender
+// appears exactly once in the layout of each replica of its coordinate, in
+// the round of its segment; a receiver expects a source in round r exactly
+// when that source sends it something in round r; the mailbox fits.
+extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
+  if (!plan_h || rounds < 1 || rounds > kMaxRounds)
+    return set_error(WS_INVALID_ARGUMENT, "ws_plan_check_exchange: bad argument");
+  const Plan& plan = *plan_h->p;
+  const int W = plan.world(), R = rounds;
+  if (W > kMaxWorld) return set_error(WS_INVALID_ARGUMENT, "world beyond kMaxWorld");
+  if ((size_t)(W + R * (2 * W + 2)) * 8 > kMailboxBytes)
+    return set_error(WS_CAPACITY, "mailbox too small for this world and round count");
+  const uint32_t tile = encode_tile_elems(plan.dtype());
+  std::vector<RecvLayout> lay(W);
+  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan, q, R, tile);
+  // expectation per (receiver, round) from the layouts
+  std::vector<std::vector<uint32_t>> expect(W, std::vector<uint32_t>(R, 0));
+  for (int q = 0; q < W; ++q)
+    for (size_t j = 0; j < lay[q].entries.size(); ++j)
+      expect[q][lay[q].round[j]] |= 1u << lay[q].entries[j].first;
+  std::vector<std::vector<uint32_t>> sends(W, std::vector<uint32_t>(R, 0));
+  for (int g = 0; g < W; ++g) {
+    const std::vector<int> rr = remote_routes(plan, g);
+    const std::vector<int> sr = segment_rounds(plan, g, R, tile);
+    int prev_round = 0;
+    for (int e = 0; e < (int)rr.size(); ++e) {
+      const Route& rt = plan.routes_of(g)[rr[e]];
+      const int round = sr[rt.seg];
+      if (round < prev_round) return set_error(WS_TRANSFER_ERROR, "entry rounds not monotonic");
+      prev_round = round;
+      for (int q = 0; q < W; ++q) {
+        if (q == g || plan.coord_of_rank(q) != rt.coord) continue;
+        int hits = 0;
+        for (size_t j = 0; j < lay[q].entries.size(); ++j)
+          if (lay[q].entries[j].first == g && lay[q].entries[j].second == e) {
+            ++hits;
+            if (lay[q].round[j] != round)
+              return set_error(WS_TRANSFER_ERROR, "entry round differs at a receiver");
+            if (lay[q].cap[j] != rt.overlap)
+              return set_error(WS_TRANSFER_ERROR, "entry capacity differs at a receiver");
+          }
+        if (hits != 1) return set_error(WS_TRANSFER_ERROR, "entry missing or duplicated at a receiver");
+        sends[g][round] |= 1u << q;
+      }
+    }
+  }
+  for (int q = 0; q < W; ++q)
+    for (int r = 0; r < R; ++r)
+      for (int g = 0; g < W; ++g)
+        if (((expect[q][r] >> g) & 1u) != ((sends[g][r] >> q) & 1u))
+          return set_error(WS_TRANSFER_ERROR, "expectation and destinations disagree");
+  return WS_OK;
+}
+
 extern "C" ws_status ws_nccl_unique_id(uint8_t out[128]) {
   ncclUniqueId id;
   WS_NCCL_TRY(ncclGetUniqueId(&id), "ncclGetUniqueId");

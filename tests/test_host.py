@@ -178,3 +178,22 @@ def test_expert_thresholds_match_restatement():
     zipf = ws.expert_thresholds(128, 0.01, 1.1, 7)
     assert max(zipf) > 0.2 * 4294967296.0  # the hottest expert runs dense (> threshold)
     assert sorted(zipf) == sorted(ws.expert_thresholds(128, 0.01, 1.1, 8))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("rounds", [1, 3, 4])
+def test_exchange_layouts_consistent(world, rounds):
+    """The P2P exchange every rank builds (receive regions, rounds, who
+    expects whom) is consistent for the bench layout up to 8 GPUs -- the
+    N = 8 path the pool cannot run is checked here on the host."""
+    import paper_2605_06534_b200 as ws
+    from paper_2605_06534_b200._lib import check, lib
+    tp = 1 if world == 1 else 2
+    layouts = [(ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp), ws.MODELS["qwen3-8b"]()),
+               (ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(max(1, world // 2), 1, min(2, world)),
+                ws.MODELS["qwen3-32b"]([0, 63])),
+               (ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1),
+                ws.MODELS["qwen3-30b-a3b"]([0, 47]))]
+    for train, serve, manifest in layouts:
+        plan = ws.Plan(manifest, ws.BF16, train, serve, world=world, rank=0)
+        check(lib.ws_plan_check_exchange(plan.h, rounds))
