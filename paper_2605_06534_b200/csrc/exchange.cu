@@ -74,8 +74,6 @@ struct ws_engine::Comm {
   bool k1_emit = false;                          // this sync's records went out from K1
   EntryDest* d_edest = nullptr;
   unsigned int* d_ent_cnt = nullptr;
-  RecvEntry* d_rentries = nullptr;
-  uint64_t* d_recv_units = nullptr;
   int nsend_entries = 0;
   // exchange rounds (P2P): K1 encodes segment runs round by round and round
   // r's pack/apply overlap the encode of round r + 1
@@ -106,8 +104,6 @@ struct ws_engine::Comm {
     cudaFree(d_rmaps);
     cudaFree(d_rseg_first);
     cudaFree(d_ent_cnt);
-    cudaFree(d_rentries);
-    cudaFree(d_recv_units);
     for (auto& x : rr) {
       cudaFree(x.d_rentries);
       cudaFree(x.d_units);
@@ -357,7 +353,6 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
     P.peer_mailbox[g] = static_cast<unsigned long long*>(g == me ? c->d_p2p : c->peer[g]);
   for (int k = 0; k < kMaxWorld; ++k)
     for (int r = 0; r < kMaxReplicas; ++r) {
-      P.dest[k][r] = nullptr;
       P.dest_rank[k][r] = -1;
     }
   // sender: where each of my remote entries goes at each replica; only the

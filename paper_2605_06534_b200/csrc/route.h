@@ -107,7 +107,6 @@ struct P2PArgs {
   uint32_t prev_epoch;              // the same round's epoch of the previous step (0: none)
   unsigned long long* mailbox;                        // local
   unsigned long long* peer_mailbox[kMaxWorld];        // mapped peers' mailboxes
-  void* dest[kMaxWorld][kMaxReplicas];                // per coordinate: my region at each replica
   int32_t dest_rank[kMaxWorld][kMaxReplicas];         // -1 terminated
   // Dense-fallback boxes bypass the records: with dense_direct the pack
   // kernel copies them straight into every replica's (IPC-mapped) serving
