@@ -46,6 +46,8 @@ struct ws_engine {
   ws_status size_send(const std::vector<uint64_t>& region_cap);
   ws_status size_recv(uint64_t records);
   void destroy_comm();
+  // refuses options the exchange was not sized for (before any work is queued)
+  ws_status exchange_admit(const ws_sync_options& o) const;
   ws_status exchange_begin(cudaStream_t s, uint32_t* launches);  // P2P "reached step" flags
   ws_status exchange_status() const;                             // faults seen by the kernels
   int exchange_rounds() const;

@@ -340,7 +340,9 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
                                uint64_t* nnz_host, ws_report* report) {
   if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "sync: unbound");
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
-  ws_status st = ensure_records(o.density_threshold, o.sparse ? 1 : 0);
+  ws_status st = exchange_admit(o);
+  if (st != WS_OK) return st;
+  st = ensure_records(o.density_threshold, o.sparse ? 1 : 0);
   if (st != WS_OK) return st;
   const int pa = o.reverse ? 1 : 0, na = 1 - pa;
   const int esz = dtype_size(dtype_);

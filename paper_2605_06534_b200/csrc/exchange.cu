@@ -182,6 +182,24 @@ struct RecvLayout {
   uint64_t records = 0;
   size_t head = 0;                           // mailbox + count slots, bytes
 };
+// WSYNC_MAX_THRESHOLD = t > 0 bounds every receive region by the records
+// its source segment can hold as a sparse shard, floor(t * n) (+1), instead
+// of the full overlap: dense boxes never travel as records when they go
+// straight into the serving arenas (bind fails otherwise), and syncs with a
+// density threshold above t are refused.
+double max_threshold() {
+  static const double t = [] {
+    const char* e = getenv("WSYNC_MAX_THRESHOLD");
+    return e ? atof(e) : 0.0;
+  }();
+  return t;
+}
+uint64_t entry_capacity(const Plan& plan, int g, const Route& r) {
+  const double t = max_threshold();
+  if (t <= 0.0 || t >= 1.0) return r.overlap;
+  const uint64_t n = plan.segments_of(g)[r.seg].n;
+  return std::min<uint64_t>(r.overlap, (uint64_t)(t * (double)n) + 1);
+}
 RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
   RecvLayout L;
   const int k = plan.coord_of_rank(q);
@@ -192,11 +210,12 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
     for (int e = 0; e < (int)rr.size(); ++e) {
       const Route& r = plan.routes_of(g)[rr[e]];
       if (r.coord != k) continue;
+      const uint64_t cap = entry_capacity(plan, g, r);
       L.entries.emplace_back(g, e);
       L.off.push_back(L.records);
-      L.cap.push_back(r.overlap);
+      L.cap.push_back(cap);
       L.round.push_back(sr[r.seg]);
-      L.records += r.overlap;
+      L.records += cap;
     }
   }
   L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
@@ -371,7 +390,7 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
     EntryDest& D = ed[e];
     std::memset(&D, 0, sizeof(D));
     const Route& rt = plan_.routes_of(me)[mine[e]];
-    D.cap = rt.overlap;
+    D.cap = entry_capacity(plan_, me, rt);
     int r = 0;
     for (int q : c->dests[rt.coord]) {
       const RecvLayout& L = lay[q];
@@ -594,7 +613,12 @@ ws_status ws_engine::map_serve() {
   for (int k = 0; k < kMaxWorld; ++k)
     for (int r = 0; r < kMaxReplicas; ++r) P.serve_dst[k][r] = nullptr;
   const char* env = getenv("WSYNC_DENSE_DIRECT");
-  if (!ok || (env && env[0] == '0')) return WS_OK;
+  if (!ok || (env && env[0] == '0')) {
+    if (max_threshold() > 0.0)
+      return set_error(WS_CAPACITY, "WSYNC_MAX_THRESHOLD needs direct dense boxes, but a serving "
+                                    "arena is not IPC-mappable (or WSYNC_DENSE_DIRECT=0)");
+    return WS_OK;
+  }
   for (int k = 0; k < c->coords; ++k) {
     int r = 0;
     for (int g : c->dests[k])
@@ -638,6 +662,14 @@ ws_status ws_engine::size_recv(uint64_t records) {
 void ws_engine::destroy_comm() {
   delete comm_;
   comm_ = nullptr;
+}
+
+ws_status ws_engine::exchange_admit(const ws_sync_options& o) const {
+  const Comm* c = comm_;
+  if (c && c->p2p && max_threshold() > 0.0 && o.sparse && o.density_threshold > max_threshold())
+    return set_error(WS_INVALID_ARGUMENT,
+                     "density_threshold above the exchange sizing (WSYNC_MAX_THRESHOLD)");
+  return WS_OK;
 }
 
 ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
@@ -962,7 +994,7 @@ extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
             ++hits;
             if (lay[q].round[j] != round)
               return set_error(WS_TRANSFER_ERROR, "entry round differs at a receiver");
-            if (lay[q].cap[j] != rt.overlap)
+            if (lay[q].cap[j] != entry_capacity(plan, g, rt))
               return set_error(WS_TRANSFER_ERROR, "entry capacity differs at a receiver");
           }
         if (hits != 1) return set_error(WS_TRANSFER_ERROR, "entry missing or duplicated at a receiver");

@@ -2,8 +2,9 @@
   3: Qwen3-32B, trainer TP-N -> serving TP-N/2 x 2 replicas, 0.5% density;
   4: Qwen3-30B-A3B, expert-sharded trainer TP-N -> EP-N serving, Zipf(1.1)
      per-expert densities around 1%.
-Layer subsets keep the worst-case receive regions within HBM (DESIGN.md §10);
-the reported figure is dense-equivalent GB/s over the synced elements.
+By default, layer subsets keep the worst-case receive regions within HBM;
+--full runs the whole models and needs WSYNC_MAX_THRESHOLD=0.2.
+The reported figure is dense-equivalent GB/s over the synced elements.
 
     torchrun --nproc-per-node 4 --master-addr 127.0.0.1 scripts/config_bench.py
 """
@@ -44,6 +45,11 @@ def timed(eng, steps):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--full", action="store_true",
+                    help="whole models (set WSYNC_MAX_THRESHOLD=0.2 to bound the receive regions)")
+    args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -59,10 +65,10 @@ def main():
         return obj[0]
     half = max(1, world // 2)
     cases = [
-        ("config3", "qwen3-32b", list(range(0, 64, 4)), ws.TrainConfig("tp", world, 1, 1),
-         ws.ServeConfig(half, 1, world // half), 0.005, None),
-        ("config4", "qwen3-30b-a3b", list(range(0, 48, 4)), ws.TrainConfig("tp", world, 1, 1),
-         ws.ServeConfig(world, 1, 1), 0.01, 1.1),
+        ("config3", "qwen3-32b", None if args.full else list(range(0, 64, 4)),
+         ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(half, 1, world // half), 0.005, None),
+        ("config4", "qwen3-30b-a3b", None if args.full else list(range(0, 48, 4)),
+         ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1), 0.01, 1.1),
     ]
     for name, model, layers, train, serve, density, zipf in cases:
         manifest = ws.MODELS[model](layers)
@@ -72,7 +78,8 @@ def main():
         ms, rep = timed(eng, 10)
         elems = plan.info.model_elems
         if rank == 0:
-            print(json.dumps({"config": name, "model": model, "layers": len(layers),
+            print(json.dumps({"config": name, "model": model,
+                              "layers": "all" if layers is None else len(layers),
                               "elements": elems, "n_gpus": world, "density": density,
                               "expert_zipf": zipf, "train": train.scheme if hasattr(train, "scheme") else "tp",
                               "serve": f"tp{serve.tp}x{serve.replicas}", "ms_per_sync": round(ms, 3),

@@ -134,6 +134,21 @@ def main():
     bad = serve_equals_gen(eng, plan, 8, 0.02, "prev")
     results["10 alternating syncs"] = bad or "ok"
     ok &= not bad
+    t = float(os.environ.get("WSYNC_MAX_THRESHOLD", "0"))
+    if world > 1 and 0 < t < 1 and os.environ.get("WSYNC_EXCHANGE", "p2p") == "p2p":
+        # receive regions sized for t: a sync with a larger threshold is refused
+        # before any work is queued, and the engine stays usable
+        try:
+            eng.sync_step(density_threshold=min(1.0, t + 0.1), report=False)
+            results["threshold above WSYNC_MAX_THRESHOLD"] = "accepted"
+            ok = False
+        except ws.TransferError as e:
+            results["threshold above WSYNC_MAX_THRESHOLD"] = "refused: " + str(e)[:60]
+        eng.sync_step(report=False)
+        torch.cuda.synchronize()
+        bad = serve_equals_gen(eng, plan, 8, 0.02, "next")
+        results["sync after refusal"] = bad or "ok"
+        ok &= not bad
     del eng
 
     # BASELINE config 3 (Qwen3-32B TP8 -> TP4 x 2, 0.5%) and config 4
