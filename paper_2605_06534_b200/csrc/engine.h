@@ -120,6 +120,11 @@ struct ws_engine {
   wsync::LocalEntry* d_local_ = nullptr;
   wsync::FuseEntry* d_fuse_ = nullptr;
   uint32_t* d_fuse_on_ = nullptr;
+  uint32_t sa_div_ = 0;  // K1 streamed apply for fused bf16 segments denser than 1/sa_div_ (0: off)
+  uint64_t* h_sa_ = nullptr;  // mapped: elements set to stream by the last worklist
+  uint64_t* d_sa_ = nullptr;
+  uint64_t sa_total_ = 0;     // elements of this rank's segments
+  bool sa_force_ = false;     // ablation: always the streamed-apply instantiation
   bool fuse_apply_ = true;  // K1 applies local sparse records (WSYNC_NO_FUSED_APPLY=1 disables)
   int nlocal_ = 0;
   uint64_t* d_unit_off_ = nullptr;

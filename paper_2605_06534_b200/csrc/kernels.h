@@ -124,6 +124,11 @@ struct EncodeArgs {
   const uint32_t* ntiles_dev;
   unsigned long long* fill;
   RemoteEmit remote;             // maps == null: no fused remote emission
+  // Streamed apply (bf16, fused identity routes, fuse_on == 2): the producer
+  // also streams the serving sub-tile into a third ring, and consumers store
+  // serve + (next - prev) for every changed 16-byte vector -- sequential
+  // instead of one scattered read-modify-write per record.
+  int32_t serve_stream;
 };
 
 // Between the two K1 launches of an engine sync: lists the super-tiles of

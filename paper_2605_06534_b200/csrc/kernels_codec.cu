@@ -91,7 +91,7 @@ struct StageMeta {
   SegDev sg;
   uint32_t t, s, lt, nsub, cnt, last;
   uint32_t count_only;  // segment predicted dense: count, stage nothing
-  uint32_t pad;
+  uint32_t sa;          // streamed apply: the serving sub-tile is in the third ring
 };
 
 #ifndef WS_ENC_SLOTS
@@ -104,7 +104,7 @@ struct StageMeta {
 #define WS_ENC_EVICT 0  // (measured: no gain) prev/next streamed evict-first, prefetched serving words evict-last
 #endif
 
-template <int DT>
+template <int DT, bool SA = false>
 struct EncCfg {
   using T = typename Traits<DT>::T;
   static constexpr int VE = Traits<DT>::kVE;                          // elements per vector
@@ -112,22 +112,27 @@ struct EncCfg {
   static constexpr uint32_t VPT = kStageBytes / 16 / kEncConsumers;   // vectors per thread per stage
   static constexpr uint32_t SUB = kStageBytes / sizeof(T);            // elements per sub-tile
   static constexpr uint32_t SUPER = SUB * kEncodeSubTiles;
-  static constexpr int K = WS_ENC_SLOTS;                              // staged changes per thread per super-tile
+  // staged changes per thread per super-tile (SA: fewer, to fit the third ring)
+  static constexpr int K = SA ? 4 : WS_ENC_SLOTS;
   static constexpr uint32_t SPW = SUPER / NCW;                        // spill capacity per warp (all its elements)
   using SpillRec = typename std::conditional<sizeof(T) == 2, uint32_t, uint2>::type;  // li | val
   static constexpr uint32_t WORDS = SUPER / 32;                       // change-bitmap words
   static constexpr int NB = kEncBuffers;                              // staging buffers
   // bf16: the serving word a fused record updates is fetched (cp.async) into
   // shared memory when the record is staged
-  static constexpr bool PRE = WS_ENC_PREFETCH && DT == WS_BF16;
-  static constexpr size_t kRingBytes = 2 * kRing * (size_t)kStageBytes;
+  // (SA: streamed tiles need no prefetch; the other fused tiles read the
+  // word at the flush -- the engine runs SA only when most tiles stream)
+  static constexpr bool PRE = WS_ENC_PREFETCH && DT == WS_BF16 && !SA;
+  // streamed apply: three arrays per stage (prev, next, serving)
+  static constexpr int RING = kRing;
+  static constexpr size_t kRingBytes = (SA ? 3 : 2) * RING * (size_t)kStageBytes;
   // per buffer: bitmap u32[WORDS] | [serving words u32[K][threads]] | val T[K][threads] |
   //             word prefix u16[WORDS] | idx u16[K][threads]
   static constexpr size_t kBufBytes =
       WORDS * 6 + (size_t)K * kEncConsumers * (sizeof(T) + 2 + (PRE ? 4 : 0));
   static constexpr size_t kSmem = kRingBytes + NB * kBufBytes +
-                                  (kRing + NB) * sizeof(StageMeta) + NB * 8 +
-                                  (2 * kRing + 2 * NB) * 8 + NB * NCW * 4 + NB * 4 + 4 + 32;
+                                  (RING + NB) * sizeof(StageMeta) + NB * 8 +
+                                  (2 * RING + 2 * NB) * 8 + NB * NCW * 4 + NB * 4 + 4 + 32;
   static_assert(VPT >= 1 && VPT * 16 * kEncConsumers == kStageBytes, "stage split");
   static_assert(SUPER <= 65536, "u16 in-tile index");
   static_assert(WORDS % 128 == 0, "bitmap words per resolver lane in 16-byte loads");
@@ -221,6 +226,7 @@ struct PendingSlice {
   uint64_t base, rec, cap;
   uint32_t lt, nsub, cnt, seg;
   uint32_t mine;  // this thread's changes in the super-tile
+  uint32_t sa;    // applied by the streamed apply at staging
 };
 
 // serve[dst(i)] += v for a record of a segment with a local serving shard
@@ -284,15 +290,15 @@ __device__ __forceinline__ uint32_t tile_rank(const uint32_t* bm, const uint16_t
 // super-tile (warp-cooperative: record r of the warp is slot r - start(l)
 // of the lane l owning it), then the spilled ones, then clears its bitmap
 // words for the buffer's next super-tile.
-template <int DT, bool REMOTE>
+template <int DT, bool REMOTE, bool SA>
 __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSlice& ti,
                                             uint64_t prefix, uint32_t* bm, const uint16_t* wpre,
                                             const uint16_t* sidx,
                                             const typename Traits<DT>::T* sval,
                                             const uint32_t* spre, uint32_t* ovf,
-                                            const typename EncCfg<DT>::SpillRec* spill,
+                                            const typename EncCfg<DT, SA>::SpillRec* spill,
                                             const uint32_t* s_acks) {
-  using C = EncCfg<DT>;
+  using C = EncCfg<DT, SA>;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
   constexpr int VE = C::VE, K = C::K;
@@ -302,8 +308,9 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
   const uint64_t e0 = (uint64_t)ti.lt * SUPER;
   if (!(a.debug & 2) && prefix < ti.cap) {
     T* out_val = reinterpret_cast<T*>(a.out_val);
-    const FuseEntry* fz =
-        (a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg]) ? a.fuse + ti.seg : nullptr;
+    const FuseEntry* fz = (!ti.sa && a.fuse && a.fuse[ti.seg].mode && a.fuse_on[ti.seg])
+                              ? a.fuse + ti.seg
+                              : nullptr;
     // identity-mapped fused segments had their serving words fetched at staging
     const bool pre = C::PRE && fz && fz->mode == 1;
     // routes of this segment to other GPUs (bf16 engine, P2P): emitted here
@@ -419,9 +426,10 @@ __device__ __forceinline__ void flush_slice(const EncodeArgs& a, const PendingSl
         bm[(g * SUB + (v * kEncConsumers + threadIdx.x) * VE) >> 5] = 0;
 }
 
-template <int DT, bool REMOTE>
+template <int DT, bool REMOTE, bool SA>
 __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
-  using C = EncCfg<DT>;
+  using C = EncCfg<DT, SA>;
+  constexpr int kRing = C::RING;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
   constexpr int VE = C::VE, NCW = C::NCW, NB = C::NB, K = C::K;
@@ -431,6 +439,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring_prev = dsm;
   uint8_t* ring_next = dsm + kRing * kStageBytes;
+  uint8_t* ring_serve = dsm + 2 * kRing * kStageBytes;  // SA only
   uint8_t* bufs = dsm + C::kRingBytes;  // NB x kBufBytes
   auto buf_bm = [&](int b) { return reinterpret_cast<uint32_t*>(bufs + b * C::kBufBytes); };
   auto buf_pre = [&](int b) { return buf_bm(b) + WORDS; };  // K x threads words when PRE
@@ -470,6 +479,18 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
   __syncthreads();
   const T* prevT = reinterpret_cast<const T*>(a.prev);
   const T* nextT = reinterpret_cast<const T*>(a.next);
+  // streamed apply of a super-tile: its segment is fused with SA (fuse_on 2)
+  // through an identity route whose keep window holds the whole super-tile,
+  // and whose serving sub-tiles are 16-byte aligned; returns the serving
+  // element of in-tile index 0, or null
+  auto sa_dst = [&](uint32_t s, uint64_t e0, uint32_t cnt) -> T* {
+    if (!SA || !a.fuse || a.fuse_on[s] != 2u) return nullptr;
+    const FuseEntry* f = a.fuse + s;
+    if (f->mode != 1 || e0 < f->keep_lo || e0 + cnt > f->keep_hi || (cnt % VE)) return nullptr;
+    const int64_t off = (int64_t)f->dst_base + f->shift;
+    if (off & (VE - 1)) return nullptr;
+    return reinterpret_cast<T*>(a.serve) + off + e0;
+  };
 
   if (warp == NCW) {
     // ---------------- producer ----------------
@@ -521,6 +542,8 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         const uint32_t cnt = rem_n < SUPER ? (uint32_t)rem_n : SUPER;
         const uint32_t nsub = (cnt + SUB - 1) / SUB;
         const uint32_t last = (a.tile0 ? __ldg(a.tile0 + s + 1) : a.ntiles) == t + 1;
+        const uint32_t count_only = a.seg_mode ? __ldg(a.seg_mode + s) : 0u;
+        const T* sv = count_only ? nullptr : sa_dst((uint32_t)s, e0, cnt);
         for (uint32_t g = 0; g < nsub; ++g) {
           wait_empty(k);
           ebits ^= 1u << k;
@@ -532,10 +555,11 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
           m.nsub = nsub;
           m.cnt = cnt;
           m.last = last;
-          m.count_only = a.seg_mode ? __ldg(a.seg_mode + s) : 0u;
+          m.count_only = count_only;
+          m.sa = sv != nullptr;
           const uint32_t sub_cnt = min(SUB, cnt - g * SUB);
           const uint32_t bytes = (sub_cnt / VE) * 16u;
-          mbar_arrive_expect_tx(&full[k], 2 * bytes);
+          mbar_arrive_expect_tx(&full[k], (sv ? 3 : 2) * bytes);
           if (bytes) {
             const uint64_t el = sg.base + e0 + (uint64_t)g * SUB;
             if (WS_ENC_EVICT) {
@@ -545,6 +569,8 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
               tma_load_1d(ring_prev + k * kStageBytes, prevT + el, bytes, &full[k]);
               tma_load_1d(ring_next + k * kStageBytes, nextT + el, bytes, &full[k]);
             }
+            if (SA && sv)
+              tma_load_1d(ring_serve + k * kStageBytes, sv + (uint64_t)g * SUB, bytes, &full[k]);
           }
           k = (k + 1) % kRing;
         }
@@ -583,7 +609,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     }
     mbar_wait(&resolved[pb], (rbits >> pb) & 1u);
     rbits ^= 1u << pb;
-    flush_slice<DT, REMOTE>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
+    flush_slice<DT, REMOTE, SA>(a, p, s_prefix[pb], buf_bm(pb), buf_wpre(pb), buf_idx(pb), buf_val(pb),
                     buf_pre(pb), s_ovf + pb * NCW + warp,
                     spill_blk + ((size_t)pb * NCW + warp) * C::SPW, s_acks);
   };
@@ -605,7 +631,11 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     uint32_t mine = 0;  // this thread's changes in this super-tile
     const T* pf = nullptr;  // fused identity segment: serving element of in-tile index 0
     uint32_t pf_lo = 0, pf_n = 0;
-    if (C::PRE && a.fuse && a.fuse_on[ti.s]) {
+    T* sa_out = nullptr;  // streamed apply: serving element of in-tile index 0
+    if (SA && ti.sa) {
+      const FuseEntry* f = a.fuse + ti.s;
+      sa_out = reinterpret_cast<T*>(a.serve) + ((int64_t)f->dst_base + f->shift) + e0;
+    } else if (C::PRE && a.fuse && a.fuse_on[ti.s]) {
       const FuseEntry* f = a.fuse + ti.s;
       if (f->mode == 1) {
         pf = reinterpret_cast<const T*>(a.serve) + ((int64_t)f->dst_base + f->shift) + e0;
@@ -622,6 +652,7 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
       const uint32_t nvec = sub_cnt / VE;
       const uint4* P = reinterpret_cast<const uint4*>(ring_prev + kk * kStageBytes);
       const uint4* N = reinterpret_cast<const uint4*>(ring_next + kk * kStageBytes);
+      const uint4* S = reinterpret_cast<const uint4*>(ring_serve + kk * kStageBytes);
 #pragma unroll
       for (uint32_t v = 0; v < VPT; ++v) {
         const uint32_t j = v * kEncConsumers + tid;
@@ -647,6 +678,15 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
         if (ti.count_only) {
           mine += __popc(mv);
         } else if (mv) {
+          if (SA && sa_out) {  // the whole vector: unchanged lanes add 0 (u16 wrap)
+            const uint4 so = S[j];
+            uint4 o;
+            o.x = __vadd2(so.x, __vsub2(pb.x, pa.x));
+            o.y = __vadd2(so.y, __vsub2(pb.y, pa.y));
+            o.z = __vadd2(so.z, __vsub2(pb.z, pa.z));
+            o.w = __vadd2(so.w, __vsub2(pb.w, pa.w));
+            *reinterpret_cast<uint4*>(sa_out + g * SUB + j * VE) = o;
+          }
           const uint32_t li = g * SUB + j * VE;
           atomicOr(bm + (li >> 5), mv << (li & 31));
           const T* Pe = reinterpret_cast<const T*>(P) + (size_t)j * VE;
@@ -690,7 +730,8 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
     if (tid == 0) tinfo[b] = ti;  // for the resolver only
     __syncwarp();
     named_arrive(kStagedBar + b, kEncConsumers + 32);
-    const PendingSlice cur{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt, ti.nsub, ti.cnt, ti.s, mine};
+    const PendingSlice cur{ti.sg.base, ti.sg.rec, ti.sg.cap, ti.lt,  ti.nsub,
+                           ti.cnt,     ti.s,      mine,      ti.sa};
     if constexpr (NB == 3) {
       if (i >= 2) flush_tile((int)((i - 2) % NB), pend0, rbits, false);  // super-tile i-2
       pend0 = pend1;
@@ -982,14 +1023,17 @@ size_t encode_spill_bytes(int dtype, uint32_t blocks) {
 cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(encode_kernel<WS_BF16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)EncCfg<WS_BF16>::kSmem);
-    cudaFuncSetAttribute(encode_kernel<WS_BF16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)EncCfg<WS_BF16>::kSmem);
-    cudaFuncSetAttribute(encode_kernel<WS_I32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)EncCfg<WS_I32>::kSmem);
-    cudaFuncSetAttribute(encode_kernel<WS_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)EncCfg<WS_F32>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_BF16, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_BF16>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_BF16, true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_BF16>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_BF16, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)EncCfg<WS_BF16, true>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_I32, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_I32>::kSmem);
+    cudaFuncSetAttribute(encode_kernel<WS_F32, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_F32>::kSmem);
     attr_done = true;
   }
   // one persistent block per SM; the producer warp claims super-tiles in order
@@ -1007,12 +1051,21 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
   switch (dtype) {
     case WS_BF16:
       if (a2.remote.maps)
-        encode_kernel<WS_BF16, true><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
+        encode_kernel<WS_BF16, true, false>
+            <<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
+      else if (a2.serve_stream && a2.fuse && a2.serve)
+        encode_kernel<WS_BF16, false, true>
+            <<<grid, kEncodeBlock, EncCfg<WS_BF16, true>::kSmem, s>>>(a2);
       else
-        encode_kernel<WS_BF16, false><<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
+        encode_kernel<WS_BF16, false, false>
+            <<<grid, kEncodeBlock, EncCfg<WS_BF16>::kSmem, s>>>(a2);
       break;
-    case WS_I32: encode_kernel<WS_I32, false><<<grid, kEncodeBlock, EncCfg<WS_I32>::kSmem, s>>>(a2); break;
-    case WS_F32: encode_kernel<WS_F32, false><<<grid, kEncodeBlock, EncCfg<WS_F32>::kSmem, s>>>(a2); break;
+    case WS_I32:
+      encode_kernel<WS_I32, false, false><<<grid, kEncodeBlock, EncCfg<WS_I32>::kSmem, s>>>(a2);
+      break;
+    case WS_F32:
+      encode_kernel<WS_F32, false, false><<<grid, kEncodeBlock, EncCfg<WS_F32>::kSmem, s>>>(a2);
+      break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -76,10 +76,10 @@ __device__ __forceinline__ void warp_tile_records(const RouteSideArgs& a, const 
 }
 
 __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
-  __shared__ uint64_t s_carry;
+  __shared__ uint64_t s_carry, s_sa;
   __shared__ uint64_t s_warp[kWlThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = 0;
+  if (tid == 0) s_carry = s_sa = 0;
   __syncthreads();
   for (int base = 0; base < a.nentries; base += kWlThreads) {
     const int e = base + tid;
@@ -88,8 +88,16 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
       // Next sync: fuse the apply into K1 only for segments that stayed well
       // below the dense threshold; the others skip the scattered
       // read-modify-writes of records a dense copy would overwrite anyway.
+      // With K1's streamed apply (fuse_on = 2) the serving tile is read
+      // sequentially, which beats the per-record RMW from 1/sa_div up to the
+      // dense threshold.
       const int s = a.entries[e].seg;
-      a.fuse_on[s] = a.seg_nnz[s] * kStreamDiv <= a.segs[s].n ? 1u : 0u;
+      const uint64_t nz = a.seg_nnz[s], n = a.segs[s].n;
+      const uint32_t on = (a.sa_div && nz * a.sa_div >= n && nz <= a.seg_cap[s]) ? 2u
+                          : nz * kStreamDiv <= n                                   ? 1u
+                                                                                   : 0u;
+      a.fuse_on[s] = on;
+      if (on == 2u) atomicAdd(reinterpret_cast<unsigned long long*>(&s_sa), n);
     }
     uint64_t inc = u;
 #pragma unroll
@@ -115,7 +123,11 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
     if (tid == kWlThreads - 1) s_carry = excl + u;
     __syncthreads();
   }
-  if (tid == 0) a.unit_off[a.nentries] = s_carry;
+  if (tid == 0) {
+    a.unit_off[a.nentries] = s_carry;
+    // the host picks K1's instantiation for the next sync from this word
+    if (a.fused && a.sa_elems) *reinterpret_cast<volatile uint64_t*>(a.sa_elems) = s_sa;
+  }
 }
 
 __device__ __forceinline__ int find_entry(const uint64_t* off, int n, uint64_t u) {

@@ -248,3 +248,38 @@ def test_predicted_dense_segments_fixup(restatement, first):
             assert bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
             total += want_i.size
         assert rep["nnz"] == total
+
+
+@pytest.mark.parametrize("density", [0.006, 0.03, 0.15])
+def test_streamed_apply_adds_delta(density):
+    """K1's streamed apply (fuse_on = 2): from the second sync
+    on, fused segments denser than 1/sa_div get serve + (next - prev) stored
+    per changed 16-byte vector.  The serving shards are perturbed first, so
+    overwriting with `next` (or touching unchanged lanes) would fail: the
+    result must be the reference's in-place add (codec.cpp:80-91), or `next`
+    for segments that went dense."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.MODELS["qwen2.5-0.5b"]([0, 1]))
+    eng.generate(seed=7, density=density)
+    eng.sync_step()
+    eng.sync_step(reverse=True)  # fuse_on now reflects this density
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    before = []
+    for i in range(len(plan.segments)):
+        v = eng.serve_view(i).view(torch.int16)
+        flip = torch.randint(0, 2, v.shape, device=v.device, generator=gen, dtype=torch.int16)
+        v.bitwise_xor_(flip * 0x0101)
+        before.append(v.to(torch.int32) & 0xFFFF)
+    rep = eng.sync_step()
+    torch.cuda.synchronize()
+    dense = 0
+    for i in range(len(plan.segments)):
+        p = eng.segment_view(i, 0).view(torch.int16).to(torch.int32) & 0xFFFF
+        q = eng.segment_view(i, 1).view(torch.int16).to(torch.int32) & 0xFFFF
+        got = eng.serve_view(i).view(torch.int16).to(torch.int32) & 0xFFFF
+        if eng.segment_delta(i)[1] == "D":
+            dense += 1
+            assert torch.equal(got, q), i
+        else:
+            assert torch.equal(got, (before[i] + q - p) & 0xFFFF), i
+    assert rep["dense_shards"] == dense
