@@ -121,10 +121,14 @@ struct ws_engine {
   wsync::FuseEntry* d_fuse_ = nullptr;
   uint32_t* d_fuse_on_ = nullptr;
   uint32_t sa_div_ = 0;  // K1 streamed apply for fused bf16 segments denser than 1/sa_div_ (0: off)
-  uint64_t* h_sa_ = nullptr;  // mapped: elements set to stream by the last worklist
+  uint64_t* h_sa_ = nullptr;  // mapped [2]: fused elements set to stream / RMW by the last worklist
   uint64_t* d_sa_ = nullptr;
-  uint64_t sa_total_ = 0;     // elements of this rank's segments
   bool sa_force_ = false;     // ablation: always the streamed-apply instantiation
+  bool sa_env_ = false;       // WSYNC_SA_DIV given explicitly
+  // Off by default under overlapped exchange rounds (N >= 4): the serving
+  // stream then competes with the receive scatter for HBM (measured: 3.77 ->
+  // 3.92 ms at N = 4).
+  uint32_t sa_div() const { return (sa_env_ || exchange_rounds() <= 1) ? sa_div_ : 0u; }
   bool fuse_apply_ = true;  // K1 applies local sparse records (WSYNC_NO_FUSED_APPLY=1 disables)
   int nlocal_ = 0;
   uint64_t* d_unit_off_ = nullptr;

@@ -155,14 +155,15 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
                          cudaMemcpyHostToDevice), "H2D");
   if (const char* f = getenv("WSYNC_NO_FUSED_APPLY")) fuse_apply_ = atoi(f) == 0;
   sa_div_ = dtype_ == WS_BF16 ? 250u : 0u;  // K1 streamed apply from 0.4% density
-  if (const char* f = getenv("WSYNC_SA_DIV")) sa_div_ = dtype_ == WS_BF16 ? (uint32_t)atoi(f) : 0u;
+  if (const char* f = getenv("WSYNC_SA_DIV")) {
+    sa_div_ = dtype_ == WS_BF16 ? (uint32_t)atoi(f) : 0u;
+    sa_env_ = true;
+  }
   if (sa_div_) {
-    WS_CUDA_TRY(cudaHostAlloc(&h_sa_, 8, cudaHostAllocMapped), "cudaHostAlloc");
-    *h_sa_ = 0;
+    WS_CUDA_TRY(cudaHostAlloc(&h_sa_, 16, cudaHostAllocMapped), "cudaHostAlloc");
+    h_sa_[0] = h_sa_[1] = 0;
     WS_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sa_), h_sa_, 0), "mapped");
     if (const char* f = getenv("WSYNC_SA_FORCE")) sa_force_ = atoi(f) != 0;
-    sa_total_ = 0;
-    for (int i = 0; i < nseg_; ++i) sa_total_ += segs[i].n;
   }
   WS_CUDA_TRY(cudaMalloc(&d_local_, std::max<size_t>(1, local.size()) * sizeof(LocalEntry)),
               "cudaMalloc");
@@ -288,13 +289,12 @@ EncodeArgs ws_engine::encode_args(int pa, int na) {
     a.fuse = d_fuse_;
     a.fuse_on = d_fuse_on_;
     a.serve = serve;
-    // the streamed-apply instantiation when most elements stream (from the
-    // last sync whose worklist has run; a stale answer only costs speed --
-    // either instantiation is exact for any fuse_on)
-    a.serve_stream = (sa_div_ && (sa_force_ || 2 * *reinterpret_cast<volatile uint64_t*>(h_sa_) >=
-                                                   sa_total_))
-                         ? 1
-                         : 0;
+    // the streamed-apply instantiation when more fused elements stream than
+    // take the per-record RMW (from the last sync whose worklist has run; a
+    // stale answer only costs speed -- either instantiation is exact for any
+    // fuse_on)
+    const volatile uint64_t* sa = h_sa_;
+    a.serve_stream = (sa_div() && (sa_force_ || (sa[0] && sa[0] >= sa[1]))) ? 1 : 0;
   }
   a.nseg = nseg_;
   a.ntiles = ntiles_;
@@ -349,7 +349,7 @@ ws_status ws_engine::local_route(const ws_sync_options& o, int pa, int na, cudaS
   r.unit_off = d_unit_off_;
   r.fused = (fuse_apply_ && o.sparse && ntiles_) ? 1 : 0;
   r.fuse_on = d_fuse_on_;
-  r.sa_div = sa_div_;
+  r.sa_div = sa_div();
   r.sa_elems = d_sa_;
   WS_CUDA_TRY(launch_local_route(dtype_, r, route_grid_, s), "local route");
   if (nlocal_) *launches += 2;

@@ -76,10 +76,10 @@ __device__ __forceinline__ void warp_tile_records(const RouteSideArgs& a, const 
 }
 
 __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
-  __shared__ uint64_t s_carry, s_sa;
+  __shared__ uint64_t s_carry, s_sa[2];
   __shared__ uint64_t s_warp[kWlThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = s_sa = 0;
+  if (tid == 0) s_carry = s_sa[0] = s_sa[1] = 0;
   __syncthreads();
   for (int base = 0; base < a.nentries; base += kWlThreads) {
     const int e = base + tid;
@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
                           : nz * kStreamDiv <= n                                   ? 1u
                                                                                    : 0u;
       a.fuse_on[s] = on;
-      if (on == 2u) atomicAdd(reinterpret_cast<unsigned long long*>(&s_sa), n);
+      if (on && a.sa_elems)  // fused elements: [0] streamed, [1] per-record RMW
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sa[on == 2u ? 0 : 1]), n);
     }
     uint64_t inc = u;
 #pragma unroll
@@ -126,7 +127,10 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
   if (tid == 0) {
     a.unit_off[a.nentries] = s_carry;
     // the host picks K1's instantiation for the next sync from this word
-    if (a.fused && a.sa_elems) *reinterpret_cast<volatile uint64_t*>(a.sa_elems) = s_sa;
+    if (a.fused && a.sa_elems) {
+      reinterpret_cast<volatile uint64_t*>(a.sa_elems)[0] = s_sa[0];
+      reinterpret_cast<volatile uint64_t*>(a.sa_elems)[1] = s_sa[1];
+    }
   }
 }
 

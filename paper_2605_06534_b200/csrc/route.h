@@ -51,7 +51,7 @@ struct RouteSideArgs {
   const SegDev* segs;           // segment sizes
   int32_t stream_apply;         // local routes: dense-ish sparse segments apply by streaming
   uint32_t sa_div;              // K1 streamed apply: fuse_on = 2 for density in [1/sa_div, cap] (0: off)
-  uint64_t* sa_elems;           // mapped host word: elements of the segments set to fuse_on = 2
+  uint64_t* sa_elems;           // mapped host words: fused elements set to stream / to per-record RMW
   int32_t k1_emitted;           // pack: K1 already stored the sparse records remotely
   const void* train_prev;
   const void* train_next;
