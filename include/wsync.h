@@ -408,14 +408,16 @@ typedef struct ws_relay_report { /* TransferReport (engine.hpp:34-42) */
   uint32_t dense_shards, sparse_shards;
 } ws_relay_report;
 
-/* TransferEngine::sync_step across clusters (engine.cpp:66-254) with this
- * GPU as both sides: the pusher encodes on the GPU (K1 + payloads) and puts
- * every shard's buckets (BucketKey keys, bucket_bytes) through pinned
- * double-buffered staging; the puller fetches the buckets of every source of
- * its serving shards (plan_pulls; codec probed from the first key as
- * engine.cpp:164-171), stages them to the GPU, decodes, reslices and applies
- * there.  Async runs both sides concurrently, Batch pushes first.  world ==
- * 1 plans only. */
+/* TransferEngine::sync_step across clusters (engine.cpp:66-254), one call
+ * per rank: this rank's pusher encodes on the GPU (K1 + payloads) and puts
+ * its trainer shards' buckets (BucketKey keys, bucket_bytes) through pinned
+ * double-buffered staging; its puller (one per serving rank, as
+ * engine.cpp:233-238) fetches the buckets of every trainer shard of any rank
+ * routed to its serving coordinate (plan_pulls; codec probed from the first
+ * key as engine.cpp:164-171), stages them to the GPU, decodes, reslices and
+ * applies there.  Async runs both sides concurrently, Batch pushes first.
+ * With world > 1 every rank calls it for the same step on a relay the ranks
+ * share; the NVLink exchange is not used. */
 ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step, const ws_sync_options* opts,
                                const ws_relay_options* relay_opts, const ws_relay* relay,
                                ws_relay_report* report);

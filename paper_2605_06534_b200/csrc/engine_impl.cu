@@ -373,7 +373,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
   last_stream_ = s;
 
   WS_CUDA_TRY(cudaEventRecord(ev_[0], s), "event");
-  if (plan_.world() > 1) {
+  if (plan_.world() > 1 && !encode_only_) {  // (the relay path exchanges nothing here)
     st = exchange_begin(s, &launches);
     if (st != WS_OK) return st;
   }
@@ -396,7 +396,7 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
       WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
       if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
       EncodeArgs a = encode_args(pa, na);
-      if (plan_.world() > 1) {
+      if (plan_.world() > 1 && !encode_only_) {
         st = exchange_fuse_k1(a, s);
         if (st != WS_OK) return st;
       }

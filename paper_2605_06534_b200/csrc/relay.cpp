@@ -6,13 +6,15 @@
 //   pusher  K1 (encode only) -> per shard: device payload -> bucket D2H into
 //           pinned staging on a copy stream, bucket k+1 in flight while bucket
 //           k is paced (TokenBucket, relay.cpp:69-84) and put;
-//   puller  per source of every serving shard (plan_pulls): probe the codec
+//   puller  (one per serving rank) per source, on any rank, of every
+//           serving shard of this rank's coordinate (plan_pulls): probe the codec
 //           with get_any over the D0/S4/S8 keys (engine.cpp:164-171), fetch
 //           the remaining buckets, stage the payload to the GPU, decode,
 //           reslice and apply (or copy the dense overlap) there.
 //   modes   Async runs both sides concurrently, Batch pushes first
 //           (engine.cpp:231-238).
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -108,8 +110,6 @@ struct RelayError {
 ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
                                 const ws_relay_options& ro, const ws_relay& relay,
                                 ws_relay_report* rep) {
-  if (plan_.world() != 1)
-    return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: single-GPU plans only");
   if (!relay.put || !relay.get_any)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: relay callbacks missing");
   if (ro.bucket_bytes == 0) return set_error(WS_INVALID_ARGUMENT, "bucket_bytes must be > 0");
@@ -159,17 +159,34 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   }
   rep->encode_s = secs(wall0, Clock::now());
 
-  // sizes: the largest payload (dense bound) and record count of a segment
+  // What this rank pulls: every trainer shard, of any rank, with a route to
+  // its serving coordinate (plan_pulls, one puller per serving rank as
+  // engine.cpp:233-238; replicas of a coordinate pull independently).
   const auto& segs = plan_.segments();
+  struct Pull {
+    const Segment* src;
+    const Route* route;
+  };
+  std::vector<Pull> pulls;
+  const int my_coord = plan_.my_coord();
+  for (int g = 0; g < plan_.world(); ++g)
+    for (const Route& r : plan_.routes_of(g))
+      if (r.coord == my_coord) pulls.push_back(Pull{&plan_.segments_of(g)[r.seg], &r});
+  // sizes: the largest payload (dense bound) and record count of a shard
+  // pushed or pulled here (a sparse payload holds at most threshold x n + 1)
   uint64_t max_payload = 64, max_n = 1, max_cap = 1;
-  for (size_t i = 0; i < segs.size(); ++i) {
-    const int nd = (int)plan_.manifest()[segs[i].shard.param].shape.size();
+  auto size_for = [&](const Segment& sg) {
+    const int nd = (int)plan_.manifest()[sg.shard.param].shape.size();
+    const uint64_t cap = std::min<uint64_t>(
+        sg.n, (uint64_t)std::floor(std::max(0.0, o.density_threshold) * (double)sg.n) + 1);
     max_payload = std::max<uint64_t>(
-        max_payload, std::max(ws_payload_bytes((ws_dtype)dtype_, nd, 'D', 0, segs[i].n),
-                              ws_payload_bytes((ws_dtype)dtype_, nd, 'S', 8, segs_[i].cap)));
-    max_n = std::max<uint64_t>(max_n, segs[i].n);
-    max_cap = std::max<uint64_t>(max_cap, segs_[i].cap);
-  }
+        max_payload, std::max(ws_payload_bytes((ws_dtype)dtype_, nd, 'D', 0, sg.n),
+                              ws_payload_bytes((ws_dtype)dtype_, nd, 'S', 8, cap)));
+    max_n = std::max<uint64_t>(max_n, sg.n);
+    max_cap = std::max<uint64_t>(max_cap, cap);
+  };
+  for (const Segment& sg : segs) size_for(sg);
+  for (const Pull& pl : pulls) size_for(*pl.src);
   const uint64_t B = ro.bucket_bytes;
 
   Pacer push_pacer(ro.push_bytes_per_s, ro.burst_bytes > 0 ? ro.burst_bytes : (double)B);
@@ -242,9 +259,10 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   auto puller = [&] {
     const auto t0 = Clock::now();
     double apply_acc = 0;
-    for (const Route& r : plan_.routes()) {
+    for (const Pull& pl : pulls) {
       if (first_err.st != WS_OK) return;
-      const Segment& src = segs[r.seg];
+      const Route& r = *pl.route;
+      const Segment& src = *pl.src;
       const ParamMeta& p = plan_.manifest()[src.shard.param];
       std::string cand[3] = {key_of(step, p.name, src.shard, 'D', 0, 0),
                              key_of(step, p.name, src.shard, 'S', 4, 0),

@@ -11,11 +11,19 @@ Every rank checks its own serving shards after each sync:
   * I32 and F32 with the reference's own layouts (TrainConfig{N,1,1} ->
     ServeConfig{N,1}): serving == the compiled reference engine's serving
     shards (oracle/_ref, run on the same weights on the host).
+  * the relay path (ws_engine_sync_relay) with one pusher and one puller
+    per rank through a relay shared by the processes (a directory): serving
+    == `next`, then a reverse sync through a fresh relay == `prev`.
 Prints one JSON line per rank; exits non-zero on any mismatch.
 """
+import ctypes as C
+import hashlib
 import json
 import os
+import shutil
 import sys
+import tempfile
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -36,6 +44,73 @@ def serve_equals_gen(eng, plan, seed, density, which, tabs=None):
         if not torch.equal(eng.serve_view(i).view(torch.int16), want):
             bad.append(meta.name)
     return bad
+
+
+class DirRelay:
+    """A relay the ranks share through a directory (test infrastructure): put
+    writes the bucket to a file named by the key's hash and renames it into
+    place; get_any polls the candidate keys until one exists, as
+    MemoryRelay::get_any waits on its condition variable (relay.cpp:29-45)."""
+    PUT = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64)
+    GET = C.CFUNCTYPE(C.c_int64, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_int,
+                      C.c_int, C.POINTER(C.c_int), C.c_void_p, C.c_uint64)
+
+    def __init__(self, path):
+        self.path = path
+        self._put, self._get = self.PUT(self.put), self.GET(self.get_any)
+        self.callbacks = (None, C.cast(self._put, C.c_void_p).value,
+                          C.cast(self._get, C.c_void_p).value)
+
+    def _file(self, key):
+        return os.path.join(self.path, hashlib.sha1(key).hexdigest())
+
+    def put(self, ctx, key, klen, data, n):
+        f = self._file(C.string_at(key, klen))
+        with open(f + ".tmp", "wb") as fh:
+            fh.write(C.string_at(data, n) if n else b"")
+        os.rename(f + ".tmp", f)
+        return 0
+
+    def get_any(self, ctx, keys, lens, n, timeout_ms, hit, out, cap):
+        files = [self._file(C.string_at(keys[i], lens[i])) for i in range(n)]
+        end = time.time() + timeout_ms / 1e3
+        while True:
+            for i, f in enumerate(files):
+                if os.path.exists(f):
+                    with open(f, "rb") as fh:
+                        b = fh.read()
+                    hit[0] = i
+                    if len(b) <= cap:
+                        C.memmove(out, b, len(b))
+                    return len(b)
+            if time.time() > end:
+                return -1
+            time.sleep(0.001)
+
+
+def relay_case(rank, world, uid_fn, manifest, density, seed, mode):
+    """ws_engine_sync_relay on every rank at once (FSDP-N -> TP2 x N/2):
+    each rank pushes its trainer shards and pulls every shard routed to its
+    serving coordinate (engine.cpp:109-238, one puller per serving rank)."""
+    tp = 1 if world == 1 else 2
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+                   world=world, rank=rank)
+    eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
+    eng.generate(seed=seed, density=density)
+    obj = [tempfile.mkdtemp(prefix="wsync_relay_") if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    bad = []
+    for step, (rev, which) in enumerate(((False, "next"), (True, "prev")), start=1):
+        relay = DirRelay(obj[0])
+        dist.barrier()
+        rep = eng.sync_relay(relay.callbacks, step=step, mode=mode, reverse=rev,
+                             bucket_bytes=8 << 20, timeout_ms=60000)
+        torch.cuda.synchronize()
+        bad += [f"step{step}:{b}" for b in serve_equals_gen(eng, plan, seed, density, which)]
+        dist.barrier()
+    if rank == 0:
+        shutil.rmtree(obj[0], ignore_errors=True)
+    return bad, rep
 
 
 def bf16_case(rank, world, uid_fn, manifest, density, seed):
@@ -169,6 +244,12 @@ def main():
         for density, sparse in ((0.05, True), (0.45, True), (0.05, False)):
             bad = ref_case(rank, world, uid, dtype, density, sparse)
             results[f"ref dtype={dtype} d={density} sparse={sparse}"] = bad or "ok"
+            ok &= not bad
+    if world > 1:
+        for density, mode in ((0.01, "async"), (0.45, "batch")):
+            bad, rep = relay_case(rank, world, uid, ws.MODELS["qwen2.5-0.5b"]([0, 23]), density, 6,
+                                  mode)
+            results[f"relay {mode} d={density}"] = bad or (rep["pull_buckets"], rep["push_buckets"])
             ok &= not bad
     # rank 0 prints every rank's line (concurrent writers can interleave)
     allres = [None] * world
