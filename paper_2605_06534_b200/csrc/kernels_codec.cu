@@ -74,7 +74,7 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
 //                bitmap -- no warp-level communication per vector.  Each
 //                stage is released as soon as it is read, so HBM streams
 //                continuously;
-//   warps 17-19  resolvers (one per staging buffer): popcount-scan the
+//   warps 17..   resolvers (one per staging buffer): popcount-scan the
 //                bitmap (the ascending rank of every change inside its
 //                super-tile) and place the super-tile in its segment's
 //                stream: one atomic reservation (the engine: super-tiles in
@@ -82,7 +82,9 @@ __device__ __forceinline__ unsigned long long block_scan_packed(unsigned long lo
 //                look-back (ws_diff_shards: one ascending stream);
 //   each consumer warp writes its staged records of super-tile i to
 //   base + rank after staging super-tile i + NB - 1, applying them in place
-//   to a serving shard on this GPU when the engine asks for the fused apply.
+//   to a serving shard on this GPU when the engine asks for the fused apply;
+//   SA (streamed apply): the producer also streams the serving sub-tile, and
+//   consumers store serve + (next - prev) per changed vector at staging.
 // A thread with more than SLOTS changes in one super-tile re-derives the
 // rest from global memory at write-out; the bitmap still gives their ranks.
 constexpr int kStagedBar = 2;  // named barriers 2.. : "super-tile staged in buffer b"
