@@ -240,6 +240,14 @@ def main():
         results[name] = bad or "ok"
         results[name + " shards dense/sparse"] = (rep["dense_shards"], rep["sparse_shards"])
         ok &= not bad
+    # replica fan-out: FSDP-N -> TP1 x N replicas, every record to all N
+    # serving ranks (the N = 8 bench layout sends to 4 replicas)
+    if world > 1:
+        for density in (0.01, 0.45):
+            bad, rep = layout_case(rank, world, uid, ws.MODELS["qwen2.5-0.5b"]([0, 23]),
+                                   ws.TrainConfig("fsdp"), ws.ServeConfig(1, 1, world), density, 7)
+            results[f"fan-out tp1x{world} d={density}"] = bad or "ok"
+            ok &= not bad
     for dtype in (ws.I32, ws.F32):
         for density, sparse in ((0.05, True), (0.45, True), (0.05, False)):
             bad = ref_case(rank, world, uid, dtype, density, sparse)
