@@ -206,8 +206,10 @@ class TransferEngine:
                    force_wide_index=False, staging_buffers=2):
         """TransferEngine::sync_step across clusters (engine.cpp:66-254): this
         GPU pushes its trainer shards through `relay` -- a (ctx, put, get_any)
-        triple of C pointers implementing ws_relay -- and pulls them into its
-        serving shards; mode "async" or "batch" (SyncMode)."""
+        triple of C pointers implementing ws_relay -- and pulls every shard
+        routed to its serving coordinate, from any rank; mode "async" or
+        "batch" (SyncMode).  With world > 1 every rank calls it for the same
+        step on a relay the ranks share."""
         o = _lib.SyncOptions(int(sparse), density_threshold, int(reverse))
         ro = _lib.RelayOptions(bucket_bytes, 256 << 20, push_bytes_per_s, pull_bytes_per_s,
                                burst_bytes, timeout_ms, int(mode == "async"),
