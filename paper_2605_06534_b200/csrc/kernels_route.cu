@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
       // dense threshold.
       const int s = a.entries[e].seg;
       const uint64_t nz = a.seg_nnz[s], n = a.segs[s].n;
-      const uint32_t on = (a.sa_div && nz * a.sa_div >= n && nz <= a.seg_cap[s]) ? 2u
-                          : nz * kStreamDiv <= n                                   ? 1u
-                                                                                   : 0u;
+      // (only identity routes can stream the serving tile)
+      const bool stream =
+          a.sa_div && a.entries[e].identity && nz * a.sa_div >= n && nz <= a.seg_cap[s];
+      const uint32_t on = stream ? 2u : (nz * kStreamDiv <= n ? 1u : 0u);
       a.fuse_on[s] = on;
       if (on && a.sa_elems)  // fused elements: [0] streamed, [1] per-record RMW
         atomicAdd(reinterpret_cast<unsigned long long*>(&s_sa[on == 2u ? 0 : 1]), n);
