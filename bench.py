@@ -135,7 +135,7 @@ class ClockSampler:
 # The reference's CPU path (oracle/_ref, the unmodified transfer engine)
 # ---------------------------------------------------------------------------
 
-def cpu_reference(args, threads=None, reps=1):
+def cpu_reference(args, threads=None, reps=1, warmup=0):
     """Times TransferEngine::sync_step of the compiled reference on a bounded
     sample of the same workload: one Qwen layer (no embedding) per thread, I32
     weights of identical element counts (the reference has no bf16; I32 is the
@@ -171,12 +171,13 @@ def cpu_reference(args, threads=None, reps=1):
         states = list(ex.map(make, range(t)))
     elems = sum(st.model_bytes() / 4 for st in states)
     walls = []
-    for _ in range(reps):
+    for it in range(warmup + reps):
         t0 = time.perf_counter()
         with ThreadPoolExecutor(t) as ex:
             reps_ = list(ex.map(lambda st: st.run(True, True, True, args.threshold, 64 << 20),
                                 states))
-        walls.append(time.perf_counter() - t0)
+        if it >= warmup:  # untimed warm-up reps first
+            walls.append(time.perf_counter() - t0)
     wall = statistics.median(walls)
     gbs = elems * 2 / wall / 1e9
     return {"value": gbs, "unit": "GB/s", "cores": t, "kind": "reference",
@@ -193,11 +194,13 @@ def run_reference_arm(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    reps = max(1, min(args.steps, 3))
-    cb = cpu_reference(args, reps=reps)
+    # bounded: at most 3 timed reps and 1 warm-up rep of the CPU sample, so the
+    # arm ends within minutes
+    reps, warm = max(1, min(args.steps, 3)), min(max(args.warmup, 0), 1)
+    cb = cpu_reference(args, reps=reps, warmup=warm)
     tp, rep_ = layouts(args.gpus)
     line = {"metric": METRIC, "value": round(cb["value"], 4), "unit": "GB/s",
-            "n_gpus": args.gpus, "steps": reps, "warmup": 0,
+            "n_gpus": args.gpus, "steps": reps, "warmup": warm,
             "ms_per_step": round(cb["wall_s"] * 1e3 * (8.19e9 / max(cb["elems"], 1)), 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i32",
             "data": "synthetic", "impl": "reference",
