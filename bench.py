@@ -161,9 +161,12 @@ def cpu_reference(args, threads=None, reps=1, warmup=0):
     t = max(1, min(t, nproc, int(avail * 0.5 // per)))
     states = []
 
+    # middle layers only (layer 0 and the last carry the embedding / lm_head)
+    mid = max(1, max(p.layer for p in mf.MODELS[args.model]()) - 1)
+
     def make(i):
         layers = [1 + i * args.cpu_sample_layers + k for k in range(args.cpu_sample_layers)]
-        layers = [1 + (l - 1) % 34 for l in layers]
+        layers = [1 + (l - 1) % mid for l in layers]
         m = [p.as_tuple() for p in mf.MODELS[args.model](layer_subset=layers)]
         return ref.state(m, I32, (1, 1, 1), (1, 1), args.density, args.seed + i)
 
