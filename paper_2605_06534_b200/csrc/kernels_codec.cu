@@ -249,7 +249,7 @@ __device__ __forceinline__ typename Traits<DT>::T* fuse_target(const FuseEntry* 
 }
 
 #ifndef WS_FLUSH_BATCH
-#define WS_FLUSH_BATCH 2
+#define WS_FLUSH_BATCH 1
 #endif
 
 // Fused remote emission (bf16): the record (segment-local i, value v) of a
