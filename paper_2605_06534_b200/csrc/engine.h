@@ -26,10 +26,19 @@ struct ws_engine {
                           char* codec);
   ws_status timing(int reset, ws_timing* out);
   ws_status payload(int i, bool wide, void* out_dev, ws_payload_info* info, cudaStream_t s);
+  // payload of segment i from its ascending stream (idx, val, nnz, codec);
+  // out_dev == null: sizes only.  Synchronises stream s only.
+  ws_status payload_from(int i, bool wide, const uint32_t* idx, const void* val, uint64_t nnz,
+                         char codec, void* out_dev, ws_payload_info* info, cudaStream_t s);
+  // segment i's ascending record stream into (out_idx, out_val), on stream s
+  ws_status compact_segment(int i, uint32_t* out_idx, void* out_val, cudaStream_t s);
   // cross-cluster sync through a relay (relay.cpp)
   ws_status sync_relay(uint64_t step, const ws_sync_options& o, const ws_relay_options& ro,
                        const ws_relay& relay, ws_relay_report* rep);
   bool encode_only_ = false;  // sync_step: K1 only (no fused apply, no routes)
+  // sync_relay's staging (device / pinned host) and streams, kept across calls
+  std::vector<std::pair<void*, size_t>> relay_dev_, relay_host_;
+  cudaStream_t relay_streams_[3] = {nullptr, nullptr, nullptr};
 
   // caller-owned arenas (ws_engine_bind)
   void* arena[2] = {nullptr, nullptr};

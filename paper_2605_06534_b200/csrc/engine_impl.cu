@@ -48,6 +48,10 @@ ws_engine::~ws_engine() {
   cudaFree(d_unit_off_);
   if (h_nnz_pinned_) cudaFreeHost(h_nnz_pinned_);
   if (h_sa_) cudaFreeHost(h_sa_);
+  for (auto& e : relay_dev_) cudaFree(e.first);
+  for (auto& e : relay_host_) cudaFreeHost(e.first);
+  for (cudaStream_t st : relay_streams_)
+    if (st) cudaStreamDestroy(st);
   if (ring_) {
     for (int i = 0; i < kRing; ++i)
       for (auto& e : ring_[i])
@@ -511,6 +515,22 @@ ws_status ws_engine::payload(int i, bool wide, void* out_dev, ws_payload_info* i
   char codec = 'D';
   ws_status st = segment_delta(i, &idx, &val, &nnz, &codec);  // ascending stream
   if (st != WS_OK) return st;
+  return payload_from(i, wide, idx, val, nnz, codec, out_dev, info, s);
+}
+
+ws_status ws_engine::compact_segment(int i, uint32_t* out_idx, void* out_val, cudaStream_t s) {
+  const size_t esz = dtype_size(dtype_);
+  const uint32_t t0 = plan_tile0_[i], nt = plan_tile0_[i + 1] - t0;
+  WS_CUDA_TRY(launch_compact(dtype_, d_tile_cnt_ + t0, d_tile_base_ + t0, nt, segs_[i].cap,
+                             d_idx_ + segs_[i].rec, (const char*)d_val_ + segs_[i].rec * esz,
+                             out_idx, out_val, s),
+              "compact");
+  return WS_OK;
+}
+
+ws_status ws_engine::payload_from(int i, bool wide, const uint32_t* idx, const void* val,
+                                  uint64_t nnz, char codec, void* out_dev,
+                                  ws_payload_info* info, cudaStream_t s) {
   const Segment& sg = plan_.segments()[i];
   const ParamMeta& p = plan_.manifest()[sg.shard.param];
   int64_t shape[8];
@@ -531,6 +551,7 @@ ws_status ws_engine::payload(int i, bool wide, void* out_dev, ws_payload_info* i
                                        codec == 'S' ? nnz : sg.n);
   if (!out_dev) return WS_OK;
   const ws_stream_t ss = reinterpret_cast<ws_stream_t>(s);
+  ws_status st;
   if (codec == 'S')
     st = ws_encode_sparse_dev((ws_dtype)dtype_, shape, nd, iw, idx, val, nnz, out_dev, ss);
   else

@@ -17,6 +17,8 @@
 #include <cmath>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -117,29 +119,36 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   const int esz = dtype_size(dtype_);
   const int depth = std::max(2, ro.staging_buffers);
   const int timeout = ro.timeout_ms > 0 ? ro.timeout_ms : 10000;
-  cudaStream_t s_enc = nullptr, s_push = nullptr, s_pull = nullptr;
-  cudaStreamCreateWithFlags(&s_enc, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&s_push, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&s_pull, cudaStreamNonBlocking);
-  std::vector<void*> host_bufs, dev_bufs;
-  auto cleanup = [&] {
-    for (void* p : host_bufs) cudaFreeHost(p);
-    for (void* p : dev_bufs) cudaFree(p);
-    cudaStreamDestroy(s_enc);
-    cudaStreamDestroy(s_push);
-    cudaStreamDestroy(s_pull);
-  };
+  // streams and staging live in the engine across calls: pinning and
+  // allocating hundreds of MB per sync would dominate it
+  for (cudaStream_t& st : relay_streams_)
+    if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaStream_t s_enc = relay_streams_[0], s_push = relay_streams_[1], s_pull = relay_streams_[2];
+  auto cleanup = [] {};
+  size_t dslot = 0, hslot = 0;  // the same allocation order every call
   auto dev_alloc = [&](size_t bytes) -> void* {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(16, bytes)) != cudaSuccess) return nullptr;
-    dev_bufs.push_back(p);
-    return p;
+    bytes = std::max<size_t>(16, bytes);
+    if (dslot == relay_dev_.size()) relay_dev_.push_back({nullptr, 0});
+    auto& e = relay_dev_[dslot++];
+    if (e.second < bytes) {
+      cudaFree(e.first);
+      e = {nullptr, 0};
+      if (cudaMalloc(&e.first, bytes) != cudaSuccess) return nullptr;
+      e.second = bytes;
+    }
+    return e.first;
   };
   auto host_alloc = [&](size_t bytes) -> uint8_t* {
-    void* p = nullptr;
-    if (cudaMallocHost(&p, std::max<size_t>(16, bytes)) != cudaSuccess) return nullptr;
-    host_bufs.push_back(p);
-    return static_cast<uint8_t*>(p);
+    bytes = std::max<size_t>(16, bytes);
+    if (hslot == relay_host_.size()) relay_host_.push_back({nullptr, 0});
+    auto& e = relay_host_[hslot++];
+    if (e.second < bytes) {
+      cudaFreeHost(e.first);
+      e = {nullptr, 0};
+      if (cudaMallocHost(&e.first, bytes) != cudaSuccess) return nullptr;
+      e.second = bytes;
+    }
+    return static_cast<uint8_t*>(e.first);
   };
 
   std::memset(rep, 0, sizeof(*rep));
@@ -158,6 +167,12 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
     return set_error(WS_CUDA, "sync_relay: encode");
   }
   rep->encode_s = secs(wall0, Clock::now());
+  // per-shard counts once (the pusher then never synchronises the device)
+  std::vector<uint64_t> nnz_h(std::max(1, nseg_));
+  if (nseg_ && cudaMemcpy(nnz_h.data(), d_nnz_, nseg_ * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cleanup();
+    return set_error(WS_CUDA, "sync_relay: counts");
+  }
 
   // What this rank pulls: every trainer shard, of any rank, with a route to
   // its serving coordinate (plan_pulls, one puller per serving rank as
@@ -203,6 +218,8 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
 
   // ---- pusher --------------------------------------------------------------
   void* d_payload = dev_alloc(max_payload);
+  uint32_t* d_seq_idx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
+  void* d_seq_val = dev_alloc(max_cap * esz);
   std::vector<uint8_t*> stage(depth);
   for (auto& p : stage) p = host_alloc(std::min<uint64_t>(B, max_payload));
   std::vector<cudaEvent_t> ev(depth);
@@ -211,7 +228,15 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
     const auto t0 = Clock::now();
     for (size_t i = 0; i < segs.size() && first_err.st == WS_OK; ++i) {
       ws_payload_info info;
-      ws_status e = payload((int)i, ro.force_wide_index != 0, d_payload, &info, s_push);
+      // the shard's ascending stream on the pusher's stream (codec.cpp:48-49
+      // order), then its payload (engine.cpp:118-128)
+      const uint64_t n = nnz_h[i];
+      const bool sparse = o.sparse && n <= segs_[i].cap;
+      ws_status e = WS_OK;
+      if (sparse && n) e = compact_segment((int)i, d_seq_idx, d_seq_val, s_push);
+      if (e == WS_OK)
+        e = payload_from((int)i, ro.force_wide_index != 0, d_seq_idx, d_seq_val, n,
+                         sparse ? 'S' : 'D', d_payload, &info, s_push);
       if (e != WS_OK) {
         fail(e, "sync_relay: payload");
         return;
@@ -256,6 +281,8 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   uint32_t* d_err = static_cast<uint32_t*>(dev_alloc(4));
   const size_t ws_bytes = ws_diff_workspace_bytes(max_cap);
   void* d_ws = dev_alloc(ws_bytes);
+  const bool dbg = getenv("WSYNC_RELAY_DEBUG") != nullptr;
+  double dt[5] = {0, 0, 0, 0, 0};  // debug: h2d, peek, decode, reslice, apply
   auto puller = [&] {
     const auto t0 = Clock::now();
     double apply_acc = 0;
@@ -315,8 +342,18 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
       const auto ta = Clock::now();
       cudaMemcpyAsync(d_in, h_payload, total, cudaMemcpyHostToDevice, s_pull);
       cudaStreamSynchronize(s_pull);
+      auto tk = Clock::now();
+      auto lap = [&](int q) {
+        if (!dbg) return;
+        cudaStreamSynchronize(s_pull);
+        const auto now = Clock::now();
+        dt[q] += secs(tk, now);
+        tk = now;
+      };
+      dt[0] += dbg ? secs(ta, tk) : 0.0;
       ws_payload_info info;
       ws_status e = ws_peek_payload_dev(d_in, total, &info);
+      lap(1);
       if (e != WS_OK) {
         fail(e, std::string(ws_last_error()));
         return;
@@ -326,6 +363,7 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
       char* tgt = static_cast<char*>(serve) + r.dst_offset * esz;
       if (info.codec == 'S') {
         e = ws_decode_sparse_dev(d_in, &info, d_idx, d_val, ps);
+        lap(2);
         if (e == WS_OK)
           e = ws_reslice_delta((ws_dtype)dtype_, p.shape.data(), nd, src.shard.d, r.dst.d, 1,
                                d_idx, d_val, info.nnz, nullptr, d_ridx, d_rval, d_rnnz, d_err,
@@ -333,8 +371,10 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         uint64_t dn = 1;
         for (int dd = 0; dd < nd; ++dd)
           dn *= (uint64_t)(r.dst.d.slice_dim == dd ? r.dst.d.end - r.dst.d.start : p.shape[dd]);
+        lap(3);
         if (e == WS_OK)
           e = ws_apply_delta((ws_dtype)dtype_, tgt, dn, d_ridx, d_rval, 0, d_rnnz, d_err, ps);
+        lap(4);
         uint32_t herr = 0;
         cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s_pull);
         cudaStreamSynchronize(s_pull);
@@ -366,6 +406,9 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   }
   (void)t_net;
   for (auto& e : ev) cudaEventDestroy(e);
+  if (dbg)
+    fprintf(stderr, "relay puller: h2d %.4f peek %.4f decode %.4f reslice %.4f apply %.4f s\n",
+            dt[0], dt[1], dt[2], dt[3], dt[4]);
   cleanup();
   rep->wall_s = secs(wall0, Clock::now());
   rep->push_s = push_s;

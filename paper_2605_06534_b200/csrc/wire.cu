@@ -11,7 +11,9 @@
 //             table-driven CRC per 256-byte piece and the GF(2) fold
 //             crc(A|B) = crc(A) * x^(8|B|) mod P  xor  crc(B), which makes
 //             every piece's contribution independent (XOR-reducible).
+#include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -268,6 +270,31 @@ int grid_for(uint64_t work, int threads) {
 
 ws_status wire_cuda(cudaError_t e, const char* what) { return cuda_status(e, what); }
 
+
+// Stream-ordered scratch from the device's default memory pool, kept cached.
+// With the pool's default release threshold (0), every synchronisation hands
+// the memory back to the driver, so each call paid a full allocation (~4 ms
+// per decode on the relay path).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      done[dev] = true;
+    }
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -407,7 +434,7 @@ ws_status ws_decode_sparse_dev(const void* payload_dev, const ws_payload_info* i
   const uint8_t* p = static_cast<const uint8_t*>(payload_dev);
   if ((uintptr_t)p & 7) return set_error(WS_INVALID_ARGUMENT, "payload must be 8-byte aligned");
   uint32_t* d_err = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_err, 4, s);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&d_err), 4, s);
   if (e != cudaSuccess) return wire_cuda(e, "decode");
   cudaMemsetAsync(d_err, 0, 4, s);
   if (info->nnz)
@@ -444,8 +471,8 @@ ws_status ws_crc32_dev(const void* const* data_dev, const uint64_t* len, int n, 
   }
   CrcJob* d_jobs = nullptr;
   uint32_t* d_acc = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_jobs, n * sizeof(CrcJob), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&d_acc, n * 4, s);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&d_jobs), n * sizeof(CrcJob), s);
+  if (e == cudaSuccess) e = scratch_alloc(reinterpret_cast<void**>(&d_acc), n * 4, s);
   if (e != cudaSuccess) return wire_cuda(e, "crc alloc");
   cudaMemcpyAsync(d_jobs, jobs.data(), n * sizeof(CrcJob), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(d_acc, 0, n * 4, s);
@@ -485,8 +512,9 @@ ws_status ws_encode_bucket_frames_dev(const void* payload_dev, uint64_t payload_
   if (off > out_cap) return set_error(WS_CAPACITY, "frame buffer too small");
   FrameDesc* d_fr = nullptr;
   uint8_t* d_keys = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_fr, nbuckets * sizeof(FrameDesc), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&d_keys, std::max<size_t>(1, blob.size()), s);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&d_fr), nbuckets * sizeof(FrameDesc), s);
+  if (e == cudaSuccess)
+    e = scratch_alloc(reinterpret_cast<void**>(&d_keys), std::max<size_t>(1, blob.size()), s);
   if (e != cudaSuccess) return wire_cuda(e, "frames alloc");
   cudaMemcpyAsync(d_fr, fr.data(), nbuckets * sizeof(FrameDesc), cudaMemcpyHostToDevice, s);
   if (!blob.empty()) cudaMemcpyAsync(d_keys, blob.data(), blob.size(), cudaMemcpyHostToDevice, s);
