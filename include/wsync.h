@@ -108,7 +108,8 @@ ws_status ws_diff_shards(ws_dtype dtype, const void* prev_dev,
 
 /* K4, replaces apply_delta (codec.hpp:41, codec.cpp:65-92): target[idx[k]]
  * += val[k] (F32 IEEE add; I32/BF16 wrap-around add).  The record count is
- * read from nnz_dev when non-null, else nnz.  All indices are validated
+ * read from nnz_dev when non-null (nnz is then an upper bound that sizes the
+ * launch; pass 0 if unknown), else nnz.  All indices are validated
  * before any write; an index >= n sets WS_ERRBIT_INDEX_OUT_OF_SHARD in
  * err_dev and leaves target unchanged. */
 ws_status ws_apply_delta(ws_dtype dtype, void* target_dev, uint64_t n,

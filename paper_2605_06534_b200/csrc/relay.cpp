@@ -373,7 +373,8 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
           dn *= (uint64_t)(r.dst.d.slice_dim == dd ? r.dst.d.end - r.dst.d.start : p.shape[dd]);
         lap(3);
         if (e == WS_OK)
-          e = ws_apply_delta((ws_dtype)dtype_, tgt, dn, d_ridx, d_rval, 0, d_rnnz, d_err, ps);
+          e = ws_apply_delta((ws_dtype)dtype_, tgt, dn, d_ridx, d_rval, info.nnz /* bound */,
+                             d_rnnz, d_err, ps);
         lap(4);
         uint32_t herr = 0;
         cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s_pull);
