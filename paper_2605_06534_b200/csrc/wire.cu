@@ -271,28 +271,37 @@ int grid_for(uint64_t work, int threads) {
 ws_status wire_cuda(cudaError_t e, const char* what) { return cuda_status(e, what); }
 
 
-// Stream-ordered scratch from the device's default memory pool, kept cached.
-// With the pool's default release threshold (0), every synchronisation hands
-// the memory back to the driver, so each call paid a full allocation (~4 ms
-// per decode on the relay path).
+// Stream-ordered scratch from this library's own memory pool per device,
+// which keeps freed memory cached. Through the default pool, with its release
+// threshold of 0, every synchronisation handed the memory back to the driver,
+// so each call paid a full allocation (~4 ms per decode on the relay path).
+// The process's default pool is left untouched.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   static std::mutex mu;
-  static bool done[64] = {};
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev >= 0 && dev < 64) {
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+  cudaMemPool_t pool;
+  {
     std::lock_guard<std::mutex> lk(mu);
-    if (!done[dev]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (!pools[dev]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) {
+        pools[dev] = nullptr;
+        return e;
       }
-      done[dev] = true;
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
+    pool = pools[dev];
   }
-  return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 }  // namespace
