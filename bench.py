@@ -38,8 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default="qwen3-8b")
-    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--density", type=float, default=None)
     ap.add_argument("--threshold", type=float, default=0.20)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -47,8 +47,41 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1,
                     help="Qwen layers per CPU thread in the reference sample")
-    ap.add_argument("--verify", action="store_true", help="check serving == snapshot after run")
-    return ap.parse_args()
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
+                    help="BASELINE.json config: 2 Qwen3-8B FSDP-N -> TP2 x N/2 at 1%% (default), "
+                         "3 Qwen3-32B TP-N -> TP-N/2 x 2 at 0.5%%, 4 Qwen3-30B-A3B expert-sharded "
+                         "TP-N -> EP-N, Zipf(1.1) per-expert densities around 1%% (3/4: N >= 2)")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the bit-exact check of every serving shard after the run")
+    args = ap.parse_args()
+    preset = CONFIGS[args.config]
+    if args.model is None:
+        args.model = preset["model"]
+    if args.density is None:
+        args.density = preset["density"]
+    return args
+
+
+# BASELINE.json configs this bench can run (config 1 is the CPU reference's
+# own case; config 5 is the density sweep, scripts/density_sweep.py)
+CONFIGS = {
+    2: {"model": "qwen3-8b", "density": 0.01},
+    3: {"model": "qwen3-32b", "density": 0.005},
+    4: {"model": "qwen3-30b-a3b", "density": 0.01, "zipf": 1.1},
+}
+
+
+def load_manifest_module():
+    """paper_2605_06534_b200/manifest.py by path: the model shapes without
+    importing the package (whose __init__ maps libwsync.so) -- the reference
+    arm must not load this repo's library."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_2605_06534_b200", "manifest.py")
+    spec = importlib.util.spec_from_file_location("_wsync_manifest", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["_wsync_manifest"] = mod
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def dist_env():
@@ -58,10 +91,17 @@ def dist_env():
     return world, rank, local
 
 
-def layouts(n):
-    """FSDP-N trainer -> TP2 x N/2 serving replicas (TP1 at N=1)."""
+def layouts(n, config=2):
+    """(trainer layout, serving tp, replicas, description) at n GPUs:
+    config 2: FSDP-N -> TP2 x N/2 (TP1 at N=1); config 3: TP-N -> TP-N/2 x 2;
+    config 4: expert-sharded TP-N -> EP-N (one replica)."""
+    if config == 3:
+        tp = max(1, n // 2)
+        return ("tp", n), tp, n // tp, f"trainer TP{n} -> serving TP{tp} x {n // tp} replica(s)"
+    if config == 4:
+        return ("tp", n), n, 1, f"expert-sharded trainer TP{n} -> serving EP{n} (TP{n})"
     tp = 1 if n == 1 else 2
-    return tp, n // tp
+    return ("fsdp", n), tp, n // tp, f"trainer FSDP{n} -> serving TP{tp} x {n // tp} replica(s)"
 
 
 def load_peaks():
@@ -146,7 +186,7 @@ def cpu_reference(args, threads=None, reps=1, warmup=0):
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle.oracle import I32, Reference
-    import paper_2605_06534_b200.manifest as mf
+    mf = load_manifest_module()
     ref = Reference()
     nproc = os.cpu_count() or 1
     layer_elems = sum(p.numel() for p in mf.MODELS[args.model](layer_subset=[1]))
@@ -174,13 +214,16 @@ def cpu_reference(args, threads=None, reps=1, warmup=0):
         states = list(ex.map(make, range(t)))
     elems = sum(st.model_bytes() / 4 for st in states)
     walls = []
-    for it in range(warmup + reps):
-        t0 = time.perf_counter()
-        with ThreadPoolExecutor(t) as ex:
+    with ThreadPoolExecutor(t) as ex:
+        for it in range(warmup + reps):
+            # ServeState::init outside the timed region: the timed part is
+            # TransferEngine::sync_step alone, as bench.cpp:21-43 times it
+            list(ex.map(lambda st: st.prepare(), states))
+            t0 = time.perf_counter()
             reps_ = list(ex.map(lambda st: st.run(True, True, True, args.threshold, 64 << 20),
                                 states))
-        if it >= warmup:  # untimed warm-up reps first
-            walls.append(time.perf_counter() - t0)
+            if it >= warmup:  # untimed warm-up reps first
+                walls.append(time.perf_counter() - t0)
     wall = statistics.median(walls)
     gbs = elems * 2 / wall / 1e9
     return {"value": gbs, "unit": "GB/s", "cores": t, "kind": "reference",
@@ -189,6 +232,7 @@ def cpu_reference(args, threads=None, reps=1, warmup=0):
                       f"reference TransferEngine::sync_step TP1->TP1 Async+shard-aware+sparse; "
                       f"dense-eq at 2 B/elem ({gbs * 2:.3f} GB/s at 4 B/elem)",
             "wall_s": wall, "elems": int(elems),
+            "sync_wall_s_max": max(r["wall_s"] for r in reps_),
             "encode_s_sum": sum(r["encode_s"] for r in reps_),
             "host_cpus": nproc}
 
@@ -201,13 +245,15 @@ def run_reference_arm(args):
     # arm ends within minutes
     reps, warm = max(1, min(args.steps, 3)), min(max(args.warmup, 0), 1)
     cb = cpu_reference(args, reps=reps, warmup=warm)
-    tp, rep_ = layouts(args.gpus)
+    mf = load_manifest_module()
+    model_elems = sum(p.numel() for p in mf.MODELS[args.model]())
     line = {"metric": METRIC, "value": round(cb["value"], 4), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": reps, "warmup": warm,
-            "ms_per_step": round(cb["wall_s"] * 1e3 * (8.19e9 / max(cb["elems"], 1)), 1),
+            "ms_per_step": round(cb["wall_s"] * 1e3 * (model_elems / max(cb["elems"], 1)), 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.model} 1% density weight sync, reference CPU path "
+            "config": {"workload": f"{args.model} {args.density:.2%} density weight sync, "
+                                   f"reference CPU path (TransferEngine::sync_step timed alone) "
                                    f"on a bounded layer sample (TP1->TP1)",
                        "model": args.model, "density": args.density},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -240,12 +286,17 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
 
+    if args.config in (3, 4) and n < 2:
+        print(json.dumps({"error": f"config {args.config} ({args.model}) needs >= 2 GPUs: "
+                                   "prev + next + serving copies exceed one GPU's HBM"}))
+        return 2
     manifest = ws.MODELS[args.model]()
-    tp, replicas = layouts(n)
-    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, replicas),
-                   world=n, rank=rank)
+    (scheme, _), tp, replicas, layout_desc = layouts(n, args.config)
+    train = ws.TrainConfig("fsdp") if scheme == "fsdp" else ws.TrainConfig("tp", n, 1, 1)
+    plan = ws.Plan(manifest, ws.BF16, train, ws.ServeConfig(tp, 1, replicas), world=n, rank=rank)
     eng = ws.TransferEngine(plan, device=local, unique_id=uid)
-    eng.generate(seed=args.seed, density=args.density)
+    zipf = CONFIGS[args.config].get("zipf")
+    eng.generate(seed=args.seed, density=args.density, expert_zipf=zipf, perm_seed=11)
     torch.cuda.synchronize()
     model_elems = plan.info.model_elems
     dense_eq_bytes = 2 * model_elems
@@ -263,12 +314,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     probe = eng.sync_step(sparse=True, density_threshold=args.threshold, reverse=rev, report=True)
     rev = not rev
+    xbytes = eng.exchange_bytes() if n > 1 else None
     eng.timing(reset=True)
 
     # ---- timed region: K syncs, no host synchronisation inside ----
+    nvl = NvlinkCounters(local) if n > 1 else None
     barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl0 = nvl.read() if nvl else None
     with ClockSampler(local) as clocks:
         start.record(stream)
         for _ in range(args.steps):
@@ -277,6 +331,7 @@ def run_ours(args):
             rev = not rev
         end.record(stream)
         torch.cuda.synchronize()
+    nvl1 = nvl.read() if nvl else None
     barrier()
     ms = start.elapsed_time(end) / args.steps
     tim = eng.timing(reset=True)
@@ -288,16 +343,16 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (K1 encode) ----
     enc_s = tim["encode_s"] / max(1, tim["steps"])
+    route_s = tim["route_s"] / max(1, tim["steps"])
     train_elems = plan.info.train_elems
     nnz = probe["nnz"]
     # K1 reads prev+next (2 B each) and writes idx u32 + val u16 per change;
     # with the fused apply it also read-modify-writes the 2-B serving element
     # of every change routed to this GPU's own serving shard (4 B).
-    fused = os.environ.get("WSYNC_NO_FUSED_APPLY", "0") in ("", "0")
     my_coord = plan.info.serve_coord
     local_frac = (sum(ov for (_, c, _, ov) in plan.routes if c == my_coord) /
                   max(1, train_elems))
-    alg_bytes = int(4 * train_elems + 6 * nnz + (4 * nnz * local_frac if fused else 0))
+    alg_bytes = int(4 * train_elems + 6 * nnz + 4 * nnz * local_frac)
     peak, peak_src = load_peaks()
     achieved = alg_bytes / enc_s / 1e9 if enc_s > 0 else None
     traffic = None
@@ -309,14 +364,41 @@ def run_ours(args):
     except Exception:
         pass
 
+    # ---- route stage on NVLink (N > 1) ----
+    route = None
+    if n > 1:
+        sent = xbytes["sent_records"] + xbytes["sent_dense"]
+        # 6 B per record (u32 index + u16 value) per remote replica
+        remote_recs = xbytes["sent_records"] // 8
+        route = {"bytes_per_sync": sent, "wire_bytes_per_record": 8,
+                 "alg_bytes_per_sync": 6 * remote_recs + xbytes["sent_dense"],
+                 "recv_bytes_per_sync": xbytes["recv_records"],
+                 "stage_ms": round(route_s * 1e3, 4),
+                 "nvlink_gbs": round(sent / route_s / 1e9, 1) if route_s > 0 else None,
+                 "peak_gbs": 900.0,
+                 "frac_of_900": round(sent / route_s / 1e9 / 900.0, 4) if route_s > 0 else None,
+                 "stage": ("pack + apply after the last K1 round" if tim.get("steps") else "")}
+        if nvl0 is not None and nvl1 is not None:
+            tx = (nvl1[0] - nvl0[0]) * 1024 / args.steps
+            rx = (nvl1[1] - nvl0[1]) * 1024 / args.steps
+            route["nvml_tx_bytes_per_sync"] = int(tx)
+            route["nvml_rx_bytes_per_sync"] = int(rx)
+            if route_s > 0:
+                route["nvml_tx_gbs_over_stage"] = round(tx / route_s / 1e9, 1)
+
     # ---- end-to-end through the C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
         e2e, rev = run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev)
 
+    # ---- bit-exact check of every serving shard (every rank) ----
     verified = None
-    if args.verify:
-        verified = verify_serving(eng, plan, rev)
+    if not args.no_verify:
+        ok = verify_serving(ws, eng, plan, rev, args, zipf)
+        v = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+        if world > 1:
+            dist.all_reduce(v, op=dist.ReduceOp.MIN)
+        verified = bool(v.item())
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
@@ -334,33 +416,71 @@ def run_ours(args):
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic",
-            "config": {"workload": f"{args.model} bf16 weight sync, {args.density:.2%} i.i.d. "
-                                   f"change density, trainer FSDP{n} -> serving TP{tp} x "
-                                   f"{replicas} replica(s)",
-                       "model": args.model, "density": args.density,
-                       "density_threshold": args.threshold, "train": f"fsdp{n}",
-                       "serve": f"tp{tp}x{replicas}", "model_elems": model_elems,
+            "config": {"workload": f"BASELINE config {args.config}: {args.model} bf16 weight "
+                                   f"sync, {args.density:.2%} "
+                                   + ("Zipf(%.1f) per-expert " % zipf if zipf else "i.i.d. ")
+                                   + f"change density, {layout_desc}",
+                       "config": args.config, "model": args.model, "density": args.density,
+                       "density_threshold": args.threshold,
+                       "train": f"{scheme}{n}", "serve": f"tp{tp}x{replicas}",
+                       "model_elems": model_elems,
                        "l2": "inputs larger than L2 (prev+next %.1f GB per GPU per step)"
                              % (4 * train_elems / 1e9)},
             "per_gpu_value": round(value / n, 2),
             "stages_ms": {"encode": round(enc_s * 1e3, 4),
                           "apply": round(tim["apply_s"] / max(1, tim["steps"]) * 1e3, 4),
-                          "route": round(tim["route_s"] / max(1, tim["steps"]) * 1e3, 4)},
+                          "route": round(route_s * 1e3, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
                          "traffic": traffic, "kernel": "encode_kernel<bf16> (K1)",
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "route": route,
             "e2e": e2e, "cpu_baseline": cpu,
             "gpu_launches": int(tim["kernel_launches"]),
             "clocks": clocks.summary(), "nnz_per_step": nnz,
+            "verified": verified,
         }
-        if verified is not None:
-            line["verified"] = verified
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+class NvlinkCounters:
+    """NVLink data throughput counters of this rank's GPU (NVML field values
+    NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed over the links): read before
+    and after the timed region, they give the hardware's count of the bytes
+    the exchange moved."""
+
+    def __init__(self, gpu):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[0].isdigit() else gpu
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.read()
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            nv = self.nv
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                                        nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                out.append(int(v.value.ullVal))
+            return out
+        except Exception:
+            return None
 
 
 def run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev):
@@ -407,16 +527,27 @@ def run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev):
             "path": "ws_engine_sync_step_host (C-ABI), host timer around H2D+sync+D2H"}, rev
 
 
-def verify_serving(eng, plan, rev):
-    """After an even number of syncs the serving shards equal arena[rev]."""
+def verify_serving(ws, eng, plan, rev, args, zipf):
+    """Every serving shard of this rank, bit for bit, after the last sync:
+    `next` if it ran forward, `prev` if reversed -- regenerated on the device
+    from the generator (oracle/wsync_oracle.c gen_elem), so no rank needs
+    another rank's data."""
     import torch
     torch.cuda.synchronize()
-    ok = True
-    if plan.world == 1:
-        for i in range(len(plan.segments)):
-            a = eng.segment_view(i, 1 if rev else 0)
-            ok &= bool(torch.equal(eng.serve_view(i).view(torch.int16), a.view(torch.int16)))
-    return ok
+    which = "next" if rev else "prev"  # rev was toggled after the last sync
+    tabs = {}
+    if zipf is not None:
+        tabs = {i: ws.expert_thresholds(m.shape[0], args.density, zipf, 11)
+                for i, m in enumerate(plan.manifest) if m.kind == ws.ModuleKind.EXPERT}
+    for i, (p, desc, off, n) in enumerate(plan.serve_shards):
+        meta = plan.manifest[p]
+        pv, nx = ws.gen_pair_bf16(args.seed, meta.name, meta.shape, desc, args.density,
+                                  device=eng.device, thr_dim0=tabs.get(p))
+        want = nx if which == "next" else pv
+        if not torch.equal(eng.serve_view(i).view(torch.int16), want.view(torch.int16)):
+            return False
+        del pv, nx
+    return True
 
 
 def main():

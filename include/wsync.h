@@ -350,6 +350,7 @@ typedef struct ws_report { /* TransferReport, engine.hpp:34-42 */
   uint64_t nnz;           /* changed elements found on this rank */
   int32_t dense_shards, sparse_shards;
   uint32_t kernel_launches; /* kernels launched by this sync */
+  int32_t streamed_apply;   /* K1 ran its streamed-apply instantiation */
 } ws_report;
 
 /* unique_id: 128-byte NCCL unique id (ws_nccl_unique_id on rank 0, then
@@ -439,6 +440,30 @@ ws_status ws_engine_sync_step_host(ws_engine* eng, const void* next_host,
                                    ws_stream_t stream, uint64_t* nnz_host,
                                    ws_report* report);
 
+/* ------------------------------------------------------------------------ */
+/* Process-local rank groups                                                  */
+/* ------------------------------------------------------------------------ */
+
+/* All `world` ranks of a layout as engines of ONE process on one GPU: the
+ * ranks share mailboxes, receive regions and serving arenas as plain device
+ * pointers instead of CUDA IPC, and a group sync runs every rank's kernels
+ * (K1, local route, pack_kernel, apply_p2p_kernel -- the multi-GPU data path)
+ * interleaved on one stream.  Used to run any multi-rank layout of the
+ * reference (TrainConfig{tp,pp,dp} -> ServeConfig{tp,pp}, engine.cpp:66-254)
+ * on a single device.  Order: ws_group_create; per rank
+ * ws_engine_create_grouped + ws_engine_bind; ws_group_connect; then
+ * ws_group_sync_step (ws_engine_sync_step refuses grouped engines).  Destroy
+ * the engines before the group. */
+typedef struct ws_group ws_group;
+ws_status ws_group_create(int world, ws_group** out);
+void ws_group_destroy(ws_group* group);
+ws_status ws_engine_create_grouped(const ws_plan* plan, int device, ws_group* group,
+                                   ws_engine** out);
+ws_status ws_group_connect(ws_group* group);
+/* One sync of every rank; reports: NULL or `world` entries (synchronises). */
+ws_status ws_group_sync_step(ws_group* group, const ws_sync_options* opts, ws_stream_t stream,
+                             ws_report* reports);
+
 /* Device-time totals of the syncs since the last reset (the most recent 256
  * at most), summed from CUDA events recorded on each sync's stream -- so a
  * timed loop needs no per-step synchronisation.  Synchronises the engine's
@@ -449,6 +474,14 @@ typedef struct ws_timing {
   double wall_s, encode_s, route_s, apply_s;
 } ws_timing;
 ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out);
+
+/* NVLink traffic of the last sync on this rank (bytes): wire records stored
+ * into the replicas' receive regions (one copy per replica), dense-fallback
+ * boxes stored straight into their serving arenas, and the records other
+ * ranks published into this rank's regions.  NCCL-fallback exchange: bytes
+ * sent / received.  Zero at world 1.  Synchronises. */
+ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records, uint64_t* sent_dense,
+                                   uint64_t* recv_records);
 
 /* Segment i's delta stream from the last sync: device pointers into the
  * engine's record buffer, its record count (host, needs a synchronised

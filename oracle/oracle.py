@@ -306,6 +306,8 @@ class Reference:
         L.ref_state_weights.restype = C.c_void_p
         L.ref_state_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
                                     C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+        L.ref_state_prepare.argtypes = [C.c_void_p]
+        L.ref_state_prepare.restype = C.c_int
         L.ref_state_model_bytes.argtypes = [C.c_void_p]
         L.ref_state_model_bytes.restype = C.c_double
         L.ref_state_serve.argtypes = [C.c_void_p, C.c_int, C.c_int, _u64p]
@@ -490,6 +492,11 @@ class RefState:
                                                    int(sparse), threshold, bucket_bytes,
                                                    int(force_wide), rep))
         return dict(zip(REPORT_FIELDS, rep[:11]))
+
+    def prepare(self):
+        """ServeState::init ahead of the next run(), which then times
+        TransferEngine::sync_step alone."""
+        self.ref._check(self.ref.lib.ref_state_prepare(self.h))
 
     def model_bytes(self):
         return self.ref.lib.ref_state_model_bytes(self.h)

@@ -8,6 +8,7 @@ from ._lib import (BF16, F32, I32, CapacityError, CudaError, IncompleteCoverage,
 from .codec import (SparseDelta, apply_delta, copy_overlap, diff_shards,  # noqa: F401
                     extract_shard, expert_thresholds, gen_pair_bf16, reslice_delta,
                     shard_shape)
-from .engine import Plan, ServeConfig, TrainConfig, TransferEngine, nccl_unique_id  # noqa: F401
+from .engine import (EngineGroup, Plan, ServeConfig, TrainConfig, TransferEngine,  # noqa: F401
+                     nccl_unique_id)
 from . import wire  # noqa: F401
 from .manifest import MODELS, ModuleKind, ParamMeta, toy_transformer_manifest  # noqa: F401

@@ -116,7 +116,7 @@ class Report(C.Structure):  # ws_report
                 ("apply_s", C.c_double), ("pushed_bytes", C.c_uint64),
                 ("pulled_bytes", C.c_uint64), ("nnz", C.c_uint64),
                 ("dense_shards", C.c_int32), ("sparse_shards", C.c_int32),
-                ("kernel_launches", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("streamed_apply", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -222,6 +222,13 @@ _SIGS = {
     "ws_engine_sync_step_host": ([_vp, _vp, C.POINTER(SyncOptions), _vp, C.POINTER(_u64),
                                   C.POINTER(Report)], C.c_int),
     "ws_engine_timing": ([_vp, C.c_int, C.POINTER(Timing)], C.c_int),
+    "ws_engine_exchange_bytes": ([_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)],
+                                 C.c_int),
+    "ws_group_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
+    "ws_group_destroy": ([_vp], None),
+    "ws_engine_create_grouped": ([_vp, C.c_int, _vp, C.POINTER(_vp)], C.c_int),
+    "ws_group_connect": ([_vp], C.c_int),
+    "ws_group_sync_step": ([_vp, C.POINTER(SyncOptions), _vp, _vp], C.c_int),
     "ws_engine_segment_delta": ([_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_u64),
                                  C.c_char_p], C.c_int),
 }

@@ -184,6 +184,8 @@ ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev, void* train_next_
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_bind: null engine");
   const uintptr_t a = (uintptr_t)train_prev_dev | (uintptr_t)train_next_dev | (uintptr_t)serve_dev;
   if (a & 15) return set_error(WS_INVALID_ARGUMENT, "ws_engine_bind: arenas must be 16-byte aligned");
+  if (eng->grouped() && eng->connected())
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_bind: engine of a connected ws_group");
   eng->arena[0] = train_prev_dev;
   eng->arena[1] = train_next_dev;
   eng->serve = serve_dev;

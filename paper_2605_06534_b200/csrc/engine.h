@@ -4,6 +4,7 @@
 #include <functional>
 #include <vector>
 
+#include "fabric.h"
 #include "plan.h"
 #include "route.h"
 
@@ -17,7 +18,9 @@ struct ws_engine {
   ws_engine(const wsync::Plan& plan, int device);
   ~ws_engine();
 
-  ws_status init(const uint8_t* unique_id);
+  // group: the engine is one rank of a process-local ws_group (its exchange
+  // is wired by ws_group_connect); otherwise unique_id (world > 1)
+  ws_status init(const uint8_t* unique_id, bool grouped = false);
   ws_status generate(uint64_t seed, double density, cudaStream_t s, double zipf_s = -1.0,
                      uint64_t perm_seed = 0);
   ws_status sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
@@ -47,19 +50,49 @@ struct ws_engine {
   // copies.  Collective: every rank binds (ws_engine_bind) in the same order.
   ws_status map_serve();
 
+  // One sync in phases (sync_step runs them back to back; ws_group_sync_step
+  // interleaves the phases of all ranks of a group on one stream, so every
+  // flag a kernel waits for was published by an earlier launch).
+  struct SyncCtx {
+    ws_sync_options o{};
+    int pa = 0, na = 1;
+    cudaEvent_t* ev = nullptr;
+    uint32_t launches = 0;
+    bool streamed_apply = false;  // K1's streamed-apply instantiation ran
+  };
+  ws_status sync_begin(SyncCtx& x, const ws_sync_options& o, cudaStream_t s,
+                       const void* next_host);
+  // K1 (every exchange round's segments back to back) + local route
+  ws_status sync_encode(SyncCtx& x, cudaStream_t s);
+  ws_status sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host, ws_report* report);
+  int exchange_rounds() const;
+  ws_status exchange_pack(const ws_sync_options& o, int next_arena, int round, cudaStream_t s,
+                          uint32_t* launches);
+  ws_status exchange_apply(int round, cudaStream_t s, uint32_t* launches);
+  ws_status exchange_end(cudaStream_t s);
+  ws_status exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense, uint64_t* recv_records);
+  bool exchange_needs_resize(const ws_sync_options& o) const;
+  // grows the P2P receive regions for o.density_threshold (collective)
+  ws_status exchange_prepare(const ws_sync_options& o);
+  ws_status init_comm(const uint8_t* unique_id, wsync::GroupShared* group);  // exchange.cu
+  int device() const { return device_; }
+  int world() const { return plan_.world(); }
+  int rank() const { return plan_.rank(); }
+  bool grouped() const { return grouped_; }
+  bool connected() const { return comm_ != nullptr; }
+  bool bound() const { return arena[0] && arena[1] && serve; }
+
  private:
+  bool grouped_ = false;
   ws_status ensure_records(double threshold, int sparse);
-  ws_status init_comm(const uint8_t* unique_id);  // exchange.cu
-  ws_status init_p2p(const std::vector<uint64_t>& send_full,
-                     const std::vector<uint64_t>& recv_full);
+  ws_status init_p2p();
+  ws_status p2p_size(double t);  // receive regions for syncs with threshold <= t
   ws_status size_send(const std::vector<uint64_t>& region_cap);
   ws_status size_recv(uint64_t records);
   void destroy_comm();
-  // refuses options the exchange was not sized for (before any work is queued)
-  ws_status exchange_admit(const ws_sync_options& o) const;
   ws_status exchange_begin(cudaStream_t s, uint32_t* launches);  // P2P "reached step" flags
   ws_status exchange_status() const;                             // faults seen by the kernels
-  int exchange_rounds() const;
+  wsync::P2PArgs round_args(int round) const;
   // R > 1 (P2P): K1 round by round on a high-priority stream, round r's
   // exchange on a low-priority stream overlapping the encode of round r + 1
   ws_status sync_rounds(const ws_sync_options& o, int pa, int na, cudaStream_t s,

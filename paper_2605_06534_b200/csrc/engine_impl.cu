@@ -67,7 +67,8 @@ uint32_t ws_engine::next_epoch() {
   return epoch_;
 }
 
-ws_status ws_engine::init(const uint8_t* unique_id) {
+ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
+  grouped_ = grouped;
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
   const auto& segs = plan_.segments();
   // Encode tiles: one look-back chain per segment.
@@ -180,7 +181,8 @@ ws_status ws_engine::init(const uint8_t* unique_id) {
   ring_ = new cudaEvent_t[kRing][6]();
   for (int i = 0; i < kRing; ++i)
     for (auto& e : ring_[i]) WS_CUDA_TRY(cudaEventCreate(&e), "cudaEventCreate");
-  return init_comm(unique_id);
+  // a group wires the exchange of all its ranks at once (ws_group_connect)
+  return grouped ? WS_OK : init_comm(unique_id, nullptr);
 }
 
 ws_status ws_engine::ensure_records(double threshold, int sparse) {
@@ -191,14 +193,7 @@ ws_status ws_engine::ensure_records(double threshold, int sparse) {
   uint64_t total = 0;
   std::vector<uint64_t> cap(nseg_), rec(nseg_);
   for (int i = 0; i < nseg_; ++i) {
-    const uint64_t n = segs_[i].n;
-    uint64_t c = 0;
-    if (sparse && n) {
-      c = (uint64_t)std::floor(threshold * (double)n);
-      if (c > n) c = n;
-      while (c < n && (double)(c + 1) / (double)n <= threshold) ++c;
-      while (c > 0 && (double)c / (double)n > threshold) --c;
-    }
+    const uint64_t c = sparse ? sparse_capacity(segs_[i].n, threshold) : 0;
     cap[i] = c;
     rec[i] = total;
     total += (c + 63) / 64 * 64;
@@ -360,85 +355,89 @@ ws_status ws_engine::local_route(const ws_sync_options& o, int pa, int na, cudaS
   return WS_OK;
 }
 
-ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
-                               uint64_t* nnz_host, ws_report* report) {
-  if (!arena[0] || !arena[1] || !serve) return set_error(WS_INVALID_ARGUMENT, "sync: unbound");
+ws_status ws_engine::sync_begin(SyncCtx& x, const ws_sync_options& o, cudaStream_t s,
+                                const void* next_host) {
+  if (!bound()) return set_error(WS_INVALID_ARGUMENT, "sync: unbound");
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
-  ws_status st = exchange_admit(o);
+  if (!(o.density_threshold >= 0.0))
+    return set_error(WS_INVALID_ARGUMENT, "density_threshold must be >= 0");
+  // larger receive regions for a higher threshold (collective; a group has
+  // done this for all its ranks already)
+  ws_status st = exchange_prepare(o);
   if (st != WS_OK) return st;
   st = ensure_records(o.density_threshold, o.sparse ? 1 : 0);
   if (st != WS_OK) return st;
-  const int pa = o.reverse ? 1 : 0, na = 1 - pa;
-  const int esz = dtype_size(dtype_);
-  uint32_t launches = 0;
-  cudaEvent_t* ev_ = ring_[ring_head_];
+  x.o = o;
+  x.pa = o.reverse ? 1 : 0;
+  x.na = 1 - x.pa;
+  x.launches = 0;
+  x.ev = ring_[ring_head_];
   ring_head_ = (ring_head_ + 1) % kRing;
   ring_steps_ = std::min<uint32_t>(ring_steps_ + 1, kRing);
   last_stream_ = s;
-
-  WS_CUDA_TRY(cudaEventRecord(ev_[0], s), "event");
+  WS_CUDA_TRY(cudaEventRecord(x.ev[0], s), "event");
   if (plan_.world() > 1 && !encode_only_) {  // (the relay path exchanges nothing here)
-    st = exchange_begin(s, &launches);
+    st = exchange_begin(s, &x.launches);
     if (st != WS_OK) return st;
   }
   if (next_host) {
-    WS_CUDA_TRY(cudaMemcpyAsync(arena[na], next_host, plan_.train_arena_elems() * esz,
+    WS_CUDA_TRY(cudaMemcpyAsync(arena[x.na], next_host,
+                                plan_.train_arena_elems() * dtype_size(dtype_),
                                 cudaMemcpyHostToDevice, s),
                 "H2D next snapshot");
   }
-  WS_CUDA_TRY(cudaEventRecord(ev_[1], s), "event");
+  WS_CUDA_TRY(cudaEventRecord(x.ev[1], s), "event");
   last_sparse_ = o.sparse != 0;
-  last_next_arena_ = na;
-  const bool rounds = plan_.world() > 1 && o.sparse && ntiles_ && !encode_only_ &&
-                      exchange_rounds() > 1;
-  if (rounds) {
-    st = sync_rounds(o, pa, na, s, &launches, ev_);
-    if (st != WS_OK) return st;
-  } else {
-    if (o.sparse && ntiles_) {
-      // K1 reserves each super-tile's records with an atomic on its segment's count
-      WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
-      if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
-      EncodeArgs a = encode_args(pa, na);
-      if (plan_.world() > 1 && !encode_only_) {
-        st = exchange_fuse_k1(a, s);
-        if (st != WS_OK) return st;
-      }
-      WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
-      ++launches;
-      if (count_only_) {
-        st = launch_fixup(a, 0, nseg_, s, &launches);
-        if (st != WS_OK) return st;
-      }
+  last_next_arena_ = x.na;
+  return WS_OK;
+}
+
+ws_status ws_engine::sync_encode(SyncCtx& x, cudaStream_t s) {
+  const ws_sync_options& o = x.o;
+  if (o.sparse && ntiles_) {
+    // K1 reserves each super-tile's records with an atomic on its segment's count
+    WS_CUDA_TRY(cudaMemsetAsync(d_nnz_, 0, nseg_ * 8, s), "memset counts");
+    if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, s), "memset fill");
+    EncodeArgs a = encode_args(x.pa, x.na);
+    if (plan_.world() > 1 && !encode_only_ && !grouped_) {
+      ws_status st = exchange_fuse_k1(a, s);
+      if (st != WS_OK) return st;
     }
-    WS_CUDA_TRY(cudaEventRecord(ev_[2], s), "event");
-    if (encode_only_) {  // relay pusher: the serving side applies what it pulls
-      WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
-      WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
-      WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
-      launch_total_ += launches;
-      return WS_OK;
-    }
-    st = local_route(o, pa, na, s, &launches);
-    if (st != WS_OK) return st;
-    WS_CUDA_TRY(cudaEventRecord(ev_[3], s), "event");
-    if (plan_.world() > 1) {
-      st = exchange(o, na, s, &launches);
+    WS_CUDA_TRY(launch_encode(dtype_, a, s), "encode");
+    ++x.launches;
+    x.streamed_apply = a.serve_stream != 0;
+    if (count_only_) {
+      ws_status st = launch_fixup(a, 0, nseg_, s, &x.launches);
       if (st != WS_OK) return st;
     }
   }
+  WS_CUDA_TRY(cudaEventRecord(x.ev[2], s), "event");
+  if (!encode_only_) {  // relay pusher: the serving side applies what it pulls
+    ws_status st = local_route(o, x.pa, x.na, s, &x.launches);
+    if (st != WS_OK) return st;
+  }
+  WS_CUDA_TRY(cudaEventRecord(x.ev[3], s), "event");
+  return WS_OK;
+}
+
+ws_status ws_engine::sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host,
+                                 ws_report* report) {
+  const ws_sync_options& o = x.o;
+  cudaEvent_t* ev_ = x.ev;
   WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
   if ((nnz_host || report) && nseg_)
     WS_CUDA_TRY(cudaMemcpyAsync(h_nnz_pinned_, d_nnz_, nseg_ * 8, cudaMemcpyDeviceToHost, s),
                 "D2H counts");
   WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
-  launch_total_ += launches;
+  launch_total_ += x.launches;
   if (!nnz_host && !report) return WS_OK;
   WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
-  if ((st = exchange_status()) != WS_OK) return st;
+  ws_status st = exchange_status();
+  if (st != WS_OK) return st;
   std::memcpy(h_nnz_.data(), h_nnz_pinned_, nseg_ * 8);
   if (nnz_host) std::memcpy(nnz_host, h_nnz_.data(), nseg_ * 8);
   if (report) {
+    const int esz = dtype_size(dtype_);
     std::memset(report, 0, sizeof(*report));
     float ms = 0;
     cudaEventElapsedTime(&ms, ev_[0], ev_[5]);
@@ -465,9 +464,33 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
       report->nnz += o.sparse ? h_nnz_[i] : 0;
     }
     report->pulled_bytes = pulled_bytes_;
-    report->kernel_launches = launches;
+    report->kernel_launches = x.launches;
+    report->streamed_apply = x.streamed_apply ? 1 : 0;
   }
   return WS_OK;
+}
+
+ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
+                               uint64_t* nnz_host, ws_report* report) {
+  if (grouped_)
+    return set_error(WS_INVALID_ARGUMENT, "engine of a ws_group: sync through ws_group_sync_step");
+  SyncCtx x;
+  ws_status st = sync_begin(x, o, s, next_host);
+  if (st != WS_OK) return st;
+  const bool rounds = plan_.world() > 1 && o.sparse && ntiles_ && !encode_only_ &&
+                      exchange_rounds() > 1;
+  if (rounds) {
+    st = sync_rounds(o, x.pa, x.na, s, &x.launches, x.ev);
+    if (st != WS_OK) return st;
+  } else {
+    st = sync_encode(x, s);
+    if (st != WS_OK) return st;
+    if (plan_.world() > 1 && !encode_only_) {
+      st = exchange(o, x.na, s, &x.launches);
+      if (st != WS_OK) return st;
+    }
+  }
+  return sync_finish(x, s, nnz_host, report);
 }
 
 ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,

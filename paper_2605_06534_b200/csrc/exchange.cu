@@ -27,6 +27,7 @@
 
 #include "capi_util.h"
 #include "engine.h"
+#include "fabric.h"
 
 using namespace wsync;
 
@@ -44,12 +45,14 @@ using namespace wsync;
   } while (0)
 
 struct ws_engine::Comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;                     // one process per GPU (not in a ws_group)
+  std::unique_ptr<Fabric> fab;                   // how peers map each other's memory
   int world = 1, rank = 0, coords = 1;
   // remote routes (this rank as a sender)
   LocalEntry* d_entries = nullptr;
   int nentries = 0;
   uint64_t* d_unit_off = nullptr;
+  // NCCL-fallback exchange (no CUDA IPC between the GPUs)
   std::vector<uint64_t> region_off, region_cap;  // per coordinate, records
   uint64_t* d_region_off = nullptr;
   uint64_t* d_region_cap = nullptr;
@@ -64,12 +67,18 @@ struct ws_engine::Comm {
   std::vector<std::vector<int>> dests;           // per coordinate: receiving ranks != me
   // peer-memory mode
   bool p2p = false;
-  void* d_p2p = nullptr;                         // [mailbox | receive buffer] (IPC-exported)
-  std::vector<void*> peer;                       // mapped d_p2p of every rank (null: me)
-  std::vector<void*> peer_serve_map;             // mapped serving allocations (null: me)
+  void* d_head = nullptr;                        // [mailbox | count slots], fixed size
+  void* d_rec = nullptr;                         // receive regions, sized by the threshold
+  std::vector<void*> peer_head, peer_rec, peer_serve;  // every rank's, mapped here
+  double sized_t = -1.0;                         // density threshold the regions hold
+  double want_t = kDefaultThreshold;             // the largest a sync has asked for
   P2PArgs pargs{};
+  std::vector<int> mine;                         // my remote routes (indices into routes())
+  std::vector<EntryDest> edest;                  // host copy of d_edest
+  std::vector<RemoteMap> rmaps;                  // K1's view of them, grouped by segment
+  std::vector<int> rmap_entry;                   // remote entry of every rmaps element
   uint32_t epoch = 0;
-  RemoteMap* d_rmaps = nullptr;                  // my remote routes grouped by segment (K1)
+  RemoteMap* d_rmaps = nullptr;
   uint32_t* d_rseg_first = nullptr;
   bool k1_emit = false;                          // this sync's records went out from K1
   EntryDest* d_edest = nullptr;
@@ -94,12 +103,17 @@ struct ws_engine::Comm {
   std::vector<cudaEvent_t> ev_round;               // K1 round r done
   cudaEvent_t ev_start = nullptr, ev_xdone = nullptr, ev_encdone = nullptr;
 
+  void release_peers(std::vector<void*>& v) {
+    for (int g = 0; g < (int)v.size(); ++g)
+      if (g != rank && v[g] && fab) fab->release(v[g]);
+    v.clear();
+  }
   ~Comm() {
-    for (void* p : peer)
-      if (p) cudaIpcCloseMemHandle(p);
-    for (void* p : peer_serve_map)
-      if (p) cudaIpcCloseMemHandle(p);
-    cudaFree(d_p2p);
+    release_peers(peer_head);
+    release_peers(peer_rec);
+    release_peers(peer_serve);
+    cudaFree(d_head);
+    cudaFree(d_rec);
     cudaFree(d_edest);
     cudaFree(d_rmaps);
     cudaFree(d_rseg_first);
@@ -125,6 +139,7 @@ struct ws_engine::Comm {
     cudaFree(d_send);
     cudaFree(d_recv);
     if (h_allcnt) cudaFreeHost(h_allcnt);
+    fab.reset();
     if (comm) ncclCommDestroy(comm);
   }
 };
@@ -147,6 +162,139 @@ void exchange_caps(const Plan& plan, int me, std::vector<uint64_t>* send_cap,
       else if (rt.coord == my_coord) (*recv_cap)[r] += rt.overlap;
     }
   }
+}
+
+// ---- fabrics ------------------------------------------------------------------
+
+namespace {
+// Base of the allocation holding `p` (driver entry point; the library does
+// not link libcuda).  IPC handles are per allocation, and the serving arena
+// may be a view into a larger caller allocation.
+bool allocation_base(void* p, void** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) return false;
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<void*>(b);
+  return true;
+}
+
+struct IpcEntry {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+  uint32_t ok, present;
+};
+}  // namespace
+
+ws_status NcclFabric::share(void* p, std::vector<void*>* out) {
+  const int W = world_, me = rank_;
+  IpcEntry mine{};
+  if (p) {
+    mine.present = 1;
+    void* base = nullptr;
+    if (allocation_base(p, &base) && cudaIpcGetMemHandle(&mine.h, base) == cudaSuccess) {
+      mine.offset = static_cast<char*>(p) - static_cast<char*>(base);
+      mine.ok = 1;
+    }
+    cudaGetLastError();
+  } else {
+    mine.ok = 1;
+  }
+  IpcEntry* d = nullptr;
+  if (cudaMalloc(&d, (size_t)W * sizeof(IpcEntry)) != cudaSuccess)
+    return set_error(WS_CUDA, "fabric: cudaMalloc");
+  cudaMemcpy(d + me, &mine, sizeof(mine), cudaMemcpyHostToDevice);
+  cudaStream_t s0;
+  cudaStreamCreate(&s0);
+  ncclResult_t nr = ncclAllGather(d + me, d, sizeof(IpcEntry), ncclUint8, comm_, s0);
+  cudaStreamSynchronize(s0);
+  cudaStreamDestroy(s0);
+  std::vector<IpcEntry> all(W);
+  cudaMemcpy(all.data(), d, (size_t)W * sizeof(IpcEntry), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (nr != ncclSuccess) return set_error(WS_NCCL, "fabric: handle all-gather failed");
+  out->assign(W, nullptr);
+  int ok = 1;
+  for (int g = 0; g < W; ++g) ok &= all[g].ok ? 1 : 0;
+  for (int g = 0; g < W && ok; ++g) {
+    if (!all[g].present) continue;
+    if (g == me) {
+      (*out)[g] = p;
+      continue;
+    }
+    void* q = nullptr;
+    if (cudaIpcOpenMemHandle(&q, all[g].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    (*out)[g] = static_cast<char*>(q) + all[g].offset;
+  }
+  ws_status st = all_min(&ok);  // every rank must agree, or one would wait forever for a flag
+  if (st == WS_OK && ok) return WS_OK;
+  for (int g = 0; g < W; ++g)
+    if (g != me && (*out)[g]) release((*out)[g]);
+  out->assign(W, nullptr);
+  return st != WS_OK ? st : set_error(WS_CUDA, "fabric: CUDA IPC unavailable between the ranks");
+}
+
+void NcclFabric::release(void* p) {
+  void* base = nullptr;
+  if (allocation_base(p, &base)) cudaIpcCloseMemHandle(base);
+  cudaGetLastError();
+}
+
+ws_status NcclFabric::all_min(int* v) {
+  int* d = nullptr;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return set_error(WS_CUDA, "fabric: cudaMalloc");
+  cudaMemcpy(d, v, sizeof(int), cudaMemcpyHostToDevice);
+  cudaStream_t s0;
+  cudaStreamCreate(&s0);
+  ncclResult_t nr = ncclAllReduce(d, d, 1, ncclInt32, ncclMin, comm_, s0);
+  cudaStreamSynchronize(s0);
+  cudaStreamDestroy(s0);
+  cudaMemcpy(v, d, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return nr == ncclSuccess ? WS_OK : set_error(WS_NCCL, "fabric: all-reduce failed");
+}
+
+void GroupShared::barrier() {
+  std::unique_lock<std::mutex> lk(m);
+  const unsigned gen = generation;
+  if (++arrived == world) {
+    arrived = 0;
+    ++generation;
+    cv.notify_all();
+  } else {
+    cv.wait(lk, [&] { return generation != gen; });
+  }
+}
+
+ws_status GroupFabric::share(void* p, std::vector<void*>* out) {
+  g_->slots[rank_] = p;
+  g_->barrier();
+  *out = g_->slots;
+  g_->barrier();
+  return WS_OK;
+}
+
+ws_status GroupFabric::all_min(int* v) {
+  g_->ints[rank_] = *v;
+  g_->barrier();
+  int m = *v;
+  for (int x : g_->ints) m = std::min(m, x);
+  g_->barrier();
+  *v = m;
+  return WS_OK;
 }
 
 }  // namespace wsync
@@ -182,25 +330,17 @@ struct RecvLayout {
   uint64_t records = 0;
   size_t head = 0;                           // mailbox + count slots, bytes
 };
-// WSYNC_MAX_THRESHOLD = t > 0 bounds every receive region by the records
-// its source segment can hold as a sparse shard, floor(t * n) (+1), instead
-// of the full overlap: dense boxes never travel as records when they go
-// straight into the serving arenas (bind fails otherwise), and syncs with a
-// density threshold above t are refused.
-double max_threshold() {
-  static const double t = [] {
-    const char* e = getenv("WSYNC_MAX_THRESHOLD");
-    return e ? atof(e) : 0.0;
-  }();
-  return t;
-}
-uint64_t entry_capacity(const Plan& plan, int g, const Route& r) {
-  const double t = max_threshold();
-  if (t <= 0.0 || t >= 1.0) return r.overlap;
+// Records one remote entry (route r of rank g) can carry in a sync whose
+// density threshold is at most t: a sparse source segment holds at most
+// sparse_capacity(n, t) records, and with direct dense boxes a dense one
+// sends none -- so the region needs min(overlap, that), not the worst case
+// of every routed element as a record (t >= 1).
+uint64_t entry_capacity(const Plan& plan, int g, const Route& r, double t) {
+  if (t >= 1.0) return r.overlap;
   const uint64_t n = plan.segments_of(g)[r.seg].n;
-  return std::min<uint64_t>(r.overlap, (uint64_t)(t * (double)n) + 1);
+  return std::min<uint64_t>(r.overlap, sparse_capacity(n, t));
 }
-RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
+RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile, double t) {
   RecvLayout L;
   const int k = plan.coord_of_rank(q);
   for (int g = 0; g < plan.world(); ++g) {
@@ -210,7 +350,7 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
     for (int e = 0; e < (int)rr.size(); ++e) {
       const Route& r = plan.routes_of(g)[rr[e]];
       if (r.coord != k) continue;
-      const uint64_t cap = entry_capacity(plan, g, r);
+      const uint64_t cap = entry_capacity(plan, g, r, t);
       L.entries.emplace_back(g, e);
       L.off.push_back(L.records);
       L.cap.push_back(cap);
@@ -221,23 +361,35 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile) {
   L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
   return L;
 }
+int default_rounds(int world) {
+  // Measured (Qwen3-8B, 1%): 3 rounds take N = 4 from 4.10 to 3.74 ms; at
+  // N = 2 the 0.46 ms exchange gains nothing from the split.
+  int R = world >= 4 ? 3 : 1;
+  if (const char* e = getenv("WSYNC_ROUNDS")) R = std::max(1, std::min(kMaxRounds, atoi(e)));
+  return R;
+}
 }  // namespace
 
-ws_status ws_engine::init_comm(const uint8_t* unique_id) {
+ws_status ws_engine::init_comm(const uint8_t* unique_id, GroupShared* group) {
   if (plan_.world() == 1) return WS_OK;
-  if (!unique_id) return set_error(WS_INVALID_ARGUMENT, "multi-GPU engine needs an NCCL unique id");
+  if (!unique_id && !group)
+    return set_error(WS_INVALID_ARGUMENT, "multi-GPU engine needs an NCCL unique id");
   auto* c = new Comm;
   comm_ = c;
   c->world = plan_.world();
   c->rank = plan_.rank();
   c->coords = plan_.coords();
-  ncclUniqueId id;
-  std::memcpy(&id, unique_id, sizeof(id));
-  WS_NCCL_TRY(ncclCommInitRank(&c->comm, c->world, id, c->rank), "ncclCommInitRank");
+  if (group) {
+    c->fab.reset(new GroupFabric(c->world, c->rank, group));
+  } else {
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    WS_NCCL_TRY(ncclCommInitRank(&c->comm, c->world, id, c->rank), "ncclCommInitRank");
+    c->fab.reset(new NcclFabric(c->world, c->rank, c->comm));
+  }
 
   // remote routes: every route whose coordinate has a replica other than me
-  const int me = plan_.rank(), my_coord = plan_.my_coord();
-  (void)my_coord;
+  const int me = plan_.rank();
   std::vector<LocalEntry> remote;
   const auto& segs = plan_.segments();
   for (int ri : remote_routes(plan_, me)) {
@@ -256,23 +408,9 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
                            cudaMemcpyHostToDevice),
                 "H2D");
   WS_CUDA_TRY(cudaMalloc(&c->d_unit_off, (remote.size() + kMaxRounds + 1) * 8), "cudaMalloc");
-
-  // Buffers start at a fraction of the worst case (every routed element sent
-  // dense) and grow on demand: the all-gathered counts tell every rank what
-  // it must send and receive before any byte moves (see exchange()).
-  std::vector<uint64_t> send_full, recv_full;
-  exchange_caps(plan_, me, &send_full, &recv_full);
-  double frac = 0.25;
-  if (const char* f = getenv("WSYNC_EXCHANGE_FRACTION")) frac = atof(f);
-  std::vector<uint64_t> region_cap(c->coords);
-  for (int k = 0; k < c->coords; ++k)
-    region_cap[k] = send_full[k] ? std::max<uint64_t>(4096, (uint64_t)(frac * send_full[k])) : 0;
-  uint64_t recv_full_total = 0;
-  for (auto v : recv_full) recv_full_total += v;
   c->dests.assign(c->coords, {});
   for (int g = 0; g < c->world; ++g)
     if (g != me) c->dests[plan_.coord_of_rank(g)].push_back(g);
-
   WS_CUDA_TRY(cudaMalloc(&c->d_region_off, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_region_cap, c->coords * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_region_cnt, c->coords * 8), "cudaMalloc");
@@ -283,101 +421,75 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id) {
   *c->h_err = 0;
   WS_CUDA_TRY(cudaMallocHost(&c->h_allcnt, (size_t)c->world * c->coords * 8), "cudaMallocHost");
   const char* mode = getenv("WSYNC_EXCHANGE");
-  const bool want_p2p = !(mode && std::string(mode) == "nccl") && c->world <= kMaxWorld &&
-                        c->coords <= kMaxWorld && plan_.replicas() <= kMaxReplicas;
-  if (want_p2p) {
-    ws_status st = init_p2p(send_full, recv_full);
-    if (st == WS_OK) return WS_OK;
-    // fall back to the NCCL exchange (e.g. no CUDA IPC between these GPUs)
-    c->p2p = false;
+  const bool fits = c->world <= kMaxWorld && c->coords <= kMaxWorld &&
+                    plan_.replicas() <= kMaxReplicas;
+  if (group && !fits) return set_error(WS_INVALID_ARGUMENT, "group: world beyond kMaxWorld");
+  if (group || (fits && !(mode && std::string(mode) == "nccl"))) {
+    ws_status st = init_p2p();
+    if (st == WS_OK || group) return st;
+    c->p2p = false;  // fall back to the NCCL exchange (e.g. no CUDA IPC between these GPUs)
   }
+  // NCCL exchange: buffers start at a fraction of the worst case (every routed
+  // element sent dense) and grow on demand: the all-gathered counts tell every
+  // rank what it must send and receive before any byte moves (see exchange()).
+  std::vector<uint64_t> send_full, recv_full;
+  exchange_caps(plan_, me, &send_full, &recv_full);
+  double frac = 0.25;
+  if (const char* f = getenv("WSYNC_EXCHANGE_FRACTION")) frac = atof(f);
+  std::vector<uint64_t> region_cap(c->coords);
+  for (int k = 0; k < c->coords; ++k)
+    region_cap[k] = send_full[k] ? std::max<uint64_t>(4096, (uint64_t)(frac * send_full[k])) : 0;
+  uint64_t recv_full_total = 0;
+  for (auto v : recv_full) recv_full_total += v;
   ws_status st = size_send(region_cap);
   if (st != WS_OK) return st;
   return size_recv(recv_full_total ? std::max<uint64_t>(4096, (uint64_t)(frac * recv_full_total)) : 0);
 }
 
-// Peer-memory exchange: every rank exports [mailbox | counts | records] with
-// CUDA IPC.  The records area holds one region per (source rank, remote
-// entry of that source) whose coordinate is this rank's, sized by the route's
-// overlap; the layouts of all ranks follow from the static plan (no data
-// exchange beyond the 64-byte handles, all-gathered over NCCL).
-
-ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
-                              const std::vector<uint64_t>& recv_full) {
+// Peer-memory exchange.  Every rank owns two shared allocations: the head
+// [mailbox | one count slot per receive region], fixed for the plan, and
+// the receive area, one region per (source rank, remote entry of that
+// source) whose coordinate is this rank's -- sized by p2p_size for a density
+// threshold.  The layouts of all ranks follow from the static plan, so the
+// only data exchanged is the fabric's handles.  This sets up the head and
+// the static tables; regions are sized when the serving arena is bound.
+ws_status ws_engine::init_p2p() {
   Comm* c = comm_;
   const int me = c->rank, W = c->world;
-  const size_t wb = wire_bytes(dtype_);
-  (void)send_full;
-  (void)recv_full;
-  // rounds: WSYNC_ROUNDS (1..kMaxRounds).  Measured (Qwen3-8B, 1%): 3 rounds
-  // take N = 4 from 4.10 to 3.74 ms; at N = 2 the 0.46 ms exchange gains
-  // nothing from the split, so one round there.
-  int R = W >= 4 ? 3 : 1;
-  if (const char* e = getenv("WSYNC_ROUNDS")) R = std::max(1, std::min(kMaxRounds, atoi(e)));
+  const int R = default_rounds(W);
+  c->R = R;
   const uint32_t tile = encode_tile_elems(dtype_);
-  std::vector<RecvLayout> lay(W);
-  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q, R, tile);
-  const size_t bytes = lay[me].head + std::max<uint64_t>(1, lay[me].records) * wb;
-  if (cudaMalloc(&c->d_p2p, bytes) != cudaSuccess)
-    return set_error(WS_CUDA, "p2p: receive buffer allocation failed");
-  WS_CUDA_TRY(cudaMemset(c->d_p2p, 0, lay[me].head), "memset mailbox");
-  cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, c->d_p2p) != cudaSuccess) {
-    cudaGetLastError();
-    return set_error(WS_CUDA, "p2p: cudaIpcGetMemHandle failed");
+  const RecvLayout L = recv_layout(plan_, me, R, tile, 1.0);
+  int ok = cudaMalloc(&c->d_head, L.head) == cudaSuccess &&
+           cudaMemset(c->d_head, 0, L.head) == cudaSuccess;
+  cudaGetLastError();
+  ws_status st = c->fab->all_min(&ok);
+  if (st != WS_OK || !ok) {
+    cudaFree(c->d_head);
+    c->d_head = nullptr;
+    return st != WS_OK ? st : set_error(WS_CUDA, "p2p: mailbox allocation failed");
   }
-  void* d_h = nullptr;
-  WS_CUDA_TRY(cudaMalloc(&d_h, (size_t)W * sizeof(h)), "cudaMalloc");
-  WS_CUDA_TRY(cudaMemcpy(static_cast<char*>(d_h) + me * sizeof(h), &h, sizeof(h),
-                         cudaMemcpyHostToDevice), "H2D");
-  cudaStream_t s0;
-  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
-  ncclResult_t nr = ncclAllGather(static_cast<char*>(d_h) + me * sizeof(h), d_h, sizeof(h),
-                                  ncclUint8, c->comm, s0);
-  std::vector<cudaIpcMemHandle_t> all(W);
-  cudaStreamSynchronize(s0);
-  cudaStreamDestroy(s0);
-  cudaMemcpy(all.data(), d_h, (size_t)W * sizeof(h), cudaMemcpyDeviceToHost);
-  cudaFree(d_h);
-  if (nr != ncclSuccess) return set_error(WS_NCCL, "p2p: handle all-gather failed");
-  c->peer.assign(W, nullptr);
-  bool ok = true;
-  for (int g = 0; g < W; ++g) {
-    if (g == me) continue;
-    if (cudaIpcOpenMemHandle(&c->peer[g], all[g], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      ok = false;
-    }
+  st = c->fab->share(c->d_head, &c->peer_head);
+  if (st != WS_OK) {
+    cudaFree(c->d_head);
+    c->d_head = nullptr;
+    return st;
   }
-  // every rank must agree, or one would wait forever for a flag
-  int* d_ok = nullptr;
-  WS_CUDA_TRY(cudaMalloc(&d_ok, sizeof(int)), "cudaMalloc");
-  int h_ok = ok ? 1 : 0;
-  WS_CUDA_TRY(cudaMemcpy(d_ok, &h_ok, sizeof(int), cudaMemcpyHostToDevice), "H2D");
-  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
-  nr = ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, s0);
-  cudaStreamSynchronize(s0);
-  cudaStreamDestroy(s0);
-  cudaMemcpy(&h_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost);
-  cudaFree(d_ok);
-  if (nr != ncclSuccess || !h_ok) return set_error(WS_CUDA, "p2p: CUDA IPC unavailable");
 
   P2PArgs& P = c->pargs;
   P = P2PArgs{};
   P.on = 1;
   P.world = W;
   P.rank = me;
-  P.mailbox = static_cast<unsigned long long*>(c->d_p2p);
+  P.mailbox = static_cast<unsigned long long*>(c->d_head);
   for (int g = 0; g < W; ++g)
-    P.peer_mailbox[g] = static_cast<unsigned long long*>(g == me ? c->d_p2p : c->peer[g]);
+    P.peer_mailbox[g] = static_cast<unsigned long long*>(c->peer_head[g]);
   for (int k = 0; k < kMaxWorld; ++k)
-    for (int r = 0; r < kMaxReplicas; ++r) {
-      P.dest_rank[k][r] = -1;
-    }
-  // sender: where each of my remote entries goes at each replica; only the
-  // coordinates I send to get destinations (their ranks ack exactly the
-  // sources they expect)
-  const std::vector<int> mine = remote_routes(plan_, me);
+    for (int r = 0; r < kMaxReplicas; ++r) P.dest_rank[k][r] = -1;
+  // sender: only the coordinates I send to get destinations (their ranks ack
+  // exactly the sources they expect)
+  c->mine = remote_routes(plan_, me);
+  const std::vector<int>& mine = c->mine;
   std::vector<char> sends_to(c->coords, 0);
   for (int e : mine) sends_to[plan_.routes_of(me)[e].coord] = 1;
   for (int k = 0; k < c->coords; ++k) {
@@ -385,32 +497,12 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
     int r = 0;
     for (int g : c->dests[k]) P.dest_rank[k][r++] = g;
   }
-  std::vector<EntryDest> ed(std::max<size_t>(1, mine.size()));
-  for (int e = 0; e < (int)mine.size(); ++e) {
-    EntryDest& D = ed[e];
-    std::memset(&D, 0, sizeof(D));
-    const Route& rt = plan_.routes_of(me)[mine[e]];
-    D.cap = entry_capacity(plan_, me, rt);
-    int r = 0;
-    for (int q : c->dests[rt.coord]) {
-      const RecvLayout& L = lay[q];
-      int pos = -1;
-      for (int j = 0; j < (int)L.entries.size(); ++j)
-        if (L.entries[j].first == me && L.entries[j].second == e) pos = j;
-      if (pos < 0) return set_error(WS_TRANSFER_ERROR, "p2p: entry missing from a receiver layout");
-      char* base = static_cast<char*>(c->peer[q]);
-      D.rec[r] = base + L.head + L.off[pos] * wb;
-      D.cnt[r] = reinterpret_cast<uint32_t*>(base + kMailboxBytes) + pos;
-      ++r;
-    }
-  }
-  WS_CUDA_TRY(cudaMalloc(&c->d_edest, ed.size() * sizeof(EntryDest)), "cudaMalloc");
-  WS_CUDA_TRY(cudaMemcpy(c->d_edest, ed.data(), ed.size() * sizeof(EntryDest),
-                         cudaMemcpyHostToDevice), "H2D");
+  WS_CUDA_TRY(cudaMalloc(&c->d_edest, std::max<size_t>(1, mine.size()) * sizeof(EntryDest)),
+              "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&c->d_ent_cnt, std::max<size_t>(1, mine.size()) * 4), "cudaMalloc");
-  {  // the same routes as K1 sees them, grouped by segment
+  {  // the same routes as K1 sees them, grouped by segment (regions filled by p2p_size)
     const auto& segs = plan_.segments();
-    std::vector<std::vector<RemoteMap>> by_seg(segs.size());
+    std::vector<std::vector<std::pair<RemoteMap, int>>> by_seg(segs.size());
     for (int e = 0; e < (int)mine.size(); ++e) {
       const Route& rt = plan_.routes_of(me)[mine[e]];
       const ParamMeta& p = plan_.manifest()[rt.dst.param];
@@ -424,29 +516,25 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
       m.shift = le.shift;
       m.dst_base = le.dst_base;
       m.map = le.map;
-      m.cap = ed[e].cap;
       m.cnt = c->d_ent_cnt + e;
-      for (int r = 0; r < kMaxReplicas && r < 8; ++r) m.rec[r] = ed[e].rec[r];
-      by_seg[rt.seg].push_back(m);
+      by_seg[rt.seg].emplace_back(m, e);
     }
-    std::vector<RemoteMap> flat;
     std::vector<uint32_t> first(segs.size() + 1, 0);
     for (size_t sg = 0; sg < segs.size(); ++sg) {
-      first[sg] = (uint32_t)flat.size();
-      flat.insert(flat.end(), by_seg[sg].begin(), by_seg[sg].end());
+      first[sg] = (uint32_t)c->rmaps.size();
+      for (auto& me_ : by_seg[sg]) {
+        c->rmaps.push_back(me_.first);
+        c->rmap_entry.push_back(me_.second);
+      }
     }
-    first[segs.size()] = (uint32_t)flat.size();
-    WS_CUDA_TRY(cudaMalloc(&c->d_rmaps, std::max<size_t>(1, flat.size()) * sizeof(RemoteMap)),
+    first[segs.size()] = (uint32_t)c->rmaps.size();
+    WS_CUDA_TRY(cudaMalloc(&c->d_rmaps, std::max<size_t>(1, c->rmaps.size()) * sizeof(RemoteMap)),
                 "cudaMalloc");
-    if (!flat.empty())
-      WS_CUDA_TRY(cudaMemcpy(c->d_rmaps, flat.data(), flat.size() * sizeof(RemoteMap),
-                             cudaMemcpyHostToDevice), "H2D");
     WS_CUDA_TRY(cudaMalloc(&c->d_rseg_first, first.size() * 4), "cudaMalloc");
     WS_CUDA_TRY(cudaMemcpy(c->d_rseg_first, first.data(), first.size() * 4,
                            cudaMemcpyHostToDevice), "H2D");
   }
   // rounds of my segments / entries (sender side)
-  c->R = R;
   {
     const std::vector<int> sr = segment_rounds(plan_, me, R, tile);
     const auto& segs = plan_.segments();
@@ -468,8 +556,7 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
       for (int e = (int)mine.size() - 1; e >= 0; --e)
         if (sr[plan_.routes_of(me)[mine[e]].seg] >= r) c->ent_first[r] = e;
   }
-  // receiver: my regions, per round
-  const RecvLayout& L = lay[me];
+  // receiver: which sources send in which round (region offsets: p2p_size)
   c->rr.assign(R, Comm::RoundRecv{});
   for (int r = 0; r < R; ++r) {
     Comm::RoundRecv& X = c->rr[r];
@@ -483,20 +570,15 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
       int q = 0;
       for (int g : c->dests[k]) X.dest_rank[k][q++] = g;
     }
-    std::vector<RecvEntry> re;
     for (int j = 0; j < (int)L.entries.size(); ++j)
       if (L.round[j] == r) {
-        re.push_back(RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first});
+        ++X.n;
         X.mask |= 1u << L.entries[j].first;
       }
-    X.n = (int)re.size();
     P.expect_mask |= X.mask;
-    WS_CUDA_TRY(cudaMalloc(&X.d_rentries, std::max<size_t>(1, re.size()) * sizeof(RecvEntry)),
+    WS_CUDA_TRY(cudaMalloc(&X.d_rentries, std::max<size_t>(1, X.n) * sizeof(RecvEntry)),
                 "cudaMalloc");
-    if (!re.empty())
-      WS_CUDA_TRY(cudaMemcpy(X.d_rentries, re.data(), re.size() * sizeof(RecvEntry),
-                             cudaMemcpyHostToDevice), "H2D");
-    WS_CUDA_TRY(cudaMalloc(&X.d_units, (re.size() + 1) * 8), "cudaMalloc");
+    WS_CUDA_TRY(cudaMalloc(&X.d_units, (X.n + 1) * 8), "cudaMalloc");
   }
   if (R > 1) {
     int lo = 0, hi = 0;
@@ -511,121 +593,127 @@ ws_status ws_engine::init_p2p(const std::vector<uint64_t>& send_full,
   }
   P.edest = c->d_edest;
   P.ent_cnt = c->d_ent_cnt;
-  P.recv = static_cast<char*>(c->d_p2p) + L.head;
-  P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_p2p) + kMailboxBytes);
+  P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_head) + kMailboxBytes);
   P.err = c->d_err;
+#ifdef WSYNC_ABLATIONS
   if (const char* d = getenv("WSYNC_P2P_DEBUG")) P.debug = atoi(d);
+#endif
   c->nsend_entries = (int)mine.size();
   WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "memset");
   c->p2p = true;
   return WS_OK;
 }
 
-namespace {
-
-// Base of the allocation holding `p` (driver entry point; the library does
-// not link libcuda).  IPC handles are per allocation, and the serving arena
-// may be a view into a larger caller allocation.
-bool allocation_base(void* p, void** base) {
-  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static Fn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<Fn>(f);
-  }();
-  if (!fn) return false;
-  CUdeviceptr b = 0;
-  size_t sz = 0;
-  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
-  *base = reinterpret_cast<void*>(b);
-  return true;
+// (Re)sizes every rank's receive regions for syncs with density threshold
+// <= t (t >= 1: the worst case, every routed element a record) and rebuilds
+// the tables that point into them.  Collective; every rank's earlier syncs
+// are complete before any region is freed.
+ws_status ws_engine::p2p_size(double t) {
+  Comm* c = comm_;
+  const int me = c->rank, W = c->world, R = c->R;
+  const size_t wb = wire_bytes(dtype_);
+  const uint32_t tile = encode_tile_elems(dtype_);
+  int ok = cudaDeviceSynchronize() == cudaSuccess;
+  ws_status st = c->fab->all_min(&ok);  // every rank's syncs so far are done
+  if (st != WS_OK) return st;
+  if (!ok) return set_error(WS_CUDA, "p2p: a rank failed before resizing its receive regions");
+  c->release_peers(c->peer_rec);
+  cudaFree(c->d_rec);
+  c->d_rec = nullptr;
+  c->sized_t = -1.0;
+  std::vector<RecvLayout> lay(W);
+  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q, R, tile, t);
+  const size_t bytes = std::max<uint64_t>(1, lay[me].records) * wb;
+  ok = cudaMalloc(&c->d_rec, bytes) == cudaSuccess;
+  cudaGetLastError();
+  st = c->fab->all_min(&ok);
+  if (st != WS_OK || !ok) {
+    cudaFree(c->d_rec);
+    c->d_rec = nullptr;
+    return st != WS_OK ? st
+                       : set_error(WS_CAPACITY, "p2p: receive regions for density_threshold " +
+                                                    std::to_string(t) + " do not fit (" +
+                                                    std::to_string(bytes) + " bytes on rank " +
+                                                    std::to_string(me) + ")");
+  }
+  st = c->fab->share(c->d_rec, &c->peer_rec);
+  if (st != WS_OK) return st;
+  // sender: each of my remote entries' region at every replica of its coordinate
+  const std::vector<int>& mine = c->mine;
+  std::vector<EntryDest> ed(std::max<size_t>(1, mine.size()));
+  for (int e = 0; e < (int)mine.size(); ++e) {
+    EntryDest& D = ed[e];
+    std::memset(&D, 0, sizeof(D));
+    const Route& rt = plan_.routes_of(me)[mine[e]];
+    D.cap = entry_capacity(plan_, me, rt, t);
+    int r = 0;
+    for (int q : c->dests[rt.coord]) {
+      const RecvLayout& Lq = lay[q];
+      int pos = -1;
+      for (int j = 0; j < (int)Lq.entries.size(); ++j)
+        if (Lq.entries[j].first == me && Lq.entries[j].second == e) pos = j;
+      if (pos < 0) return set_error(WS_TRANSFER_ERROR, "p2p: entry missing from a receiver layout");
+      D.rec[r] = static_cast<char*>(c->peer_rec[q]) + Lq.off[pos] * wb;
+      D.cnt[r] = reinterpret_cast<uint32_t*>(static_cast<char*>(c->peer_head[q]) + kMailboxBytes) +
+                 pos;
+      ++r;
+    }
+  }
+  WS_CUDA_TRY(cudaMemcpy(c->d_edest, ed.data(), ed.size() * sizeof(EntryDest),
+                         cudaMemcpyHostToDevice), "H2D");
+  c->edest = ed;
+  for (size_t i = 0; i < c->rmaps.size(); ++i) {
+    const EntryDest& D = ed[c->rmap_entry[i]];
+    c->rmaps[i].cap = D.cap;
+    for (int r = 0; r < kMaxReplicas && r < 8; ++r) c->rmaps[i].rec[r] = D.rec[r];
+  }
+  if (!c->rmaps.empty())
+    WS_CUDA_TRY(cudaMemcpy(c->d_rmaps, c->rmaps.data(), c->rmaps.size() * sizeof(RemoteMap),
+                           cudaMemcpyHostToDevice), "H2D");
+  // receiver: my regions, per round
+  const RecvLayout& L = lay[me];
+  for (int r = 0; r < R; ++r) {
+    std::vector<RecvEntry> re;
+    for (int j = 0; j < (int)L.entries.size(); ++j)
+      if (L.round[j] == r)
+        re.push_back(RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first});
+    if (!re.empty())
+      WS_CUDA_TRY(cudaMemcpy(c->rr[r].d_rentries, re.data(), re.size() * sizeof(RecvEntry),
+                             cudaMemcpyHostToDevice), "H2D");
+  }
+  c->pargs.recv = c->d_rec;
+  c->sized_t = t;
+  return WS_OK;
 }
 
-struct ServeHandle {
-  cudaIpcMemHandle_t h;
-  uint64_t offset;
-  uint64_t ok;
-};
-
-}  // namespace
-
 // Maps the serving arena of every replica of the coordinates this rank sends
-// to, so dense-fallback boxes are stored straight into them (pack kernel).
+// to, so dense-fallback boxes are stored straight into them (pack kernel),
+// then sizes the receive regions: for the density threshold when dense boxes
+// go direct (records only for sparse shards), for the worst case otherwise.
 // Any rank failing (e.g. a virtual-memory allocation without an IPC handle)
-// turns the direct path off everywhere; dense boxes then travel as records.
+// turns the direct path off everywhere.  Collective.
 ws_status ws_engine::map_serve() {
   Comm* c = comm_;
   if (!c || !c->p2p || !serve) return WS_OK;
-  const int me = c->rank, W = c->world;
-  for (void* p : c->peer_serve_map)
-    if (p) cudaIpcCloseMemHandle(p);
-  c->peer_serve_map.assign(W, nullptr);
-  c->pargs.dense_direct = 0;
-  ServeHandle mine{};
-  void* base = nullptr;
-  if (allocation_base(serve, &base) && cudaIpcGetMemHandle(&mine.h, base) == cudaSuccess) {
-    mine.offset = static_cast<char*>(serve) - static_cast<char*>(base);
-    mine.ok = 1;
-  }
-  cudaGetLastError();
-  ServeHandle* d_h = nullptr;
-  WS_CUDA_TRY(cudaMalloc(&d_h, (size_t)W * sizeof(ServeHandle)), "cudaMalloc");
-  WS_CUDA_TRY(cudaMemcpy(d_h + me, &mine, sizeof(mine), cudaMemcpyHostToDevice), "H2D");
-  cudaStream_t s0;
-  WS_CUDA_TRY(cudaStreamCreate(&s0), "stream");
-  ncclResult_t nr = ncclAllGather(d_h + me, d_h, sizeof(ServeHandle), ncclUint8, c->comm, s0);
-  cudaStreamSynchronize(s0);
-  std::vector<ServeHandle> all(W);
-  cudaMemcpy(all.data(), d_h, (size_t)W * sizeof(ServeHandle), cudaMemcpyDeviceToHost);
-  if (nr != ncclSuccess) {
-    cudaStreamDestroy(s0);
-    cudaFree(d_h);
-    return set_error(WS_NCCL, "map_serve: handle all-gather failed");
-  }
-  int ok = 1;
-  for (int g = 0; g < W; ++g) ok &= all[g].ok ? 1 : 0;
-  std::vector<char> needed(W, 0);
-  for (int k = 0; k < c->coords; ++k)
-    for (int g : c->dests[k]) needed[g] = 1;
-  for (int g = 0; g < W && ok; ++g) {
-    if (g == me || !needed[g]) continue;
-    void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, all[g].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      ok = 0;
-      break;
-    }
-    c->peer_serve_map[g] = p;
-  }
-  // agree (all-reduce min over the flags, reusing the handle buffer)
-  int* d_ok = reinterpret_cast<int*>(d_h);
-  cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice);
-  nr = ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, s0);
-  cudaStreamSynchronize(s0);
-  cudaStreamDestroy(s0);
-  cudaMemcpy(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost);
-  cudaFree(d_h);
-  if (nr != ncclSuccess) return set_error(WS_NCCL, "map_serve: agreement failed");
+  c->release_peers(c->peer_serve);
   P2PArgs& P = c->pargs;
   for (int k = 0; k < kMaxWorld; ++k)
     for (int r = 0; r < kMaxReplicas; ++r) P.serve_dst[k][r] = nullptr;
+  P.dense_direct = 0;
+  std::vector<void*> ps;
+  const bool ok = c->fab->share(serve, &ps) == WS_OK;
   const char* env = getenv("WSYNC_DENSE_DIRECT");
-  if (!ok || (env && env[0] == '0')) {
-    if (max_threshold() > 0.0)
-      return set_error(WS_CAPACITY, "WSYNC_MAX_THRESHOLD needs direct dense boxes, but a serving "
-                                    "arena is not IPC-mappable (or WSYNC_DENSE_DIRECT=0)");
-    return WS_OK;
+  if (ok) {
+    c->peer_serve = ps;
+    if (!(env && env[0] == '0')) {
+      for (int k = 0; k < c->coords; ++k) {
+        int r = 0;
+        for (int g : c->dests[k]) P.serve_dst[k][r++] = c->peer_serve[g];
+      }
+      P.dense_direct = 1;
+    }
   }
-  for (int k = 0; k < c->coords; ++k) {
-    int r = 0;
-    for (int g : c->dests[k])
-      P.serve_dst[k][r++] = static_cast<char*>(c->peer_serve_map[g]) + all[g].offset;
-  }
-  P.dense_direct = 1;
-  return WS_OK;
+  return p2p_size(P.dense_direct ? c->want_t : 1.0);
 }
 
 // (Re)allocates the send regions with the given per-coordinate capacities.
@@ -664,12 +752,21 @@ void ws_engine::destroy_comm() {
   comm_ = nullptr;
 }
 
-ws_status ws_engine::exchange_admit(const ws_sync_options& o) const {
+// True when a sync with these options needs larger receive regions.
+bool ws_engine::exchange_needs_resize(const ws_sync_options& o) const {
   const Comm* c = comm_;
-  if (c && c->p2p && max_threshold() > 0.0 && o.sparse && o.density_threshold > max_threshold())
-    return set_error(WS_INVALID_ARGUMENT,
-                     "density_threshold above the exchange sizing (WSYNC_MAX_THRESHOLD)");
-  return WS_OK;
+  return c && c->p2p && c->pargs.dense_direct && o.sparse &&
+         std::min(1.0, o.density_threshold) > c->sized_t;
+}
+
+// Grows the receive regions (collectively) before a sync whose density
+// threshold exceeds what they were sized for.  Every rank calls this with
+// the same options (as every rank passes the same SyncOptions).
+ws_status ws_engine::exchange_prepare(const ws_sync_options& o) {
+  if (!exchange_needs_resize(o)) return WS_OK;
+  Comm* c = comm_;
+  c->want_t = std::min(1.0, std::max(c->want_t, o.density_threshold));
+  return p2p_size(c->want_t);
 }
 
 ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
@@ -720,26 +817,14 @@ ws_status ws_engine::exchange_fuse_k1(EncodeArgs& a, cudaStream_t s) {
   return WS_OK;
 }
 
-// One P2P exchange round: pack this round's remote entries (records into the
-// replicas' regions, dense boxes into their serving arenas), publish, and
-// apply what the sources sent for this round.  No host synchronisation.
-ws_status ws_engine::exchange_round(const ws_sync_options& o, int next_arena, int round,
-                                    cudaStream_t s, uint32_t* launches) {
+// One P2P exchange round, sender side: pack this round's remote entries
+// (records into the replicas' regions, dense boxes into their serving
+// arenas) and publish.  No host synchronisation.
+ws_status ws_engine::exchange_pack(const ws_sync_options& o, int next_arena, int round,
+                                   cudaStream_t s, uint32_t* launches) {
   Comm* c = comm_;
-  const Comm::RoundRecv& X = c->rr[round];
   const int e0 = c->ent_first[round], ne = c->ent_first[round + 1] - e0;
-  P2PArgs P = c->pargs;
-  P.round = round;
-  P.epoch = (uint32_t)(c->R * c->step + round);
-  P.prev_epoch = c->step > 1 ? (uint32_t)(c->R * (c->step - 1) + round) : 0u;
-  for (int k = 0; k < kMaxWorld; ++k)
-    for (int q = 0; q < kMaxReplicas; ++q) P.dest_rank[k][q] = X.dest_rank[k][q];
-  P.edest = c->d_edest + e0;
-  P.ent_cnt = c->d_ent_cnt + e0;
-  P.rentries = X.d_rentries;
-  P.nrecv = X.n;
-  P.recv_units = X.d_units;
-  P.expect_mask = X.mask;
+  const P2PArgs P = round_args(round);
   if (ne && !c->k1_emit)
     WS_CUDA_TRY(cudaMemsetAsync(c->d_ent_cnt + e0, 0, ne * 4, s), "memset");
   PackArgs pa{};
@@ -765,10 +850,51 @@ ws_status ws_engine::exchange_round(const ws_sync_options& o, int next_arena, in
   pa.p2p = P;
   WS_CUDA_TRY(launch_pack(dtype_, pa, route_grid_, s), "pack (p2p)");
   if (ne) *launches += 2;
-  if (X.mask) {
-    WS_CUDA_TRY(launch_apply_p2p(dtype_, P, serve, sm_count() * 4, s), "apply (p2p)");
-    *launches += 2;
-  }
+  return WS_OK;
+}
+
+// Receiver side of a round: apply what the sources sent for it, then ack.
+ws_status ws_engine::exchange_apply(int round, cudaStream_t s, uint32_t* launches) {
+  Comm* c = comm_;
+  if (!c->rr[round].mask) return WS_OK;
+  WS_CUDA_TRY(launch_apply_p2p(dtype_, round_args(round), serve, sm_count() * 4, s),
+              "apply (p2p)");
+  *launches += 2;
+  return WS_OK;
+}
+
+P2PArgs ws_engine::round_args(int round) const {
+  const Comm* c = comm_;
+  const Comm::RoundRecv& X = c->rr[round];
+  const int e0 = c->ent_first[round];
+  P2PArgs P = c->pargs;
+  P.round = round;
+  P.epoch = (uint32_t)(c->R * c->step + round);
+  P.prev_epoch = c->step > 1 ? (uint32_t)(c->R * (c->step - 1) + round) : 0u;
+  for (int k = 0; k < kMaxWorld; ++k)
+    for (int q = 0; q < kMaxReplicas; ++q) P.dest_rank[k][q] = X.dest_rank[k][q];
+  P.edest = c->d_edest + e0;
+  P.ent_cnt = c->d_ent_cnt + e0;
+  P.rentries = X.d_rentries;
+  P.nrecv = X.n;
+  P.recv_units = X.d_units;
+  P.expect_mask = X.mask;
+  return P;
+}
+
+ws_status ws_engine::exchange_round(const ws_sync_options& o, int next_arena, int round,
+                                    cudaStream_t s, uint32_t* launches) {
+  ws_status st = exchange_pack(o, next_arena, round, s, launches);
+  return st != WS_OK ? st : exchange_apply(round, s, launches);
+}
+
+// Queues the read-back of the exchange's device fault word (checked by the
+// next synchronising call).
+ws_status ws_engine::exchange_end(cudaStream_t s) {
+  Comm* c = comm_;
+  if (!c) return WS_OK;
+  if (c->p2p) pulled_bytes_ = 0;
+  WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
   return WS_OK;
 }
 
@@ -827,8 +953,8 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
     WS_CUDA_TRY(cudaEventRecord(c->ev_xdone, xs), "event");
     WS_CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_xdone, 0), "wait");
   }
-  pulled_bytes_ = 0;
-  WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, ks), "D2H err");
+  st = exchange_end(ks);
+  if (st != WS_OK) return st;
   WS_CUDA_TRY(cudaEventRecord(c->ev_encdone, ks), "event");
   WS_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_encdone, 0), "wait");
   return WS_OK;
@@ -844,9 +970,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
       ws_status st = exchange_round(o, next_arena, r, s, launches);
       if (st != WS_OK) return st;
     }
-    pulled_bytes_ = 0;
-    WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
-    return WS_OK;
+    return exchange_end(s);
   }
   // 1. pack
   WS_CUDA_TRY(cudaMemsetAsync(c->d_region_cnt, 0, c->coords * 8, s), "memset");
@@ -939,8 +1063,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   if (recv_total) *launches += 1;
   pulled_bytes_ = recv_total * wb;
   pushed_wire_bytes_ = sent;
-  WS_CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 4, cudaMemcpyDeviceToHost, s), "D2H err");
-  return WS_OK;
+  return exchange_end(s);
 }
 
 // Device-side exchange faults of the syncs so far (sticky in P2P mode), read
@@ -960,17 +1083,27 @@ ws_status ws_engine::exchange_status() const {
 // appears exactly once in the layout of each replica of its coordinate, in
 // the round of its segment; a receiver expects a source in round r exactly
 // when that source sends it something in round r; the mailbox fits.
+static ws_status check_exchange(const Plan& plan, int rounds, double t);
+
 extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
   if (!plan_h || rounds < 1 || rounds > kMaxRounds)
     return set_error(WS_INVALID_ARGUMENT, "ws_plan_check_exchange: bad argument");
-  const Plan& plan = *plan_h->p;
+  // the worst-case regions and the ones bounded by the default threshold
+  for (double t : {1.0, kDefaultThreshold}) {
+    ws_status st = check_exchange(*plan_h->p, rounds, t);
+    if (st != WS_OK) return st;
+  }
+  return WS_OK;
+}
+
+static ws_status check_exchange(const Plan& plan, int rounds, double t) {
   const int W = plan.world(), R = rounds;
   if (W > kMaxWorld) return set_error(WS_INVALID_ARGUMENT, "world beyond kMaxWorld");
   if ((size_t)(W + R * (2 * W + 2)) * 8 > kMailboxBytes)
     return set_error(WS_CAPACITY, "mailbox too small for this world and round count");
   const uint32_t tile = encode_tile_elems(plan.dtype());
   std::vector<RecvLayout> lay(W);
-  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan, q, R, tile);
+  for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan, q, R, tile, t);
   // expectation per (receiver, round) from the layouts
   std::vector<std::vector<uint32_t>> expect(W, std::vector<uint32_t>(R, 0));
   for (int q = 0; q < W; ++q)
@@ -994,7 +1127,7 @@ extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
             ++hits;
             if (lay[q].round[j] != round)
               return set_error(WS_TRANSFER_ERROR, "entry round differs at a receiver");
-            if (lay[q].cap[j] != entry_capacity(plan, g, rt))
+            if (lay[q].cap[j] != entry_capacity(plan, g, rt, t))
               return set_error(WS_TRANSFER_ERROR, "entry capacity differs at a receiver");
           }
         if (hits != 1) return set_error(WS_TRANSFER_ERROR, "entry missing or duplicated at a receiver");
@@ -1008,6 +1141,57 @@ extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
         if (((expect[q][r] >> g) & 1u) != ((sends[g][r] >> q) & 1u))
           return set_error(WS_TRANSFER_ERROR, "expectation and destinations disagree");
   return WS_OK;
+}
+
+// Bytes of the last sync that crossed to / arrived from other GPUs: wire
+// records stored into the replicas' receive regions (one copy per replica),
+// dense boxes stored straight into their serving arenas, and the records
+// the sources published into this rank's regions.  Synchronises.
+ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense,
+                                    uint64_t* recv_records) {
+  *sent_records = *sent_dense = *recv_records = 0;
+  Comm* c = comm_;
+  if (!c) return WS_OK;
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  if (!c->p2p) {
+    *sent_records = pushed_wire_bytes_;
+    *recv_records = pulled_bytes_;
+    return WS_OK;
+  }
+  const size_t wb = wire_bytes(dtype_), esz = dtype_size(dtype_);
+  const int ne = (int)c->mine.size();
+  std::vector<uint32_t> cnt(std::max(1, ne));
+  std::vector<uint64_t> nnz(std::max(1, nseg_)), cap(std::max(1, nseg_));
+  if (ne) WS_CUDA_TRY(cudaMemcpy(cnt.data(), c->d_ent_cnt, ne * 4, cudaMemcpyDeviceToHost), "D2H");
+  if (nseg_) {
+    WS_CUDA_TRY(cudaMemcpy(nnz.data(), d_nnz_, nseg_ * 8, cudaMemcpyDeviceToHost), "D2H");
+    WS_CUDA_TRY(cudaMemcpy(cap.data(), d_cap_, nseg_ * 8, cudaMemcpyDeviceToHost), "D2H");
+  }
+  for (int e = 0; e < ne; ++e) {
+    const Route& rt = plan_.routes()[c->mine[e]];
+    int nrep = 0;
+    while (nrep < kMaxReplicas && c->edest[e].rec[nrep]) ++nrep;
+    const bool dense = !last_sparse_ || nnz[rt.seg] > cap[rt.seg];
+    if (dense && c->pargs.dense_direct)
+      *sent_dense += rt.overlap * esz * nrep;
+    else
+      *sent_records += (uint64_t)std::min<uint64_t>(cnt[e], c->edest[e].cap) * wb * nrep;
+  }
+  const RecvLayout L = recv_layout(plan_, c->rank, c->R, encode_tile_elems(dtype_), c->sized_t);
+  std::vector<uint32_t> rc(std::max<size_t>(1, L.entries.size()));
+  if (!L.entries.empty())
+    WS_CUDA_TRY(cudaMemcpy(rc.data(), static_cast<char*>(c->d_head) + kMailboxBytes,
+                           L.entries.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+  for (size_t j = 0; j < L.entries.size(); ++j) *recv_records += (uint64_t)rc[j] * wb;
+  return WS_OK;
+}
+
+extern "C" ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records,
+                                              uint64_t* sent_dense, uint64_t* recv_records) {
+  if (!eng || !sent_records || !sent_dense || !recv_records)
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_exchange_bytes: null argument");
+  return eng->exchange_bytes(sent_records, sent_dense, recv_records);
 }
 
 extern "C" ws_status ws_nccl_unique_id(uint8_t out[128]) {

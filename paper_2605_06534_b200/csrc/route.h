@@ -14,6 +14,23 @@ constexpr uint32_t kTilesPerUnit = 8;    // super-tiles of records per work unit
 constexpr uint64_t kStreamDiv = 10;  // measured: fused RMW wins at 10%, streaming at 20%
 constexpr uint64_t kCopyChunk = 65536;   // elements per dense-copy work unit
 
+// SyncOptions::density_threshold's default (engine.hpp:27): what the P2P
+// receive regions are sized for until a sync asks for more.
+constexpr double kDefaultThreshold = 0.20;
+
+// The largest record count k of an n-element shard with k / n <= t: one more
+// change makes the shard dense (engine.cpp:121, inclusive).  This is a
+// segment's record capacity, and the most records a sparse shard can send.
+inline uint64_t sparse_capacity(uint64_t n, double t) {
+  if (!n || !(t > 0.0)) return 0;
+  if (t >= 1.0) return n;
+  uint64_t c = (uint64_t)(t * (double)n);
+  if (c > n) c = n;
+  while (c < n && (double)(c + 1) / (double)n <= t) ++c;
+  while (c > 0 && (double)c / (double)n > t) --c;
+  return c;
+}
+
 // One (trainer segment -> serving shard) route whose destination is resident
 // on this GPU.  Sparse records map through `identity` (flat shift with a keep
 // window, the same-dim dim-0 case) or the general box `map`; dense segments

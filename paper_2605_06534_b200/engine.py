@@ -109,7 +109,8 @@ def nccl_unique_id() -> bytes:
 class TransferEngine:
     """One rank's engine.  Arenas are torch CUDA tensors owned here."""
 
-    def __init__(self, plan: Plan, device=None, unique_id: bytes | None = None):
+    def __init__(self, plan: Plan, device=None, unique_id: bytes | None = None, group=None):
+        self.h = None
         self.plan = plan
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None
                                    else device)
@@ -123,14 +124,22 @@ class TransferEngine:
         if unique_id is not None:
             uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         h = C.c_void_p()
-        check(lib.ws_engine_create(plan.h, self.device.index, uid, C.byref(h)))
+        if group is not None:
+            check(lib.ws_engine_create_grouped(plan.h, self.device.index, group.h, C.byref(h)))
+        else:
+            check(lib.ws_engine_create(plan.h, self.device.index, uid, C.byref(h)))
         self.h = h
         check(lib.ws_engine_bind(h, self.arena[0].data_ptr(), self.arena[1].data_ptr(),
                                  self.serve.data_ptr()))
 
+    def close(self):
+        if self.h is not None:
+            lib.ws_engine_destroy(self.h)
+            self.h = None
+
     def __del__(self):
         try:
-            lib.ws_engine_destroy(self.h)
+            self.close()
         except Exception:
             pass
 
@@ -187,6 +196,14 @@ class TransferEngine:
         with torch.cuda.device(self.device):
             check(lib.ws_engine_timing(self.h, int(reset), C.byref(t)))
         return t.as_dict()
+
+    def exchange_bytes(self):
+        """NVLink bytes of the last sync on this rank: (records sent, dense
+        boxes sent, records received) -- ws_engine_exchange_bytes."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_exchange_bytes(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"sent_records": a.value, "sent_dense": b.value, "recv_records": c.value}
 
     def segment_payload(self, i, force_wide_index=False):
         """Segment i's payload from the last sync in the reference wire format
@@ -251,6 +268,61 @@ class TransferEngine:
         k = nnz.value if c == "S" else 0
         return SparseDelta(self.plan.dtype, shp, _wrap(idx.value, k, torch.int32, self.device),
                            _wrap(val.value, k, VAL_DTYPE[self.plan.dtype], self.device)), c, nnz.value
+
+
+class EngineGroup:
+    """Every rank of a multi-GPU layout as an engine of THIS process on one
+    GPU (ws_group, include/wsync.h): the ranks share mailboxes, receive
+    regions and serving arenas as plain device pointers, and one group sync
+    runs all ranks' kernels -- K1, the local route, the NVLink pack
+    (pack_kernel) and the receive-side apply (apply_p2p_kernel) -- phase by
+    phase on one stream.  It is the multi-GPU data path of any layout
+    (TrainConfig{tp,pp,dp} -> ServeConfig{tp,pp} x replicas, FSDP, EP) on a
+    single device, which is how the parity tests run it on one B200."""
+
+    def __init__(self, manifest, dtype, train: TrainConfig, serve: ServeConfig, world: int,
+                 device=None):
+        self.world = world
+        self.plans = [Plan(manifest, dtype, train, serve, world=world, rank=r)
+                      for r in range(world)]
+        h = C.c_void_p()
+        check(lib.ws_group_create(world, C.byref(h)))
+        self.h = h
+        self.engines = []
+        try:
+            for plan in self.plans:
+                self.engines.append(TransferEngine(plan, device, group=self))
+            with torch.cuda.device(self.engines[0].device):
+                check(lib.ws_group_connect(h))
+        except Exception:
+            self.close()
+            raise
+
+    def generate(self, seed=1, density=0.01, expert_zipf=None, perm_seed=0):
+        for e in self.engines:
+            e.generate(seed=seed, density=density, expert_zipf=expert_zipf, perm_seed=perm_seed)
+
+    def sync_step(self, sparse=True, density_threshold=0.20, reverse=False, report=True,
+                  stream=None):
+        """One sync of every rank (ws_group_sync_step); per-rank reports."""
+        o = _lib.SyncOptions(int(sparse), density_threshold, int(reverse))
+        reps = (_lib.Report * self.world)() if report else None
+        with torch.cuda.device(self.engines[0].device):
+            check(lib.ws_group_sync_step(self.h, C.byref(o), _stream(stream), reps))
+        return [r.as_dict() for r in reps] if report else None
+
+    def close(self):
+        for e in getattr(self, "engines", []):
+            e.close()
+        if getattr(self, "h", None) is not None:
+            lib.ws_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _stream(stream=None):

@@ -23,3 +23,22 @@ def test_reference_arm_line():
     assert line["warmup"] == 1 and line["steps"] == 1
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_reference_arm_never_maps_libwsync():
+    """The reference arm must run the reference alone: the model shapes come
+    from manifest.py loaded by path, never through the package (whose
+    __init__ maps libwsync.so)."""
+    code = ("import sys; sys.argv = ['bench.py']; sys.path.insert(0, %r)\n"
+            "import importlib.util\n"
+            "spec = importlib.util.spec_from_file_location('bench', %r)\n"
+            "b = importlib.util.module_from_spec(spec); spec.loader.exec_module(b)\n"
+            "mf = b.load_manifest_module(); assert mf.MODELS['qwen3-8b']()\n"
+            "from oracle.oracle import Reference\n"
+            "try:\n    Reference()\nexcept OSError:\n    pass\n"
+            "print(open('/proc/self/maps').read().count('libwsync'))\n"
+            % (ROOT, os.path.join(ROOT, "bench.py")))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert p.stdout.strip().splitlines()[-1] == "0"

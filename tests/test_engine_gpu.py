@@ -158,12 +158,13 @@ def test_matches_reference_engine(reference, dtype, density, sparse):
         assert bits(eng.serve_view(s)).tobytes() == want.tobytes(), plan.manifest[p].name
 
 
-def _check_segment_on_device(eng, i):
+def _check_segment_on_device(eng, i, reverse=False):
     """Size-independent properties of segment i's delta stream, checked with
     plain torch ops: ascending unique indices, exactly the changed positions,
-    values = next - prev (u16 wrap)."""
-    prev = eng.segment_view(i, 0).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
-    nxt = eng.segment_view(i, 1).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
+    values = next - prev (u16 wrap; the snapshots swap roles when reverse)."""
+    a, b = (1, 0) if reverse else (0, 1)
+    prev = eng.segment_view(i, a).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
+    nxt = eng.segment_view(i, b).reshape(-1).view(torch.int16).to(torch.int32) & 0xFFFF
     changed = torch.nonzero(prev != nxt).flatten()
     delta, codec, nnz = eng.segment_delta(i)
     assert nnz == changed.numel()
@@ -283,3 +284,45 @@ def test_streamed_apply_adds_delta(density):
         else:
             assert torch.equal(got, (before[i] + q - p) & 0xFFFF), i
     assert rep["dense_shards"] == dense
+
+
+def test_qwen3_8b_whole_model_bench_config(restatement):
+    """The configuration the headline number comes from (bench.py, BASELINE
+    config 2 at N = 1): the whole Qwen3-8B (8.19 G elements, 399 segments),
+    FSDP1 -> TP1, 1% density, four alternating syncs.  From the second sync
+    on K1 runs its streamed-apply instantiation (the first sync's density,
+    1% >= 1/250, selects it) -- the one the bench times.  After the first
+    and the last sync every segment's compacted record stream and every
+    serving shard is checked on the device; the largest segment (the
+    622 M-element embedding) and the smallest against the C oracle."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.MODELS["qwen3-8b"]())
+    assert plan.info.model_elems == 8_190_735_360
+    eng.generate(seed=1, density=0.01)
+    sizes = [n for (_, _, _, n) in plan.segments]
+    variants = []
+    for k in range(4):
+        rev = bool(k % 2)
+        rep = eng.sync_step(reverse=rev)
+        variants.append(rep["streamed_apply"])
+        assert rep["dense_shards"] == 0
+        if k not in (0, 3):
+            continue
+        torch.cuda.synchronize()
+        total = 0
+        for i in range(len(plan.segments)):
+            total += _check_segment_on_device(eng, i, reverse=rev)
+            want = eng.segment_view(i, 0 if rev else 1).view(torch.int16)
+            assert torch.equal(eng.serve_view(i).view(torch.int16), want), i
+        assert rep["nnz"] == total
+        for i in (sizes.index(max(sizes)), sizes.index(min(sizes))):
+            p, desc, off, n = plan.segments[i]
+            meta = plan.manifest[p]
+            pv, nx = restatement.gen_pair_bf16(1, meta.name, meta.shape, desc, 0.01)
+            wi, wv = restatement.diff_shards(BF16, nx, pv) if rev else \
+                restatement.diff_shards(BF16, pv, nx)
+            delta, codec, nnz = eng.segment_delta(i)
+            assert codec == "S" and nnz == wi.size
+            assert np.array_equal(delta.indices.cpu().numpy().view(np.uint32), wi)
+            assert delta.values.cpu().numpy().view(np.uint16).tobytes() == wv.tobytes()
+    assert variants[1:] == [1, 1, 1], variants
