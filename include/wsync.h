@@ -109,7 +109,7 @@ ws_status ws_diff_shards(ws_dtype dtype, const void* prev_dev,
 /* K4, replaces apply_delta (codec.hpp:41, codec.cpp:65-92): target[idx[k]]
  * += val[k] (F32 IEEE add; I32/BF16 wrap-around add).  The record count is
  * read from nnz_dev when non-null (nnz is then an upper bound that sizes the
- * launch; pass 0 if unknown), else nnz.  All indices are validated
+ * launch; 0 = unknown, a full-device grid), else nnz.  All indices are validated
  * before any write; an index >= n sets WS_ERRBIT_INDEX_OUT_OF_SHARD in
  * err_dev and leaves target unchanged. */
 ws_status ws_apply_delta(ws_dtype dtype, void* target_dev, uint64_t n,
@@ -424,6 +424,11 @@ ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step, const ws_sync_opti
                                const ws_relay_options* relay_opts, const ws_relay* relay,
                                ws_relay_report* report);
 
+/* Frees what ws_engine_sync_relay keeps across calls (device and pinned
+ * staging at the dense bound of the largest shard, the decode scratch pool);
+ * the next relay sync allocates it again. */
+ws_status ws_engine_release_staging(ws_engine* eng);
+
 /* Segment i's payload from the last sync in the reference wire format
  * (sparse if it was sent sparse, else the dense `next` snapshot), written to
  * out_dev when non-null (8-byte aligned, info->total_bytes long).
@@ -472,6 +477,10 @@ typedef struct ws_timing {
   uint32_t steps;
   uint32_t kernel_launches; /* libwsync kernels launched by those syncs */
   double wall_s, encode_s, route_s, apply_s;
+  /* the pack (NVLink stores) part of route_s, summed over the last
+   * pack_steps syncs (single-round P2P exchange; 0 otherwise) */
+  uint32_t pack_steps;
+  double pack_s;
 } ws_timing;
 ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out);
 

@@ -124,7 +124,8 @@ class Report(C.Structure):  # ws_report
 
 class Timing(C.Structure):  # ws_timing
     _fields_ = [("steps", C.c_uint32), ("kernel_launches", C.c_uint32), ("wall_s", C.c_double),
-                ("encode_s", C.c_double), ("route_s", C.c_double), ("apply_s", C.c_double)]
+                ("encode_s", C.c_double), ("route_s", C.c_double), ("apply_s", C.c_double),
+                ("pack_steps", C.c_uint32), ("pack_s", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -224,6 +225,7 @@ _SIGS = {
     "ws_engine_timing": ([_vp, C.c_int, C.POINTER(Timing)], C.c_int),
     "ws_engine_exchange_bytes": ([_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)],
                                  C.c_int),
+    "ws_engine_release_staging": ([_vp], C.c_int),
     "ws_group_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
     "ws_group_destroy": ([_vp], None),
     "ws_engine_create_grouped": ([_vp, C.c_int, _vp, C.POINTER(_vp)], C.c_int),

@@ -38,6 +38,8 @@ struct ws_engine {
   // cross-cluster sync through a relay (relay.cpp)
   ws_status sync_relay(uint64_t step, const ws_sync_options& o, const ws_relay_options& ro,
                        const ws_relay& relay, ws_relay_report* rep);
+  // frees sync_relay's staging and the cached wire scratch (ws_engine_release_staging)
+  ws_status release_staging();
   bool encode_only_ = false;  // sync_step: K1 only (no fused apply, no routes)
   // sync_relay's staging (device / pinned host) and streams, kept across calls
   std::vector<std::pair<void*, size_t>> relay_dev_, relay_host_;
@@ -176,12 +178,15 @@ struct ws_engine {
   uint64_t* d_unit_off_ = nullptr;
 
   // per-step stage events: [start, after H2D, after encode, after local
-  // apply, after exchange, end]; a ring so timed loops need no sync.
+  // apply, after exchange, end, after the pack (single-round exchange)]; a
+  // ring so timed loops need no sync.
   static constexpr int kRing = 256;
-  cudaEvent_t (*ring_)[6] = nullptr;
+  cudaEvent_t (*ring_)[7] = nullptr;
   uint32_t ring_steps_ = 0;    // steps recorded since reset
   uint32_t ring_head_ = 0;     // next slot
   uint32_t launch_total_ = 0;
+  uint32_t pack_steps_ = 0;    // steps since reset whose pack event was recorded
+  bool pack_ev_ = false;       // this step recorded ring slot 6
   cudaStream_t last_stream_ = nullptr;
   bool last_sparse_ = true;
   int last_next_arena_ = 1;

@@ -178,7 +178,7 @@ ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
                 "H2D");
   WS_CUDA_TRY(cudaMalloc(&d_unit_off_, (local.size() + 1) * 8), "cudaMalloc");
   route_grid_ = sm_count() * 8;
-  ring_ = new cudaEvent_t[kRing][6]();
+  ring_ = new cudaEvent_t[kRing][7]();
   for (int i = 0; i < kRing; ++i)
     for (auto& e : ring_[i]) WS_CUDA_TRY(cudaEventCreate(&e), "cudaEventCreate");
   // a group wires the exchange of all its ranks at once (ws_group_connect)
@@ -372,6 +372,7 @@ ws_status ws_engine::sync_begin(SyncCtx& x, const ws_sync_options& o, cudaStream
   x.na = 1 - x.pa;
   x.launches = 0;
   x.ev = ring_[ring_head_];
+  pack_ev_ = false;
   ring_head_ = (ring_head_ + 1) % kRing;
   ring_steps_ = std::min<uint32_t>(ring_steps_ + 1, kRing);
   last_stream_ = s;
@@ -430,6 +431,7 @@ ws_status ws_engine::sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host,
                 "D2H counts");
   WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
   launch_total_ += x.launches;
+  pack_steps_ = pack_ev_ ? pack_steps_ + 1 : 0;  // the most recent run of steps with one
   if (!nnz_host && !report) return WS_OK;
   WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
   ws_status st = exchange_status();
@@ -595,6 +597,7 @@ ws_status ws_engine::timing(int reset, ws_timing* out) {
   ws_timing t{};
   t.steps = ring_steps_;
   t.kernel_launches = launch_total_;
+  t.pack_steps = std::min(pack_steps_, ring_steps_);
   for (uint32_t k = 0; k < ring_steps_; ++k) {
     const cudaEvent_t* e = ring_[(ring_head_ + kRing - 1 - k) % kRing];
     float ms = 0;
@@ -606,10 +609,13 @@ ws_status ws_engine::timing(int reset, ws_timing* out) {
     t.apply_s += ms * 1e-3;
     cudaEventElapsedTime(&ms, e[3], e[4]);
     t.route_s += ms * 1e-3;
+    if (k < pack_steps_ && cudaEventElapsedTime(&ms, e[3], e[6]) == cudaSuccess)
+      t.pack_s += ms * 1e-3;
   }
   if (out) *out = t;
   if (reset) {
     ring_steps_ = 0;
+    pack_steps_ = 0;
     launch_total_ = 0;
   }
   return WS_OK;

@@ -967,7 +967,12 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   const size_t wb = wire_bytes(dtype_);
   if (c->p2p) {
     for (int r = 0; r < c->R; ++r) {
-      ws_status st = exchange_round(o, next_arena, r, s, launches);
+      ws_status st = exchange_pack(o, next_arena, r, s, launches);
+      if (st == WS_OK && r == c->R - 1) {  // the pack's share of the route stage
+        WS_CUDA_TRY(cudaEventRecord(ring_[(ring_head_ + kRing - 1) % kRing][6], s), "event");
+        pack_ev_ = true;
+      }
+      if (st == WS_OK) st = exchange_apply(r, s, launches);
       if (st != WS_OK) return st;
     }
     return exchange_end(s);

@@ -1083,7 +1083,8 @@ cudaError_t launch_apply(int dtype, void* target, uint64_t n, const uint32_t* id
                          uint32_t* err, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(err, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  const int grid = stream_grid(nnz, 256);
+  // count on the device and no bound given: a full grid (grid-stride loops)
+  const int grid = (nnz_dev && nnz == 0) ? sm_count() * 8 : stream_grid(nnz, 256);
   validate_kernel<<<grid, 256, 0, s>>>(idx, nnz, nnz_dev, n, err);
   switch (dtype) {
     case WS_BF16:

@@ -75,19 +75,22 @@ bool payload_total(const uint8_t* d, uint64_t n, uint64_t* total) {
   const int nd = d[5], iw = d[6];
   uint64_t pos = 8 + 8 * (uint64_t)nd, elems = 1;
   if (n < pos) return false;
+  constexpr uint64_t kMax = 1ull << 62;  // no payload is larger; keeps the products exact
   for (int k = 0; k < nd; ++k) {
     int64_t v;
     std::memcpy(&v, d + 8 + 8 * k, 8);
-    if (v <= 0) return false;
+    if (v <= 0 || (uint64_t)v > kMax / elems) return false;
     elems *= (uint64_t)v;
   }
   if (dense) {
+    if (elems > kMax / esz) return false;
     *total = pos + elems * esz;
     return true;
   }
-  if (n < pos + 8) return false;
+  if (n < pos + 8 || (iw != 4 && iw != 8)) return false;
   uint64_t nnz;
   std::memcpy(&nnz, d + pos, 8);
+  if (nnz > kMax / ((uint64_t)iw + esz)) return false;
   *total = pos + 8 + nnz * ((uint64_t)iw + esz);
   return true;
 }
@@ -224,7 +227,14 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   for (auto& p : stage) p = host_alloc(std::min<uint64_t>(B, max_payload));
   std::vector<cudaEvent_t> ev(depth);
   for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  bool staged = d_payload && d_seq_idx && d_seq_val;
+  for (auto* p : stage) staged = staged && p;
   auto pusher = [&] {
+    // (a fresh std::thread in Async mode: its current device is 0)
+    if (cudaSetDevice(device_) != cudaSuccess) {
+      fail(WS_CUDA, "sync_relay: pusher cudaSetDevice");
+      return;
+    }
     const auto t0 = Clock::now();
     for (size_t i = 0; i < segs.size() && first_err.st == WS_OK; ++i) {
       ws_payload_info info;
@@ -278,9 +288,50 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   uint32_t* d_ridx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
   void* d_rval = dev_alloc(max_cap * 4);
   uint64_t* d_rnnz = static_cast<uint64_t*>(dev_alloc(8));
-  uint32_t* d_err = static_cast<uint32_t*>(dev_alloc(4));
-  const size_t ws_bytes = ws_diff_workspace_bytes(max_cap);
+  uint32_t* d_err = static_cast<uint32_t*>(dev_alloc(8));
+  uint32_t* d_rerr = d_err ? d_err + 1 : nullptr;  // reslice's own error word
+  size_t ws_bytes = ws_diff_workspace_bytes(max_cap);
   void* d_ws = dev_alloc(ws_bytes);
+  staged = staged && h_payload && d_in && d_idx && d_val && d_ridx && d_rval && d_rnnz && d_err &&
+           d_ws;
+  if (!staged) {
+    for (auto& e : ev) cudaEventDestroy(e);
+    return set_error(WS_CUDA, "sync_relay: staging allocation failed");
+  }
+  // Record scratch beyond max_cap: a pusher with a higher density threshold
+  // than ours sends sparse payloads with more records (the reference decodes
+  // any size); grown per payload, freed at the end of the call.
+  struct Grown {
+    void* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    uint64_t cap = 0;
+    ~Grown() {
+      for (void* q : p) cudaFree(q);
+    }
+  } grown;
+  auto records_for = [&](uint64_t nnz) -> bool {
+    if (nnz <= max_cap) return true;
+    if (nnz > grown.cap) {
+      for (void*& q : grown.p) {
+        cudaFree(q);
+        q = nullptr;
+      }
+      grown.cap = 0;
+      const size_t sz[5] = {nnz * 4, nnz * 4, nnz * 4, nnz * 4, ws_diff_workspace_bytes(nnz)};
+      for (int k = 0; k < 5; ++k)
+        if (cudaMalloc(&grown.p[k], std::max<size_t>(16, sz[k])) != cudaSuccess) {
+          cudaGetLastError();
+          return false;
+        }
+      grown.cap = nnz;
+    }
+    d_idx = static_cast<uint32_t*>(grown.p[0]);
+    d_val = grown.p[1];
+    d_ridx = static_cast<uint32_t*>(grown.p[2]);
+    d_rval = grown.p[3];
+    d_ws = grown.p[4];
+    ws_bytes = ws_diff_workspace_bytes(grown.cap);
+    return true;
+  };
   const bool dbg = getenv("WSYNC_RELAY_DEBUG") != nullptr;
   double dt[5] = {0, 0, 0, 0, 0};  // debug: h2d, peek, decode, reslice, apply
   auto puller = [&] {
@@ -359,6 +410,22 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         return;
       }
       const int nd = (int)p.shape.size();
+      // the payload must be the planned source shard (codec.cpp:98-100:
+      // ShapeMismatch), or its records would land at remapped positions
+      bool shape_ok = info.ndims == nd && info.dtype == dtype_;
+      for (int dd = 0; shape_ok && dd < nd; ++dd)
+        shape_ok = info.shape[dd] == (src.shard.d.slice_dim == dd
+                                          ? src.shard.d.end - src.shard.d.start
+                                          : p.shape[dd]);
+      if (!shape_ok) {
+        fail(WS_SHAPE_MISMATCH, "sync_relay: payload of '" + cand[hit] +
+                                    "' does not have the source shard's dtype and shape");
+        return;
+      }
+      if (info.codec == 'S' && !records_for(info.nnz)) {
+        fail(WS_CUDA, "sync_relay: record scratch allocation failed");
+        return;
+      }
       const ws_stream_t ps = reinterpret_cast<ws_stream_t>(s_pull);
       char* tgt = static_cast<char*>(serve) + r.dst_offset * esz;
       if (info.codec == 'S') {
@@ -366,7 +433,7 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         lap(2);
         if (e == WS_OK)
           e = ws_reslice_delta((ws_dtype)dtype_, p.shape.data(), nd, src.shard.d, r.dst.d, 1,
-                               d_idx, d_val, info.nnz, nullptr, d_ridx, d_rval, d_rnnz, d_err,
+                               d_idx, d_val, info.nnz, nullptr, d_ridx, d_rval, d_rnnz, d_rerr,
                                d_ws, ws_bytes, ps);
         uint64_t dn = 1;
         for (int dd = 0; dd < nd; ++dd)
@@ -376,10 +443,12 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
           e = ws_apply_delta((ws_dtype)dtype_, tgt, dn, d_ridx, d_rval, info.nnz /* bound */,
                              d_rnnz, d_err, ps);
         lap(4);
-        uint32_t herr = 0;
-        cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s_pull);
+        uint32_t herr[2] = {0, 0};  // apply's and reslice's error words
+        cudaMemcpyAsync(herr, d_err, 8, cudaMemcpyDeviceToHost, s_pull);
         cudaStreamSynchronize(s_pull);
-        if (e == WS_OK && herr) e = set_error(WS_INDEX_OUT_OF_SHARD, "sync_relay: apply");
+        if (e == WS_OK && herr[1])  // reslice_delta throws IndexOutOfShard (codec.cpp:120-122)
+          e = set_error(WS_INDEX_OUT_OF_SHARD, "sync_relay: reslice: index outside the source shard");
+        if (e == WS_OK && herr[0]) e = set_error(WS_INDEX_OUT_OF_SHARD, "sync_relay: apply");
       } else {
         int64_t copied = 0;
         e = ws_copy_overlap((ws_dtype)dtype_, p.shape.data(), nd, r.dst.d, tgt, src.shard.d,
@@ -423,6 +492,28 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   rep->sparse_shards = sparse_n;
   if (first_err.st != WS_OK) return set_error(first_err.st, first_err.msg);
   return WS_OK;
+}
+
+namespace wsync {
+void scratch_trim(int dev);  // wire.cu
+}
+
+ws_status ws_engine::release_staging() {
+  if (cudaSetDevice(device_) != cudaSuccess) return set_error(WS_CUDA, "cudaSetDevice");
+  for (cudaStream_t st : relay_streams_)
+    if (st) cudaStreamSynchronize(st);
+  for (auto& e : relay_dev_) cudaFree(e.first);
+  for (auto& e : relay_host_) cudaFreeHost(e.first);
+  relay_dev_.clear();
+  relay_host_.clear();
+  cudaDeviceSynchronize();
+  scratch_trim(device_);
+  return cudaGetLastError() == cudaSuccess ? WS_OK : set_error(WS_CUDA, "release_staging");
+}
+
+extern "C" ws_status ws_engine_release_staging(ws_engine* eng) {
+  if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_release_staging: null engine");
+  return eng->release_staging();
 }
 
 extern "C" ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step,

@@ -276,9 +276,12 @@ ws_status wire_cuda(cudaError_t e, const char* what) { return cuda_status(e, wha
 // threshold of 0, every synchronisation handed the memory back to the driver,
 // so each call paid a full allocation (~4 ms per decode on the relay path).
 // The process's default pool is left untouched.
+std::mutex g_scratch_mu;
+cudaMemPool_t g_scratch_pools[64] = {};
+
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
-  static std::mutex mu;
-  static cudaMemPool_t pools[64] = {};
+  std::mutex& mu = g_scratch_mu;
+  cudaMemPool_t* pools = g_scratch_pools;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -305,6 +308,15 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
 }
 
 }  // namespace
+
+namespace wsync {
+// Hands the cached scratch of `dev` back to the driver (after the work that
+// used it has completed).
+void scratch_trim(int dev) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  if (dev >= 0 && dev < 64 && g_scratch_pools[dev]) cudaMemPoolTrimTo(g_scratch_pools[dev], 0);
+}
+}  // namespace wsync
 
 extern "C" {
 
@@ -402,6 +414,8 @@ ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_
     std::memcpy(&v, h + 8 + 8 * d, 8);
     if (v <= 0) return set_error(WS_PAYLOAD_FORMAT, "non-positive dim");
     info->shape[d] = v;
+    if ((uint64_t)v > len / elems)  // cannot fit in the payload (and no overflow below)
+      return set_error(WS_PAYLOAD_FORMAT, "payload size mismatch: dims exceed the payload");
     elems *= (uint64_t)v;
   }
   uint64_t pos = 8 + 8 * (uint64_t)nd;
@@ -428,6 +442,9 @@ ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_
   info->index_width = iw;
   info->nnz = nnz;
   info->header_bytes = pos;
+  if (nnz > (len >= pos ? len - pos : 0) / ((uint64_t)iw + esz))  // no wrap in the product
+    return set_error(WS_PAYLOAD_FORMAT, "sparse payload size mismatch: nnz " +
+                                            std::to_string(nnz) + " exceeds the payload");
   info->total_bytes = pos + nnz * ((uint64_t)iw + esz);
   if (info->total_bytes != len)
     return set_error(WS_PAYLOAD_FORMAT, "sparse payload size mismatch: header implies " +

@@ -239,6 +239,12 @@ class TransferEngine:
                                            C.byref(rep)))
         return rep.as_dict()
 
+    def release_staging(self):
+        """Frees sync_relay's staging and cached decode scratch
+        (ws_engine_release_staging)."""
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_release_staging(self.h))
+
     def segment_frames(self, i, step, bucket_bytes=None, force_wide_index=False):
         """The relay frames of segment i for `step` (engine.cpp:136-148 +
         wire.cpp:35-47): (uint8 device tensor, keys, frame offsets)."""
