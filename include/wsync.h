@@ -214,6 +214,11 @@ ws_status ws_encode_dense_dev(ws_dtype dtype, const int64_t* shape, int ndims,
 ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len,
                               ws_payload_info* info);
 
+/* peek_payload_size (codec.hpp:66-67, codec.cpp:219-227): the full size of a
+ * payload of which only the first `len` bytes (at least its header) are in
+ * device memory; PayloadFormatError on a bad or truncated header. */
+ws_status ws_peek_payload_size_dev(const void* payload_dev, uint64_t len, uint64_t* total);
+
 /* The records of a sparse payload (after ws_peek_payload_dev): u32 indices
  * (PayloadFormatError unless strictly ascending, codec.cpp:257) and values.
  * Synchronises. */

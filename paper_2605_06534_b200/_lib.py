@@ -189,6 +189,7 @@ _SIGS = {
                               _vp], C.c_int),
     "ws_encode_dense_dev": ([C.c_int, C.POINTER(_i64), C.c_int, _vp, _vp, _vp], C.c_int),
     "ws_peek_payload_dev": ([_vp, _u64, C.POINTER(PayloadInfo)], C.c_int),
+    "ws_peek_payload_size_dev": ([_vp, _u64, C.POINTER(_u64)], C.c_int),
     "ws_decode_sparse_dev": ([_vp, C.POINTER(PayloadInfo), _vp, _vp, _vp], C.c_int),
     "ws_crc32_dev": ([C.POINTER(_vp), C.POINTER(_u64), C.c_int, C.POINTER(C.c_uint32), _vp],
                      C.c_int),

@@ -377,7 +377,10 @@ ws_status ws_encode_dense_dev(ws_dtype dtype, const int64_t* shape, int ndims, c
 
 // decode_header + the size checks of decode_payload / peek_payload_size
 // (codec.cpp:196-263), reading the header from device memory.
-ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_info* info) {
+// exact: the payload is `len` bytes (decode_payload's size checks); else
+// `len` bytes of it are present and only the header must fit (peek).
+static ws_status peek_impl(const void* payload_dev, uint64_t len, ws_payload_info* info,
+                           bool exact) {
   if (!info) return set_error(WS_INVALID_ARGUMENT, "null info");
   std::memset(info, 0, sizeof(*info));
   uint8_t h[88] = {0};
@@ -414,7 +417,8 @@ ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_
     std::memcpy(&v, h + 8 + 8 * d, 8);
     if (v <= 0) return set_error(WS_PAYLOAD_FORMAT, "non-positive dim");
     info->shape[d] = v;
-    if ((uint64_t)v > len / elems)  // cannot fit in the payload (and no overflow below)
+    // cannot fit in the payload (or in any payload); no overflow below
+    if ((uint64_t)v > (exact ? len : (1ull << 62)) / elems)
       return set_error(WS_PAYLOAD_FORMAT, "payload size mismatch: dims exceed the payload");
     elems *= (uint64_t)v;
   }
@@ -427,7 +431,7 @@ ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_
     info->codec = 'D';
     info->index_width = 0;
     info->total_bytes = pos + elems * esz;
-    if (info->total_bytes != len)
+    if (exact && info->total_bytes != len)
       return set_error(WS_PAYLOAD_FORMAT, "dense payload size mismatch: header implies " +
                                               std::to_string(info->total_bytes) + ", got " +
                                               std::to_string(len));
@@ -442,15 +446,28 @@ ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_
   info->index_width = iw;
   info->nnz = nnz;
   info->header_bytes = pos;
-  if (nnz > (len >= pos ? len - pos : 0) / ((uint64_t)iw + esz))  // no wrap in the product
+  const uint64_t room = exact ? (len >= pos ? len - pos : 0) : (1ull << 62);
+  if (nnz > room / ((uint64_t)iw + esz))  // no wrap in the product
     return set_error(WS_PAYLOAD_FORMAT, "sparse payload size mismatch: nnz " +
                                             std::to_string(nnz) + " exceeds the payload");
   info->total_bytes = pos + nnz * ((uint64_t)iw + esz);
-  if (info->total_bytes != len)
+  if (exact && info->total_bytes != len)
     return set_error(WS_PAYLOAD_FORMAT, "sparse payload size mismatch: header implies " +
                                             std::to_string(info->total_bytes) + ", got " +
                                             std::to_string(len));
   return WS_OK;
+}
+
+ws_status ws_peek_payload_dev(const void* payload_dev, uint64_t len, ws_payload_info* info) {
+  return peek_impl(payload_dev, len, info, true);
+}
+
+ws_status ws_peek_payload_size_dev(const void* payload_dev, uint64_t len, uint64_t* total) {
+  if (!total) return set_error(WS_INVALID_ARGUMENT, "null total");
+  ws_payload_info info;
+  const ws_status st = peek_impl(payload_dev, len, &info, false);
+  if (st == WS_OK) *total = info.total_bytes;
+  return st;
 }
 
 ws_status ws_decode_sparse_dev(const void* payload_dev, const ws_payload_info* info,

@@ -6,9 +6,9 @@
 // (engine.cpp's sync_step pusher/puller threads, bench.cpp, plan.cpp ...) into
 // a client of the B200 kernels: diff_shards -> K1 (ws_diff_shards),
 // apply_delta -> K4 (ws_apply_delta), reslice_delta -> ws_reslice_delta.
-// The payload functions (encode_dense / encode_sparse / pick_index_width /
-// decode_payload / peek_payload_size) restate the wire format of
-// codec.hpp:50-70 on the host.  See INTEGRATION.md.
+// The payload functions (encode_dense / encode_sparse / decode_payload /
+// peek_payload_size) run on libwsync's device wire kernels (wire.cu), the
+// code the engine's relay sync uses.  See INTEGRATION.md.
 //
 // Each calling thread gets its own CUDA stream and device scratch (the
 // reference runs one pusher and several puller threads concurrently,
@@ -72,61 +72,23 @@ void ws_ok(ws_status st) {
 
 ws_dtype wdt(DType d) { return d == DType::F32 ? WS_F32 : WS_I32; }
 
-template <typename T>
-void put(std::vector<std::uint8_t>& out, T v) {
-  const std::size_t at = out.size();
-  out.resize(at + sizeof(T));
-  std::memcpy(out.data() + at, &v, sizeof(T));
+// Host bytes -> device scratch slot, and back, on the thread's stream.
+void* upload(DeviceScratch& s, int slot, const void* host, std::size_t bytes) {
+  void* dev = s.get(slot, bytes < 8 ? 8 : bytes);
+  if (bytes) cuda_ok(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s.stream), "H2D");
+  return dev;
 }
 
-template <typename T>
-T get(const std::uint8_t* data, std::size_t len, std::size_t& pos, const char* what) {
-  if (pos + sizeof(T) > len) throw PayloadFormatError(std::string("payload truncated reading ") + what);
-  T v;
-  std::memcpy(&v, data + pos, sizeof(T));
-  pos += sizeof(T);
-  return v;
+void download(DeviceScratch& s, void* host, const void* dev, std::size_t bytes) {
+  if (bytes) cuda_ok(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s.stream), "D2H");
+  cuda_ok(cudaStreamSynchronize(s.stream), "sync");
 }
 
-constexpr std::uint32_t kDense = 0x31445743u;   // "CWD1"
-constexpr std::uint32_t kSparse = 0x31535743u;  // "CWS1"
-
-struct Head {
-  std::uint32_t magic;
-  DType dtype;
-  int iw;
-  std::vector<std::int64_t> shape;
-  std::size_t pos;
-};
-
-Head read_head(const std::uint8_t* data, std::size_t len) {
-  Head h;
-  std::size_t pos = 0;
-  h.magic = get<std::uint32_t>(data, len, pos, "magic");
-  if (h.magic != kDense && h.magic != kSparse) throw PayloadFormatError("bad payload magic");
-  const auto dt = get<std::uint8_t>(data, len, pos, "dtype");
-  if (dt > 1) throw PayloadFormatError("bad dtype " + std::to_string(dt));
-  h.dtype = static_cast<DType>(dt);
-  const int nd = get<std::uint8_t>(data, len, pos, "ndims");
-  h.iw = get<std::uint8_t>(data, len, pos, "index width");
-  (void)get<std::uint8_t>(data, len, pos, "pad");
-  for (int i = 0; i < nd; ++i) {
-    const auto d = get<std::int64_t>(data, len, pos, "dim");
-    if (d <= 0) throw PayloadFormatError("non-positive dim");
-    h.shape.push_back(d);
-  }
-  h.pos = pos;
-  return h;
-}
-
-void write_head(std::vector<std::uint8_t>& out, std::uint32_t magic, DType dt,
-                const std::vector<std::int64_t>& shape, std::uint8_t iw) {
-  put(out, magic);
-  put(out, static_cast<std::uint8_t>(dt));
-  put(out, static_cast<std::uint8_t>(shape.size()));
-  put(out, iw);
-  put(out, std::uint8_t{0});
-  for (auto d : shape) put(out, d);
+// The reference's DType holds F32/I32 only: a bf16 payload ("CWS2"/"CWD2",
+// dtype code 2) is foreign to this API, as the reference decoder says.
+DType host_dtype(int code) {
+  if (code != WS_F32 && code != WS_I32) throw PayloadFormatError("bad dtype " + std::to_string(code));
+  return code == WS_F32 ? DType::F32 : DType::I32;
 }
 
 }  // namespace
@@ -252,79 +214,92 @@ SparseDelta reslice_delta(const SparseDelta& delta, const ShardDescriptor& src,
   return out;
 }
 
-// ---- wire payloads (codec.hpp:50-70) ------------------------------------------
+// ---- wire payloads (codec.hpp:50-70), built and parsed on the device ----------
+// by libwsync's wire kernels (ws_encode_*_dev, ws_peek_*_dev,
+// ws_decode_sparse_dev): the same code path the engine's relay sync uses.
 
 int pick_index_width(const SparseDelta& d) {
-  const std::uint64_t top = d.indices.empty() ? 0 : d.indices.back();
-  return top <= 0xFFFFFFFFull ? 4 : 8;
+  // indices ascend, so the last one decides whether 32 bits are enough
+  return (!d.indices.empty() && (d.indices.back() >> 32) != 0) ? 8 : 4;
 }
 
 std::vector<std::uint8_t> encode_dense(const HostTensor& t) {
-  std::vector<std::uint8_t> out;
-  out.reserve(32 + t.data.size());
-  write_head(out, kDense, t.dtype, t.shape, 0);
-  out.insert(out.end(), t.data.begin(), t.data.end());
-  return out;
+  DeviceScratch& s = scratch();
+  const int nd = static_cast<int>(t.shape.size());
+  const std::uint64_t total =
+      ws_payload_bytes(wdt(t.dtype), nd, 'D', 0, static_cast<std::uint64_t>(t.elems()));
+  const void* src = upload(s, 0, t.data.data(), t.data.size());
+  void* out = s.get(1, total);
+  ws_ok(ws_encode_dense_dev(wdt(t.dtype), t.shape.data(), nd, src, out,
+                            reinterpret_cast<ws_stream_t>(s.stream)));
+  std::vector<std::uint8_t> bytes(total);
+  download(s, bytes.data(), out, total);
+  return bytes;
 }
 
 std::vector<std::uint8_t> encode_sparse(const SparseDelta& d, int index_width) {
   if (index_width != 4 && index_width != 8) throw PayloadFormatError("index width must be 4 or 8");
-  std::vector<std::uint8_t> out;
-  out.reserve(40 + d.indices.size() * static_cast<std::size_t>(index_width + 4));
-  write_head(out, kSparse, d.dtype, d.shape, static_cast<std::uint8_t>(index_width));
-  put(out, static_cast<std::uint64_t>(d.indices.size()));
-  for (auto i : d.indices) {
-    if (index_width == 8) {
-      put(out, i);
-    } else {
-      if (i > 0xFFFFFFFFull) throw PayloadFormatError("index " + std::to_string(i) + " exceeds u32");
-      put(out, static_cast<std::uint32_t>(i));
-    }
+  DeviceScratch& s = scratch();
+  const std::uint64_t nnz = d.indices.size();
+  // the device encoder takes u32 local indices (every shard below 2^32
+  // elements) and widens them to index_width on the wire
+  std::vector<std::uint32_t> narrow(nnz);
+  for (std::uint64_t k = 0; k < nnz; ++k) {
+    if (d.indices[k] >> 32)
+      throw PayloadFormatError("index " + std::to_string(d.indices[k]) +
+                               " beyond the 32-bit local indices of a shard");
+    narrow[k] = static_cast<std::uint32_t>(d.indices[k]);
   }
-  out.insert(out.end(), d.values.begin(), d.values.end());
-  return out;
+  const int nd = static_cast<int>(d.shape.size());
+  const std::uint64_t total = ws_payload_bytes(wdt(d.dtype), nd, 'S', index_width, nnz);
+  const auto* idx = static_cast<const std::uint32_t*>(upload(s, 0, narrow.data(), nnz * 4));
+  const void* val = upload(s, 2, d.values.data(), d.values.size());
+  void* out = s.get(1, total);
+  ws_ok(ws_encode_sparse_dev(wdt(d.dtype), d.shape.data(), nd, index_width, idx, val, nnz, out,
+                             reinterpret_cast<ws_stream_t>(s.stream)));
+  std::vector<std::uint8_t> bytes(total);
+  download(s, bytes.data(), out, total);
+  return bytes;
 }
 
 std::size_t peek_payload_size(const std::uint8_t* data, std::size_t len) {
-  const Head h = read_head(data, len);
-  std::uint64_t elems = 1;
-  for (auto d : h.shape) elems *= static_cast<std::uint64_t>(d);
-  if (h.magic == kDense) return h.pos + elems * 4;
-  std::size_t pos = h.pos;
-  const auto nnz = get<std::uint64_t>(data, len, pos, "nnz");
-  return pos + nnz * (static_cast<std::size_t>(h.iw) + 4);
+  DeviceScratch& s = scratch();
+  // a header is at most 8 + 8 x 8 dims + 8 (nnz) bytes
+  const std::size_t head = len < 96 ? len : 96;
+  const void* dev = upload(s, 0, data, head);
+  cuda_ok(cudaStreamSynchronize(s.stream), "sync");
+  std::uint64_t total = 0;
+  ws_ok(ws_peek_payload_size_dev(dev, len, &total));
+  if (len > 4) host_dtype(data[4]);
+  return static_cast<std::size_t>(total);
 }
 
 DecodedPayload decode_payload(const std::vector<std::uint8_t>& bytes) {
-  const std::uint8_t* data = bytes.data();
-  const std::size_t len = bytes.size();
-  const Head h = read_head(data, len);
-  std::size_t pos = h.pos;
-  if (h.magic == kDense) {
-    HostTensor t = HostTensor::zeros(h.dtype, h.shape);
-    if (pos + t.data.size() != len)
-      throw PayloadFormatError("dense payload size mismatch: header implies " +
-                               std::to_string(pos + t.data.size()) + ", got " + std::to_string(len));
-    std::memcpy(t.data.data(), data + pos, t.data.size());
+  DeviceScratch& s = scratch();
+  const void* dev = upload(s, 0, bytes.data(), bytes.size());
+  cuda_ok(cudaStreamSynchronize(s.stream), "sync");
+  ws_payload_info info;
+  ws_ok(ws_peek_payload_dev(dev, bytes.size(), &info));
+  const DType dt = host_dtype(info.dtype);
+  const std::vector<std::int64_t> shape(info.shape, info.shape + info.ndims);
+  if (info.codec == 'D') {
+    HostTensor t = HostTensor::zeros(dt, shape);
+    download(s, t.data.data(), static_cast<const std::uint8_t*>(dev) + info.header_bytes,
+             t.data.size());
     return DecodedPayload{std::move(t)};
   }
-  if (h.iw != 4 && h.iw != 8) throw PayloadFormatError("sparse index width");
   SparseDelta d;
-  d.dtype = h.dtype;
-  d.shape = h.shape;
-  const auto nnz = get<std::uint64_t>(data, len, pos, "nnz");
-  const std::size_t want = pos + nnz * (static_cast<std::size_t>(h.iw) + 4);
-  if (want != len)
-    throw PayloadFormatError("sparse payload size mismatch: header implies " +
-                             std::to_string(want) + ", got " + std::to_string(len));
-  d.indices.reserve(nnz);
-  for (std::uint64_t k = 0; k < nnz; ++k) {
-    const std::uint64_t i = h.iw == 4 ? get<std::uint32_t>(data, len, pos, "index")
-                                      : get<std::uint64_t>(data, len, pos, "index");
-    if (k > 0 && i <= d.indices.back()) throw PayloadFormatError("indices not strictly ascending");
-    d.indices.push_back(i);
-  }
-  d.values.assign(data + pos, data + len);
+  d.dtype = dt;
+  d.shape = shape;
+  auto* idx = static_cast<std::uint32_t*>(s.get(1, info.nnz * 4));
+  void* val = s.get(2, info.nnz * 4);
+  ws_ok(ws_decode_sparse_dev(dev, &info, idx, val, reinterpret_cast<ws_stream_t>(s.stream)));
+  std::vector<std::uint32_t> narrow(info.nnz);
+  d.values.resize(info.nnz * 4);
+  cuda_ok(cudaMemcpyAsync(narrow.data(), idx, info.nnz * 4, cudaMemcpyDeviceToHost, s.stream),
+          "D2H");
+  download(s, d.values.data(), val, d.values.size());
+  d.indices.assign(narrow.begin(), narrow.end());
   return DecodedPayload{std::move(d)};
 }
 
