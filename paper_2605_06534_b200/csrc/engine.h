@@ -67,11 +67,15 @@ struct ws_engine {
   // K1 (every exchange round's segments back to back) + local route
   ws_status sync_encode(SyncCtx& x, cudaStream_t s);
   ws_status sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host, ws_report* report);
+  // sync_step without the grouped-engine check
+  ws_status sync_step_impl(const ws_sync_options& o, cudaStream_t s, const void* next_host,
+                           uint64_t* nnz_host, ws_report* report);
   int exchange_rounds() const;
   ws_status exchange_pack(const ws_sync_options& o, int next_arena, int round, cudaStream_t s,
                           uint32_t* launches);
   ws_status exchange_apply(int round, cudaStream_t s, uint32_t* launches);
   ws_status exchange_end(cudaStream_t s);
+  ws_status exchange_mark_pack(cudaStream_t s);
   ws_status exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense, uint64_t* recv_records);
   bool exchange_needs_resize(const ws_sync_options& o) const;
   // grows the P2P receive regions for o.density_threshold (collective)
@@ -86,6 +90,9 @@ struct ws_engine {
 
  private:
   bool grouped_ = false;
+  uint32_t last_launches_ = 0;
+  bool last_streamed_apply_ = false;
+  ws_status report_of(const SyncCtx& x, ws_report* report);
   ws_status ensure_records(double threshold, int sparse);
   ws_status init_p2p();
   ws_status p2p_size(double t);  // receive regions for syncs with threshold <= t

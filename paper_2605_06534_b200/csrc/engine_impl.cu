@@ -423,7 +423,6 @@ ws_status ws_engine::sync_encode(SyncCtx& x, cudaStream_t s) {
 
 ws_status ws_engine::sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host,
                                  ws_report* report) {
-  const ws_sync_options& o = x.o;
   cudaEvent_t* ev_ = x.ev;
   WS_CUDA_TRY(cudaEventRecord(ev_[4], s), "event");
   if ((nnz_host || report) && nseg_)
@@ -431,13 +430,23 @@ ws_status ws_engine::sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host,
                 "D2H counts");
   WS_CUDA_TRY(cudaEventRecord(ev_[5], s), "event");
   launch_total_ += x.launches;
+  last_launches_ = x.launches;
+  last_streamed_apply_ = x.streamed_apply;
   pack_steps_ = pack_ev_ ? pack_steps_ + 1 : 0;  // the most recent run of steps with one
   if (!nnz_host && !report) return WS_OK;
   WS_CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  if (nnz_host && nseg_) std::memcpy(nnz_host, h_nnz_pinned_, nseg_ * 8);
+  return report_of(x, report);
+}
+
+// Fills `report` (if any) from the synchronised sync x (counts in
+// h_nnz_pinned_, stage events in x.ev) and surfaces exchange faults.
+ws_status ws_engine::report_of(const SyncCtx& x, ws_report* report) {
+  const ws_sync_options& o = x.o;
+  cudaEvent_t* ev_ = x.ev;
   ws_status st = exchange_status();
   if (st != WS_OK) return st;
   std::memcpy(h_nnz_.data(), h_nnz_pinned_, nseg_ * 8);
-  if (nnz_host) std::memcpy(nnz_host, h_nnz_.data(), nseg_ * 8);
   if (report) {
     const int esz = dtype_size(dtype_);
     std::memset(report, 0, sizeof(*report));
@@ -476,6 +485,12 @@ ws_status ws_engine::sync_step(const ws_sync_options& o, cudaStream_t s, const v
                                uint64_t* nnz_host, ws_report* report) {
   if (grouped_)
     return set_error(WS_INVALID_ARGUMENT, "engine of a ws_group: sync through ws_group_sync_step");
+  return sync_step_impl(o, s, next_host, nnz_host, report);
+}
+
+ws_status ws_engine::sync_step_impl(const ws_sync_options& o, cudaStream_t s,
+                                    const void* next_host, uint64_t* nnz_host,
+                                    ws_report* report) {
   SyncCtx x;
   ws_status st = sync_begin(x, o, s, next_host);
   if (st != WS_OK) return st;

@@ -853,6 +853,14 @@ ws_status ws_engine::exchange_pack(const ws_sync_options& o, int next_arena, int
   return WS_OK;
 }
 
+// Marks the end of the last round's pack on this sync's stage events (the
+// pack's share of the route stage, ws_timing::pack_s).
+ws_status ws_engine::exchange_mark_pack(cudaStream_t s) {
+  WS_CUDA_TRY(cudaEventRecord(ring_[(ring_head_ + kRing - 1) % kRing][6], s), "event");
+  pack_ev_ = true;
+  return WS_OK;
+}
+
 // Receiver side of a round: apply what the sources sent for it, then ack.
 ws_status ws_engine::exchange_apply(int round, cudaStream_t s, uint32_t* launches) {
   Comm* c = comm_;
@@ -968,10 +976,7 @@ ws_status ws_engine::exchange(const ws_sync_options& o, int next_arena, cudaStre
   if (c->p2p) {
     for (int r = 0; r < c->R; ++r) {
       ws_status st = exchange_pack(o, next_arena, r, s, launches);
-      if (st == WS_OK && r == c->R - 1) {  // the pack's share of the route stage
-        WS_CUDA_TRY(cudaEventRecord(ring_[(ring_head_ + kRing - 1) % kRing][6], s), "event");
-        pack_ev_ = true;
-      }
+      if (st == WS_OK && r == c->R - 1) st = exchange_mark_pack(s);
       if (st == WS_OK) st = exchange_apply(r, s, launches);
       if (st != WS_OK) return st;
     }

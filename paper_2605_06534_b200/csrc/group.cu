@@ -12,6 +12,12 @@
 // earlier launch of that stream.  It runs the multi-GPU data path of any
 // layout (TrainConfig{tp,pp,dp}, FSDP-N, serving TP x PP x replicas, EP) on
 // a single device, which is how the parity tests cover it on one B200.
+//
+// A group may instead hold one rank per GPU of the process (peer access over
+// NVLink, pointers shared the same way): every rank then runs its whole sync
+// concurrently on its own GPU, exactly the deployment's kernels, driven by
+// one process (e.g. for ncu, which profiles one process).
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -24,9 +30,18 @@ using namespace wsync;
 
 struct ws_group {
   explicit ws_group(int w) : shared(w), eng(w, nullptr) {}
+  ~ws_group() {
+    for (size_t r = 0; r < streams.size(); ++r)
+      if (streams[r]) {
+        cudaSetDevice(eng[r] ? eng[r]->device() : 0);
+        cudaStreamDestroy(streams[r]);
+      }
+  }
   GroupShared shared;
   std::vector<ws_engine*> eng;
   bool connected = false;
+  bool multi_device = false;           // ranks on several GPUs of this process
+  std::vector<cudaStream_t> streams;   // multi-device: one per rank, on its GPU
 };
 
 namespace {
@@ -96,16 +111,42 @@ ws_status ws_group_connect(ws_group* g) {
     if (!g->eng[r]) return set_error(WS_INVALID_ARGUMENT, "ws_group_connect: a rank has not joined");
     if (!g->eng[r]->bound())
       return set_error(WS_INVALID_ARGUMENT, "ws_group_connect: a rank is not bound");
-    if (g->eng[r]->device() != g->eng[0]->device())
-      return set_error(WS_INVALID_ARGUMENT, "ws_group_connect: ranks on different devices");
   }
+  std::vector<int> devs;
+  for (int r = 0; r < W; ++r)
+    if (std::find(devs.begin(), devs.end(), g->eng[r]->device()) == devs.end())
+      devs.push_back(g->eng[r]->device());
+  g->multi_device = devs.size() > 1;
+  if (g->multi_device && (int)devs.size() != W)
+    return set_error(WS_INVALID_ARGUMENT,
+                     "ws_group_connect: ranks share either one GPU or one GPU each");
   ws_status st = run_ranks(g, [&](int r) {
     ws_engine* e = g->eng[r];
+    // peers' memory on other GPUs is reached over NVLink (peer access)
+    for (int d : devs) {
+      if (d == e->device()) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, e->device(), d);
+      if (!can) return set_error(WS_CUDA, "ws_group_connect: no peer access between the GPUs");
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(d, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+        return cuda_status(pe, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();
+    }
     ws_status s = e->init_comm(nullptr, &g->shared);
     return s != WS_OK ? s : e->map_serve();
   });
-  if (st == WS_OK) g->connected = true;
-  return st;
+  if (st != WS_OK) return st;
+  if (g->multi_device) {
+    g->streams.assign(W, nullptr);
+    for (int r = 0; r < W; ++r) {
+      cudaSetDevice(g->eng[r]->device());
+      if (cudaStreamCreateWithFlags(&g->streams[r], cudaStreamNonBlocking) != cudaSuccess)
+        return set_error(WS_CUDA, "ws_group_connect: stream");
+    }
+  }
+  g->connected = true;
+  return WS_OK;
 }
 
 ws_status ws_group_sync_step(ws_group* g, const ws_sync_options* opts, ws_stream_t stream,
@@ -119,19 +160,39 @@ ws_status ws_group_sync_step(ws_group* g, const ws_sync_options* opts, ws_stream
     ws_status st = run_ranks(g, [&](int r) { return E[r]->exchange_prepare(*opts); });
     if (st != WS_OK) return st;
   }
+  // Single GPU: every rank on the caller's stream.  One GPU per rank: each
+  // rank on its own GPU's stream; the phases still go out in this order, so
+  // a tool that serialises every launch of the process (ncu) runs them in an
+  // order where each wait is already satisfied, and without one the GPUs run
+  // concurrently, ordered only by the exchange's flags.
+  int cur = 0;
+  cudaGetDevice(&cur);
+  auto on = [&](int r) {
+    if (g->multi_device) cudaSetDevice(E[r]->device());
+    return g->multi_device ? g->streams[r] : s;
+  };
   std::vector<ws_engine::SyncCtx> x(W);
   ws_status st = WS_OK;
-  for (int r = 0; r < W && st == WS_OK; ++r) st = E[r]->sync_begin(x[r], *opts, s, nullptr);
-  for (int r = 0; r < W && st == WS_OK; ++r) st = E[r]->sync_encode(x[r], s);
+  for (int r = 0; r < W && st == WS_OK; ++r) st = E[r]->sync_begin(x[r], *opts, on(r), nullptr);
+  for (int r = 0; r < W && st == WS_OK; ++r) st = E[r]->sync_encode(x[r], on(r));
   if (W > 1)
     for (int round = 0; round < E[0]->exchange_rounds() && st == WS_OK; ++round) {
+      for (int r = 0; r < W && st == WS_OK; ++r) {
+        st = E[r]->exchange_pack(x[r].o, x[r].na, round, on(r), &x[r].launches);
+        if (st == WS_OK && round == E[r]->exchange_rounds() - 1) st = E[r]->exchange_mark_pack(on(r));
+      }
       for (int r = 0; r < W && st == WS_OK; ++r)
-        st = E[r]->exchange_pack(x[r].o, x[r].na, round, s, &x[r].launches);
-      for (int r = 0; r < W && st == WS_OK; ++r) st = E[r]->exchange_apply(round, s, &x[r].launches);
+        st = E[r]->exchange_apply(round, on(r), &x[r].launches);
     }
-  for (int r = 0; r < W && st == WS_OK && W > 1; ++r) st = E[r]->exchange_end(s);
+  for (int r = 0; r < W && st == WS_OK && W > 1; ++r) st = E[r]->exchange_end(on(r));
   for (int r = 0; r < W && st == WS_OK; ++r)
-    st = E[r]->sync_finish(x[r], s, nullptr, reports ? reports + r : nullptr);
+    st = E[r]->sync_finish(x[r], on(r), nullptr, reports ? reports + r : nullptr);
+  if (g->multi_device)  // the call returns with every rank's sync complete
+    for (int r = 0; r < W; ++r) {
+      const cudaError_t e = cudaStreamSynchronize(on(r));
+      if (st == WS_OK && e != cudaSuccess) st = cuda_status(e, "group sync");
+    }
+  cudaSetDevice(cur);
   return st;
 }
 

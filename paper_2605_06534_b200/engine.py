@@ -288,7 +288,11 @@ class EngineGroup:
 
     def __init__(self, manifest, dtype, train: TrainConfig, serve: ServeConfig, world: int,
                  device=None):
+        """device: one GPU for every rank, or a list with one GPU per rank
+        (the ranks then sync concurrently, each on its GPU, peer memory over
+        NVLink)."""
         self.world = world
+        devices = list(device) if isinstance(device, (list, tuple)) else [device] * world
         self.plans = [Plan(manifest, dtype, train, serve, world=world, rank=r)
                       for r in range(world)]
         h = C.c_void_p()
@@ -296,8 +300,8 @@ class EngineGroup:
         self.h = h
         self.engines = []
         try:
-            for plan in self.plans:
-                self.engines.append(TransferEngine(plan, device, group=self))
+            for plan, dev in zip(self.plans, devices):
+                self.engines.append(TransferEngine(plan, dev, group=self))
             with torch.cuda.device(self.engines[0].device):
                 check(lib.ws_group_connect(h))
         except Exception:

@@ -205,3 +205,25 @@ def test_group_matches_reference_engine(reference, dtype, train, serve):
                 bad.append((q, eng.plan.manifest[p].name))
     assert bad == []
     g.close()
+
+
+def test_group_one_rank_per_gpu():
+    """The same group with one rank per GPU of the process (peer memory over
+    NVLink, every rank's sync concurrent on its GPU): FSDP-N -> TP2 x N/2 on
+    the GPUs present (skipped on a one-GPU box)."""
+    import paper_2605_06534_b200 as ws
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs 2+ GPUs")
+    n = 4 if n >= 4 else 2
+    manifest = ws.MODELS["qwen2.5-0.5b"]([0, 1, 23])
+    g = ws.EngineGroup(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, n // 2),
+                       n, device=list(range(n)))
+    g.generate(seed=2, density=0.01)
+    for k in range(4):
+        g.sync_step(reverse=bool(k % 2), report=False)
+    assert _serve_equals_gen(ws, g, 2, 0.01, "prev") == []
+    reps = g.sync_step()
+    assert _serve_equals_gen(ws, g, 2, 0.01, "next") == []
+    assert all(r["dense_shards"] == 0 for r in reps)
+    g.close()
