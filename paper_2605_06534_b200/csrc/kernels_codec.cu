@@ -8,6 +8,7 @@
 // (segments are independent look-back chains).  The design and the
 // measurements behind it are in DESIGN.md §4.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <cstdlib>
 #include <cstring>
@@ -1023,8 +1024,13 @@ size_t encode_spill_bytes(int dtype, uint32_t blocks) {
 }
 
 cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* grid_out) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  // the shared-memory opt-in is a per-device function attribute (a process
+  // may drive several GPUs: ws_group)
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_done.load() & bit)) {
     cudaFuncSetAttribute(encode_kernel<WS_BF16, false, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_BF16>::kSmem);
     cudaFuncSetAttribute(encode_kernel<WS_BF16, true, false>,
@@ -1036,7 +1042,7 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_I32>::kSmem);
     cudaFuncSetAttribute(encode_kernel<WS_F32, false, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EncCfg<WS_F32>::kSmem);
-    attr_done = true;
+    attr_done.fetch_or(bit);
   }
   // one persistent block per SM; the producer warp claims super-tiles in order
   int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(),

@@ -417,8 +417,9 @@ static ws_status peek_impl(const void* payload_dev, uint64_t len, ws_payload_inf
     std::memcpy(&v, h + 8 + 8 * d, 8);
     if (v <= 0) return set_error(WS_PAYLOAD_FORMAT, "non-positive dim");
     info->shape[d] = v;
-    // cannot fit in the payload (or in any payload); no overflow below
-    if ((uint64_t)v > (exact ? len : (1ull << 62)) / elems)
+    // a dense payload carries every element; any payload stays below 2^62
+    // bytes -- so the product cannot overflow below
+    if ((uint64_t)v > ((exact && d1) ? len : (1ull << 62)) / elems)
       return set_error(WS_PAYLOAD_FORMAT, "payload size mismatch: dims exceed the payload");
     elems *= (uint64_t)v;
   }
