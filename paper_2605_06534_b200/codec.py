@@ -37,8 +37,11 @@ def dtype_code(t: torch.Tensor) -> int:
         raise _lib.InvalidArgument(f"unsupported dtype {t.dtype}") from None
 
 
-def _stream():
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device=None):
+    """The current stream of `device` (default: the current device).  Calls on
+    tensors of another GPU run under torch.cuda.device(tensor.device), so the
+    library launches there."""
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 def _ptr(t):
@@ -82,90 +85,95 @@ def _workspace(n, device):
 
 def diff_shards(prev: torch.Tensor, next_: torch.Tensor, cap: int | None = None) -> SparseDelta:
     """Every position whose value changed, ascending (K1 on one shard)."""
-    if prev.dtype != next_.dtype or tuple(prev.shape) != tuple(next_.shape):
-        raise ShapeMismatch(f"diff_shards: {list(prev.shape)} vs {list(next_.shape)}")
-    dt = dtype_code(prev)
-    prev = prev.contiguous()
-    next_ = next_.contiguous()
-    n = prev.numel()
-    cap = n if cap is None else cap
-    dev = prev.device
-    idx = torch.empty(max(1, cap), dtype=torch.int32, device=dev)
-    val = torch.empty(max(1, cap), dtype=_VAL_DTYPE[dt], device=dev)
-    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = _workspace(n, dev)
-    check(lib.ws_diff_shards(dt, _ptr(prev), _ptr(next_), n, _ptr(idx), _ptr(val), cap,
-                             _ptr(nnz), _ptr(ws), ws.numel(), _stream()))
-    k = int(nnz.item())
-    k = min(k, cap)
-    return SparseDelta(dt, tuple(prev.shape), idx[:k], val[:k])
+    with torch.cuda.device(prev.device):
+        if prev.dtype != next_.dtype or tuple(prev.shape) != tuple(next_.shape):
+            raise ShapeMismatch(f"diff_shards: {list(prev.shape)} vs {list(next_.shape)}")
+        dt = dtype_code(prev)
+        prev = prev.contiguous()
+        next_ = next_.contiguous()
+        n = prev.numel()
+        cap = n if cap is None else cap
+        dev = prev.device
+        idx = torch.empty(max(1, cap), dtype=torch.int32, device=dev)
+        val = torch.empty(max(1, cap), dtype=_VAL_DTYPE[dt], device=dev)
+        nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = _workspace(n, dev)
+        check(lib.ws_diff_shards(dt, _ptr(prev), _ptr(next_), n, _ptr(idx), _ptr(val), cap,
+                                 _ptr(nnz), _ptr(ws), ws.numel(), _stream()))
+        k = int(nnz.item())
+        k = min(k, cap)
+        return SparseDelta(dt, tuple(prev.shape), idx[:k], val[:k])
 
 
 def apply_delta(target: torch.Tensor, delta: SparseDelta) -> None:
     """In place ``target += delta``; validates every index before writing."""
-    dt = dtype_code(target)
-    if dt != delta.dtype or tuple(target.shape) != tuple(delta.shape):
-        raise ShapeMismatch(f"apply_delta: target {list(target.shape)} vs delta "
-                            f"{list(delta.shape)}")
-    if not target.is_contiguous():
-        raise _lib.InvalidArgument("apply_delta: target must be contiguous")
-    err = torch.zeros(1, dtype=torch.int32, device=target.device)
-    check(lib.ws_apply_delta(dt, _ptr(target), target.numel(), _ptr(delta.indices),
-                             _ptr(delta.values), delta.nnz(), None, _ptr(err), _stream()))
-    raise_device_error(int(err.item()), "apply_delta")
+    with torch.cuda.device(target.device):
+        dt = dtype_code(target)
+        if dt != delta.dtype or tuple(target.shape) != tuple(delta.shape):
+            raise ShapeMismatch(f"apply_delta: target {list(target.shape)} vs delta "
+                                f"{list(delta.shape)}")
+        if not target.is_contiguous():
+            raise _lib.InvalidArgument("apply_delta: target must be contiguous")
+        err = torch.zeros(1, dtype=torch.int32, device=target.device)
+        check(lib.ws_apply_delta(dt, _ptr(target), target.numel(), _ptr(delta.indices),
+                                 _ptr(delta.values), delta.nnz(), None, _ptr(err), _stream()))
+        raise_device_error(int(err.item()), "apply_delta")
 
 
 def reslice_delta(delta: SparseDelta, src, dst, full_shape, allow_cross_dim: bool = True
                   ) -> SparseDelta:
     """Re-express a delta local to ``src`` as one local to ``dst``."""
-    full_shape = tuple(int(d) for d in full_shape)
-    if tuple(delta.shape) != shard_shape(full_shape, src):
-        raise ShapeMismatch(f"reslice_delta: delta {list(delta.shape)} does not match source "
-                            f"shard {list(shard_shape(full_shape, src))}")
-    nnz = delta.nnz()
-    dev = delta.indices.device
-    out_idx = torch.empty(max(1, nnz), dtype=torch.int32, device=dev)
-    out_val = torch.empty(max(1, nnz), dtype=delta.values.dtype, device=dev)
-    out_n = torch.zeros(1, dtype=torch.int64, device=dev)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
-    ws = _workspace(nnz, dev)
-    check(lib.ws_reslice_delta(delta.dtype, shape_array(full_shape), len(full_shape),
-                               shard(src), shard(dst), int(allow_cross_dim),
-                               _ptr(delta.indices), _ptr(delta.values), nnz, None,
-                               _ptr(out_idx), _ptr(out_val), _ptr(out_n), _ptr(err), _ptr(ws),
-                               ws.numel(), _stream()))
-    bits = int(err.item())
-    if bits:
-        raise IndexOutOfShard("reslice_delta: delta index outside the source shard")
-    k = int(out_n.item())
-    return SparseDelta(delta.dtype, shard_shape(full_shape, dst), out_idx[:k], out_val[:k])
+    with torch.cuda.device(delta.indices.device):
+        full_shape = tuple(int(d) for d in full_shape)
+        if tuple(delta.shape) != shard_shape(full_shape, src):
+            raise ShapeMismatch(f"reslice_delta: delta {list(delta.shape)} does not match source "
+                                f"shard {list(shard_shape(full_shape, src))}")
+        nnz = delta.nnz()
+        dev = delta.indices.device
+        out_idx = torch.empty(max(1, nnz), dtype=torch.int32, device=dev)
+        out_val = torch.empty(max(1, nnz), dtype=delta.values.dtype, device=dev)
+        out_n = torch.zeros(1, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = _workspace(nnz, dev)
+        check(lib.ws_reslice_delta(delta.dtype, shape_array(full_shape), len(full_shape),
+                                   shard(src), shard(dst), int(allow_cross_dim),
+                                   _ptr(delta.indices), _ptr(delta.values), nnz, None,
+                                   _ptr(out_idx), _ptr(out_val), _ptr(out_n), _ptr(err), _ptr(ws),
+                                   ws.numel(), _stream()))
+        bits = int(err.item())
+        if bits:
+            raise IndexOutOfShard("reslice_delta: delta index outside the source shard")
+        k = int(out_n.item())
+        return SparseDelta(delta.dtype, shard_shape(full_shape, dst), out_idx[:k], out_val[:k])
 
 
 def extract_shard(full: torch.Tensor, desc) -> torch.Tensor:
     """Copy of the descriptor's slice of ``full``."""
-    dt = dtype_code(full)
-    full = full.contiguous()
-    out = torch.empty(shard_shape(full.shape, desc), dtype=full.dtype, device=full.device)
-    check(lib.ws_extract_shard(dt, shape_array(full.shape), full.dim(), shard(desc), _ptr(full),
-                               _ptr(out), _stream()))
-    return out
+    with torch.cuda.device(full.device):
+        dt = dtype_code(full)
+        full = full.contiguous()
+        out = torch.empty(shard_shape(full.shape, desc), dtype=full.dtype, device=full.device)
+        check(lib.ws_extract_shard(dt, shape_array(full.shape), full.dim(), shard(desc), _ptr(full),
+                                   _ptr(out), _stream()))
+        return out
 
 
 def copy_overlap(dst: torch.Tensor, dst_desc, src: torch.Tensor, src_desc, full_shape) -> int:
     """Copy the overlap of shard ``src`` into shard ``dst`` (both of one tensor
     of ``full_shape``); returns the copied element count."""
-    dt = dtype_code(dst)
-    if src.dtype != dst.dtype:
-        raise ShapeMismatch("copy_overlap dtype mismatch")
-    full_shape = tuple(int(d) for d in full_shape)
-    if tuple(dst.shape) != shard_shape(full_shape, dst_desc) or \
-            tuple(src.shape) != shard_shape(full_shape, src_desc):
-        raise ShapeMismatch("copy_overlap: shard shape mismatch")
-    copied = C.c_int64()
-    check(lib.ws_copy_overlap(dt, shape_array(full_shape), len(full_shape), shard(dst_desc),
-                              _ptr(dst), shard(src_desc), _ptr(src.contiguous()),
-                              C.byref(copied), _stream()))
-    return copied.value
+    with torch.cuda.device(dst.device):
+        dt = dtype_code(dst)
+        if src.dtype != dst.dtype:
+            raise ShapeMismatch("copy_overlap dtype mismatch")
+        full_shape = tuple(int(d) for d in full_shape)
+        if tuple(dst.shape) != shard_shape(full_shape, dst_desc) or \
+                tuple(src.shape) != shard_shape(full_shape, src_desc):
+            raise ShapeMismatch("copy_overlap: shard shape mismatch")
+        copied = C.c_int64()
+        check(lib.ws_copy_overlap(dt, shape_array(full_shape), len(full_shape), shard(dst_desc),
+                                  _ptr(dst), shard(src_desc), _ptr(src.contiguous()),
+                                  C.byref(copied), _stream()))
+        return copied.value
 
 
 def expert_thresholds(experts: int, density: float, zipf_s: float, perm_seed: int = 0):
@@ -179,17 +187,18 @@ def gen_pair_bf16(seed: int, name: str, full_shape, desc, density: float, device
                   thr_dim0=None):
     """Synthetic bf16 pair for one shard (device generator); thr_dim0: optional
     per-dim-0-index thresholds (expert_thresholds) replacing `density`."""
-    shp = shard_shape(full_shape, desc)
-    prev = torch.empty(shp, dtype=torch.bfloat16, device=device)
-    nxt = torch.empty(shp, dtype=torch.bfloat16, device=device)
-    if thr_dim0 is not None:
-        tab = torch.tensor(list(thr_dim0), dtype=torch.int64, device=device)
-        check(lib.ws_gen_pair_bf16_dim0(seed, name.encode(), shape_array(full_shape),
-                                        len(full_shape), shard(desc), _ptr(tab), _ptr(prev),
-                                        _ptr(nxt), _stream()))
-        torch.cuda.current_stream(device).synchronize()
+    with torch.cuda.device(torch.device(device)):
+        shp = shard_shape(full_shape, desc)
+        prev = torch.empty(shp, dtype=torch.bfloat16, device=device)
+        nxt = torch.empty(shp, dtype=torch.bfloat16, device=device)
+        if thr_dim0 is not None:
+            tab = torch.tensor(list(thr_dim0), dtype=torch.int64, device=device)
+            check(lib.ws_gen_pair_bf16_dim0(seed, name.encode(), shape_array(full_shape),
+                                            len(full_shape), shard(desc), _ptr(tab), _ptr(prev),
+                                            _ptr(nxt), _stream()))
+            torch.cuda.current_stream(device).synchronize()
+            return prev, nxt
+        thr = int(min(max(density, 0.0), 1.0) * 4294967296.0)
+        check(lib.ws_gen_pair_bf16(seed, name.encode(), shape_array(full_shape), len(full_shape),
+                                   shard(desc), thr, _ptr(prev), _ptr(nxt), _stream()))
         return prev, nxt
-    thr = int(min(max(density, 0.0), 1.0) * 4294967296.0)
-    check(lib.ws_gen_pair_bf16(seed, name.encode(), shape_array(full_shape), len(full_shape),
-                               shard(desc), thr, _ptr(prev), _ptr(nxt), _stream()))
-    return prev, nxt

@@ -159,6 +159,7 @@ ws_status ws_plan_exchange_caps(const ws_plan* plan, uint64_t* send_cap_per_coor
 
 ws_status ws_engine_create(const ws_plan* plan, int device, const uint8_t* unique_id,
                            ws_engine** out) {
+  DeviceGuard device_guard;
   if (!plan || !out) return set_error(WS_INVALID_ARGUMENT, "ws_engine_create: null argument");
   *out = nullptr;
   try {
@@ -181,6 +182,7 @@ void ws_engine_destroy(ws_engine* eng) { delete eng; }
 
 ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev, void* train_next_dev,
                          void* serve_dev) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_bind: null engine");
   const uintptr_t a = (uintptr_t)train_prev_dev | (uintptr_t)train_next_dev | (uintptr_t)serve_dev;
   if (a & 15) return set_error(WS_INVALID_ARGUMENT, "ws_engine_bind: arenas must be 16-byte aligned");
@@ -193,12 +195,14 @@ ws_status ws_engine_bind(ws_engine* eng, void* train_prev_dev, void* train_next_
 }
 
 ws_status ws_engine_generate(ws_engine* eng, uint64_t seed, double density, ws_stream_t stream) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_generate: null engine");
   return eng->generate(seed, density, reinterpret_cast<cudaStream_t>(stream));
 }
 
 ws_status ws_engine_payload(ws_engine* eng, int i, int force_wide_index, void* out_dev,
                             ws_payload_info* info, ws_stream_t stream) {
+  DeviceGuard device_guard;
   if (!eng || !info) return set_error(WS_INVALID_ARGUMENT, "ws_engine_payload: null argument");
   return eng->payload(i, force_wide_index != 0, out_dev, info,
                       reinterpret_cast<cudaStream_t>(stream));
@@ -206,6 +210,7 @@ ws_status ws_engine_payload(ws_engine* eng, int i, int force_wide_index, void* o
 
 ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double density, double zipf_s,
                                    uint64_t perm_seed, ws_stream_t stream) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_generate_skewed: null engine");
   if (!(zipf_s >= 0.0)) return set_error(WS_INVALID_ARGUMENT, "zipf_s must be >= 0");
   return eng->generate(seed, density, reinterpret_cast<cudaStream_t>(stream), zipf_s, perm_seed);
@@ -213,6 +218,7 @@ ws_status ws_engine_generate_skewed(ws_engine* eng, uint64_t seed, double densit
 
 ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts, ws_stream_t stream,
                               ws_report* report) {
+  DeviceGuard device_guard;
   if (!eng || !opts) return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_step: null argument");
   return eng->sync_step(*opts, reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, report);
 }
@@ -220,6 +226,7 @@ ws_status ws_engine_sync_step(ws_engine* eng, const ws_sync_options* opts, ws_st
 ws_status ws_engine_sync_step_host(ws_engine* eng, const void* next_host,
                                    const ws_sync_options* opts, ws_stream_t stream,
                                    uint64_t* nnz_host, ws_report* report) {
+  DeviceGuard device_guard;
   if (!eng || !opts || !next_host)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_step_host: null argument");
   return eng->sync_step(*opts, reinterpret_cast<cudaStream_t>(stream), next_host, nnz_host,
@@ -227,12 +234,14 @@ ws_status ws_engine_sync_step_host(ws_engine* eng, const void* next_host,
 }
 
 ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_timing: null engine");
   return eng->timing(reset, out);
 }
 
 ws_status ws_engine_segment_delta(ws_engine* eng, int i, const uint32_t** idx, const void** val,
                                   uint64_t* nnz, char* codec) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_segment_delta: null engine");
   return eng->segment_delta(i, idx, val, nnz, codec);
 }

@@ -1199,6 +1199,7 @@ ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense
 
 extern "C" ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records,
                                               uint64_t* sent_dense, uint64_t* recv_records) {
+  DeviceGuard device_guard;
   if (!eng || !sent_records || !sent_dense || !recv_records)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_exchange_bytes: null argument");
   return eng->exchange_bytes(sent_records, sent_dense, recv_records);

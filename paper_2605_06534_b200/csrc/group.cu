@@ -80,6 +80,7 @@ void ws_group_destroy(ws_group* g) { delete g; }
 
 ws_status ws_engine_create_grouped(const ws_plan* plan, int device, ws_group* g,
                                    ws_engine** out) {
+  DeviceGuard device_guard;
   if (!plan || !g || !out)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_create_grouped: null argument");
   *out = nullptr;
@@ -104,6 +105,7 @@ ws_status ws_engine_create_grouped(const ws_plan* plan, int device, ws_group* g,
 }
 
 ws_status ws_group_connect(ws_group* g) {
+  DeviceGuard device_guard;
   if (!g) return set_error(WS_INVALID_ARGUMENT, "ws_group_connect: null group");
   if (g->connected) return WS_OK;
   const int W = g->shared.world;
@@ -151,6 +153,7 @@ ws_status ws_group_connect(ws_group* g) {
 
 ws_status ws_group_sync_step(ws_group* g, const ws_sync_options* opts, ws_stream_t stream,
                              ws_report* reports) {
+  DeviceGuard device_guard;
   if (!g || !opts) return set_error(WS_INVALID_ARGUMENT, "ws_group_sync_step: null argument");
   if (!g->connected) return set_error(WS_INVALID_ARGUMENT, "ws_group_sync_step: not connected");
   const int W = g->shared.world;

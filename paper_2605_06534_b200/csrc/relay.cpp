@@ -512,6 +512,7 @@ ws_status ws_engine::release_staging() {
 }
 
 extern "C" ws_status ws_engine_release_staging(ws_engine* eng) {
+  DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_release_staging: null engine");
   return eng->release_staging();
 }
@@ -520,6 +521,7 @@ extern "C" ws_status ws_engine_sync_relay(ws_engine* eng, uint64_t step,
                                           const ws_sync_options* opts,
                                           const ws_relay_options* relay_opts,
                                           const ws_relay* relay, ws_relay_report* report) {
+  DeviceGuard device_guard;
   if (!eng || !opts || !relay_opts || !relay || !report)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: null argument");
   try {
