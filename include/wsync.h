@@ -395,6 +395,18 @@ typedef struct ws_relay {
              uint64_t len);
   int64_t (*get_any)(void* ctx, const char* const* keys, const uint64_t* key_lens, int n,
                      int timeout_ms, int* hit, uint8_t* out, uint64_t cap);
+  /* Optional framed transport (both or neither; NULL: put/get_any above).
+   * Every bucket then travels as the reference's bucket frame
+   * [key_len u32][key][len u32][bucket][crc32 u32] (wire.cpp:35-47), built
+   * and CRC-32'd on the GPU -- e.g. written as is after the PUT op byte of
+   * the reference's TCP relay (tcp_relay.hpp:10-17).  put_frame returns 0,
+   * or 3 when the receiver's CRC check failed (IntegrityError).
+   * get_any_frame returns the length of the whole frame of the first key
+   * present (copied to out when it fits in cap), -1 on timeout; the engine
+   * checks its key and CRC on the GPU (IntegrityError on mismatch). */
+  int (*put_frame)(void* ctx, const uint8_t* frame, uint64_t len);
+  int64_t (*get_any_frame)(void* ctx, const char* const* keys, const uint64_t* key_lens, int n,
+                           int timeout_ms, int* hit, uint8_t* out, uint64_t cap);
 } ws_relay;
 
 typedef struct ws_relay_options {

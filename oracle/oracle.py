@@ -423,6 +423,12 @@ class Reference:
         (ctx, put, get_any) triple of raw pointers, plus helpers."""
         return RefMemoryRelay(self.lib)
 
+    def tcp_relay(self, flip_put=0, flip_get=0):
+        """The reference's TcpRelayServer (tcp_relay.hpp) on a free localhost
+        port, with a framed client for ws_relay's put_frame / get_any_frame
+        (flip_*: corrupt every n-th frame in transit, to test the CRCs)."""
+        return RefTcpRelay(self.lib, flip_put, flip_get)
+
     def frame_crc32(self, data: bytes):
         arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
         return int(self.lib.ref_frame_crc32(_ptr(arr), len(data)))
@@ -516,6 +522,61 @@ class RefState:
             c = self.ref.lib.ref_state_codec(self.h, k, d)
             out.append((tuple(d[:7]), chr(c)))
         return out
+
+
+class RefTcpRelay:
+    """The reference TCP relay server plus the framed client; `callbacks` is
+    the 5-tuple (ctx, put, get_any, put_frame, get_any_frame) of raw C
+    pointers for ws_engine_sync_relay (put/get_any unused: framed only)."""
+
+    def __init__(self, lib, flip_put=0, flip_get=0):
+        self.lib = lib
+        for name, args, res in (
+                ("ref_tcp_server_create", [], C.c_void_p),
+                ("ref_tcp_server_port", [C.c_void_p], C.c_int),
+                ("ref_tcp_server_buckets", [C.c_void_p], C.c_uint64),
+                ("ref_tcp_server_destroy", [C.c_void_p], None),
+                ("ref_tcp_client_create", [C.c_int], C.c_void_p),
+                ("ref_tcp_client_destroy", [C.c_void_p], None),
+                ("ref_tcp_client_get", [C.c_void_p, C.c_char_p, C.c_uint64, C.c_void_p,
+                                        C.c_uint64], C.c_int64),
+                ("ref_framed_client_create", [C.c_int, C.c_int, C.c_int], C.c_void_p),
+                ("ref_framed_client_destroy", [C.c_void_p], None)):
+            fn = getattr(lib, name)
+            fn.argtypes, fn.restype = args, res
+        self.server = lib.ref_tcp_server_create()
+        if not self.server:
+            raise OracleError(99, lib.ref_last_error().decode(errors="replace"))
+        self.port = lib.ref_tcp_server_port(self.server)
+        self.ctx = lib.ref_framed_client_create(self.port, flip_put, flip_get)
+        self.reader = lib.ref_tcp_client_create(self.port)
+        self.callbacks = (self.ctx, None, None, C.cast(lib.ref_framed_put, C.c_void_p).value,
+                          C.cast(lib.ref_framed_get_any, C.c_void_p).value)
+
+    def buckets(self):
+        return int(self.lib.ref_tcp_server_buckets(self.server))
+
+    def get(self, key: str) -> bytes:
+        kb = key.encode("utf-8", "surrogateescape")
+        n = self.lib.ref_tcp_client_get(self.reader, kb, len(kb), None, 0)
+        if n < 0:
+            raise KeyError(key)
+        out = np.empty(max(1, n), np.uint8)
+        self.lib.ref_tcp_client_get(self.reader, kb, len(kb), out.ctypes.data, n)
+        return out[:n].tobytes()
+
+    def close(self):
+        if getattr(self, "server", None):
+            self.lib.ref_framed_client_destroy(self.ctx)
+            self.lib.ref_tcp_client_destroy(self.reader)
+            self.lib.ref_tcp_server_destroy(self.server)
+            self.server = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class RefMemoryRelay:

@@ -19,7 +19,18 @@
 #include "coserve/transfer/key.hpp"
 #include "coserve/transfer/plan.hpp"
 #include "coserve/transfer/relay.hpp"
+#include "coserve/transfer/tcp_relay.hpp"
 #include "coserve/transfer/wire.hpp"
+
+#include <arpa/inet.h>
+#include <netinet/in.h>
+#include <netinet/tcp.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
+#include <map>
+#include <mutex>
+#include <thread>
 
 using namespace coserve;
 using namespace coserve::transfer;
@@ -327,6 +338,167 @@ std::int64_t ref_memrelay_get(void* ctx, const char* key, std::uint64_t klen, st
   } catch (...) {
     return -1;
   }
+}
+
+// ---- the reference's TCP relay server (tcp_relay.hpp), and a client for
+// the engine's framed transport (ws_relay put_frame / get_any_frame): it
+// writes the GPU-built frame after the PUT op byte and hands back the whole
+// frame a GET_ANY returns, so the CRC the reference server checks on PUT was
+// computed on the GPU, and the engine checks the one it gets back.  The
+// protocol is the documented one of tcp_relay.hpp:10-17 (test harness).
+void* ref_tcp_server_create() {
+  try {
+    return new TcpRelayServer(0);
+  } catch (...) {
+    map_exception();
+    return nullptr;
+  }
+}
+int ref_tcp_server_port(void* s) { return static_cast<TcpRelayServer*>(s)->port(); }
+std::uint64_t ref_tcp_server_buckets(void* s) {
+  return static_cast<TcpRelayServer*>(s)->stored_buckets();
+}
+void ref_tcp_server_destroy(void* s) { delete static_cast<TcpRelayServer*>(s); }
+
+// The reference's own client (for reading back what the server stored).
+void* ref_tcp_client_create(int port) {
+  try {
+    return new TcpRelayClient("127.0.0.1", static_cast<std::uint16_t>(port));
+  } catch (...) {
+    map_exception();
+    return nullptr;
+  }
+}
+void ref_tcp_client_destroy(void* c) { delete static_cast<TcpRelayClient*>(c); }
+std::int64_t ref_tcp_client_get(void* c, const char* key, std::uint64_t klen, std::uint8_t* out,
+                                std::uint64_t cap) {
+  try {
+    auto v = static_cast<TcpRelayClient*>(c)->get(std::string(key, klen), 2000);
+    if (v.size() <= cap) std::memcpy(out, v.data(), v.size());
+    return static_cast<std::int64_t>(v.size());
+  } catch (...) {
+    return -1;
+  }
+}
+
+struct FramedClient {
+  int port = 0;
+  int flip_put = 0, flip_get = 0;  // corrupt one byte of every n-th frame (tests)
+  std::mutex mu;
+  std::map<std::thread::id, int> fds;  // one connection per calling thread
+  std::uint64_t puts = 0, gets = 0;
+  int fd() {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = fds.find(std::this_thread::get_id());
+    if (it != fds.end()) return it->second;
+    const int f = ::socket(AF_INET, SOCK_STREAM, 0);
+    if (f < 0) return -1;
+    sockaddr_in a{};
+    a.sin_family = AF_INET;
+    a.sin_port = htons(static_cast<std::uint16_t>(port));
+    a.sin_addr.s_addr = htonl(INADDR_LOOPBACK);
+    if (::connect(f, reinterpret_cast<sockaddr*>(&a), sizeof(a)) != 0) {
+      ::close(f);
+      return -1;
+    }
+    int one = 1;
+    ::setsockopt(f, IPPROTO_TCP, TCP_NODELAY, &one, sizeof(one));
+    fds[std::this_thread::get_id()] = f;
+    return f;
+  }
+  ~FramedClient() {
+    for (auto& kv : fds) ::close(kv.second);
+  }
+};
+
+static bool send_all(int fd, const void* p, std::size_t n) {
+  const char* c = static_cast<const char*>(p);
+  while (n) {
+    const ssize_t k = ::send(fd, c, n, MSG_NOSIGNAL);
+    if (k <= 0) return false;
+    c += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+static bool recv_all(int fd, void* p, std::size_t n) {
+  char* c = static_cast<char*>(p);
+  while (n) {
+    const ssize_t k = ::recv(fd, c, n, 0);
+    if (k <= 0) return false;
+    c += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+
+void* ref_framed_client_create(int port, int flip_put, int flip_get) {
+  auto* c = new FramedClient;
+  c->port = port;
+  c->flip_put = flip_put;
+  c->flip_get = flip_get;
+  return c;
+}
+void ref_framed_client_destroy(void* c) { delete static_cast<FramedClient*>(c); }
+
+int ref_framed_put(void* ctx, const std::uint8_t* frame, std::uint64_t len) {
+  auto* c = static_cast<FramedClient*>(ctx);
+  const int fd = c->fd();
+  if (fd < 0) return -2;
+  std::vector<std::uint8_t> msg(1 + len);
+  msg[0] = 0x01;  // PUT
+  std::memcpy(msg.data() + 1, frame, len);
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->flip_put && ++c->puts % static_cast<std::uint64_t>(c->flip_put) == 0 && len > 16)
+      msg[1 + len / 2] ^= 0x10;  // a flipped bit in transit
+  }
+  std::uint8_t status = 0xff;
+  if (!send_all(fd, msg.data(), msg.size()) || !recv_all(fd, &status, 1)) return -2;
+  return status;  // 0 ok, 3 integrity failure (tcp_relay.hpp:17)
+}
+
+std::int64_t ref_framed_get_any(void* ctx, const char* const* keys, const std::uint64_t* lens,
+                                int n, int timeout_ms, int* hit, std::uint8_t* out,
+                                std::uint64_t cap) {
+  auto* c = static_cast<FramedClient*>(ctx);
+  const int fd = c->fd();
+  if (fd < 0) return -2;
+  std::vector<std::uint8_t> req{0x03};  // GET_ANY
+  auto u32 = [&](std::uint32_t v) {
+    const auto* b = reinterpret_cast<const std::uint8_t*>(&v);
+    req.insert(req.end(), b, b + 4);
+  };
+  u32(static_cast<std::uint32_t>(n));
+  for (int i = 0; i < n; ++i) {
+    u32(static_cast<std::uint32_t>(lens[i]));
+    req.insert(req.end(), keys[i], keys[i] + lens[i]);
+  }
+  u32(static_cast<std::uint32_t>(timeout_ms));
+  std::uint8_t status = 0xff;
+  if (!send_all(fd, req.data(), req.size()) || !recv_all(fd, &status, 1)) return -2;
+  if (status == 1) return -1;  // timeout
+  if (status != 0) return -2;
+  std::uint32_t klen = 0, plen = 0;
+  if (!recv_all(fd, &klen, 4) || klen > kMaxKeyLen) return -2;
+  std::vector<std::uint8_t> f(4 + klen + 4);
+  std::memcpy(f.data(), &klen, 4);
+  if (!recv_all(fd, f.data() + 4, klen) || !recv_all(fd, &plen, 4) || plen > kMaxPayloadLen)
+    return -2;
+  std::memcpy(f.data() + 4 + klen, &plen, 4);
+  f.resize(f.size() + plen + 4);
+  if (!recv_all(fd, f.data() + 8 + klen, plen + 4)) return -2;
+  const std::string key(reinterpret_cast<const char*>(f.data()) + 4, klen);
+  *hit = -1;
+  for (int i = 0; i < n; ++i)
+    if (key == std::string(keys[i], lens[i])) *hit = i;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->flip_get && ++c->gets % static_cast<std::uint64_t>(c->flip_get) == 0 && plen > 4)
+      f[8 + klen + plen / 2] ^= 0x01;
+  }
+  if (f.size() <= cap) std::memcpy(out, f.data(), f.size());
+  return static_cast<std::int64_t>(f.size());
 }
 
 // wire.cpp:9-13

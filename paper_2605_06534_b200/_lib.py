@@ -144,7 +144,8 @@ class PayloadInfo(C.Structure):  # ws_payload_info
 
 
 class Relay(C.Structure):  # ws_relay (function pointers passed as raw addresses)
-    _fields_ = [("ctx", C.c_void_p), ("put", C.c_void_p), ("get_any", C.c_void_p)]
+    _fields_ = [("ctx", C.c_void_p), ("put", C.c_void_p), ("get_any", C.c_void_p),
+                ("put_frame", C.c_void_p), ("get_any_frame", C.c_void_p)]
 
 
 class RelayOptions(C.Structure):  # ws_relay_options

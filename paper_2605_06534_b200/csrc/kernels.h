@@ -141,8 +141,14 @@ cudaError_t launch_fixup_plan(const uint32_t* tile0, int seg_begin, int seg_end,
 constexpr uint32_t kMaxEncodeGrid = 160;  // >= SMs of a B200 (148)
 size_t encode_spill_bytes(int dtype, uint32_t blocks);
 
+// Stream-ordered scratch from the library's own caching pool of the current
+// device (wire.cu); release with cudaFreeAsync on the same stream.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+
 // Ascending segment stream from an unordered K1 output: the segment's
-// super-tiles' records in tile order (one block; API/wire path, not the sync).
+// super-tiles' records in tile order (API / wire / relay path, not the sync):
+// an exclusive scan of the tile counts, then one warp per super-tile copies
+// its records to their ascending place.
 cudaError_t launch_compact(int dtype, const uint32_t* tile_cnt, const uint32_t* tile_base,
                            uint32_t ntiles, uint64_t cap, const uint32_t* in_idx,
                            const void* in_val, uint32_t* out_idx, void* out_val, cudaStream_t s);

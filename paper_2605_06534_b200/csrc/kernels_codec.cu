@@ -756,15 +756,12 @@ __global__ void __launch_bounds__(kEncodeBlock, 1) encode_kernel(EncodeArgs a) {
 
 // ---- compaction of an unordered K1 output ---------------------------------------
 
-template <typename T>
-__global__ void __launch_bounds__(1024) compact_kernel(const uint32_t* tile_cnt,
-                                                       const uint32_t* tile_base, uint32_t ntiles,
-                                                       uint64_t cap, const uint32_t* in_idx,
-                                                       const T* in_val, uint32_t* out_idx,
-                                                       T* out_val) {
-  __shared__ uint32_t s_off[1024];
+// Exclusive scan of the super-tile record counts of one segment (one block;
+// a segment has at most a few tens of thousands of super-tiles).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* tile_cnt,
+                                                         uint32_t ntiles, uint32_t* out_off) {
   __shared__ uint32_t s_warp[32];
-  __shared__ uint64_t s_carry;
+  __shared__ uint32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_carry = 0;
   __syncthreads();
@@ -789,21 +786,33 @@ __global__ void __launch_bounds__(1024) compact_kernel(const uint32_t* tile_cnt,
       s_warp[lane] = wi - w;
     }
     __syncthreads();
-    s_off[tid] = s_warp[warp] + inc - c;
+    const uint32_t carry = s_carry;
+    if (t0 + tid < ntiles) out_off[t0 + tid] = carry + s_warp[warp] + inc - c;
     __syncthreads();
-    const uint64_t carry = s_carry;
-    for (int j = warp; j < 1024 && t0 + j < ntiles; j += 32) {
-      const uint32_t n = tile_cnt[t0 + j];
-      const uint64_t b = tile_base[t0 + j], o = carry + s_off[j];
-      for (uint32_t k = lane; k < n; k += 32)
-        if (b + k < cap && o + k < cap) {
-          out_idx[o + k] = in_idx[b + k];
-          out_val[o + k] = in_val[b + k];
-        }
-    }
+    if (tid == 1023) s_carry = carry + s_warp[31] + inc;
     __syncthreads();
-    if (tid == 1023) s_carry = carry + s_off[1023] + c;
-    __syncthreads();
+  }
+}
+
+// One warp per super-tile: its records, ascending inside the tile, move to
+// their place in the segment's ascending stream (positions >= cap dropped).
+template <typename T>
+__global__ void __launch_bounds__(256) compact_kernel(const uint32_t* tile_cnt,
+                                                      const uint32_t* tile_base,
+                                                      const uint32_t* out_off, uint32_t ntiles,
+                                                      uint64_t cap, const uint32_t* in_idx,
+                                                      const T* in_val, uint32_t* out_idx,
+                                                      T* out_val) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += nw) {
+    const uint32_t n = tile_cnt[t];
+    const uint64_t b = tile_base[t], o = out_off[t];
+    for (uint32_t k = lane; k < n; k += 32)
+      if (b + k < cap && o + k < cap) {
+        out_idx[o + k] = in_idx[b + k];
+        out_val[o + k] = in_val[b + k];
+      }
   }
 }
 
@@ -1280,13 +1289,22 @@ cudaError_t launch_compact(int dtype, const uint32_t* tile_cnt, const uint32_t* 
                            uint32_t ntiles, uint64_t cap, const uint32_t* in_idx,
                            const void* in_val, uint32_t* out_idx, void* out_val, cudaStream_t s) {
   if (!ntiles) return cudaSuccess;
+  uint32_t* off = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&off), (size_t)ntiles * 4, s);
+  if (e != cudaSuccess) return e;
+  tile_scan_kernel<<<1, 1024, 0, s>>>(tile_cnt, ntiles, off);
+  const int grid = (int)std::min<uint64_t>((ntiles + 7) / 8, (uint64_t)sm_count() * 8);
   if (dtype == WS_BF16)
-    compact_kernel<uint16_t><<<1, 1024, 0, s>>>(tile_cnt, tile_base, ntiles, cap, in_idx,
-                                                (const uint16_t*)in_val, out_idx, (uint16_t*)out_val);
+    compact_kernel<uint16_t><<<grid, 256, 0, s>>>(tile_cnt, tile_base, off, ntiles, cap, in_idx,
+                                                  (const uint16_t*)in_val, out_idx,
+                                                  (uint16_t*)out_val);
   else
-    compact_kernel<uint32_t><<<1, 1024, 0, s>>>(tile_cnt, tile_base, ntiles, cap, in_idx,
-                                                (const uint32_t*)in_val, out_idx, (uint32_t*)out_val);
-  return cudaGetLastError();
+    compact_kernel<uint32_t><<<grid, 256, 0, s>>>(tile_cnt, tile_base, off, ntiles, cap, in_idx,
+                                                  (const uint32_t*)in_val, out_idx,
+                                                  (uint32_t*)out_val);
+  e = cudaGetLastError();
+  cudaFreeAsync(off, s);
+  return e;
 }
 
 }  // namespace wsync

@@ -220,14 +220,24 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   double push_s = 0, pull_s = 0, apply_s = 0;
 
   // ---- pusher --------------------------------------------------------------
+  // Framed transport (put_frame / get_any_frame): every bucket travels as the
+  // frame of wire.cpp:35-47, built and CRC-32'd on the GPU; a frame adds
+  // 12 bytes and its key to the bucket.
+  const bool framed = relay.put_frame && relay.get_any_frame;
+  if ((relay.put_frame != nullptr) != (relay.get_any_frame != nullptr))
+    return set_error(WS_INVALID_ARGUMENT, "ws_relay: put_frame and get_any_frame go together");
+  constexpr uint64_t kKeyRoom = 8192;  // key_of's buffer
+  const uint64_t max_buckets = (max_payload + B - 1) / B + 1;
+  const uint64_t frame_cap = std::min<uint64_t>(B, max_payload) + 12 + kKeyRoom;
   void* d_payload = dev_alloc(max_payload);
   uint32_t* d_seq_idx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
   void* d_seq_val = dev_alloc(max_cap * esz);
+  void* d_frames = framed ? dev_alloc(max_payload + max_buckets * (12 + kKeyRoom)) : nullptr;
   std::vector<uint8_t*> stage(depth);
-  for (auto& p : stage) p = host_alloc(std::min<uint64_t>(B, max_payload));
+  for (auto& p : stage) p = host_alloc(framed ? frame_cap : std::min<uint64_t>(B, max_payload));
   std::vector<cudaEvent_t> ev(depth);
   for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  bool staged = d_payload && d_seq_idx && d_seq_val;
+  bool staged = d_payload && d_seq_idx && d_seq_val && (!framed || d_frames);
   for (auto* p : stage) staged = staged && p;
   auto pusher = [&] {
     // (a fresh std::thread in Async mode: its current device is 0)
@@ -255,10 +265,34 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
       const std::string& name = plan_.manifest()[segs[i].shard.param].name;
       const uint64_t total = info.total_bytes;
       const uint64_t nb = total ? (total + B - 1) / B : 1;  // engine.cpp:139
+      std::vector<std::string> keys(nb);
+      for (uint64_t k = 0; k < nb; ++k)
+        keys[k] = key_of(step, name, segs[i].shard, info.codec, info.index_width, (uint32_t)k);
+      std::vector<uint64_t> frame_off(nb + 1, 0);
+      if (framed) {  // every bucket's frame, CRC included, built on the GPU
+        std::vector<const char*> kp(nb);
+        std::vector<uint64_t> kl(nb);
+        for (uint64_t k = 0; k < nb; ++k) {
+          kp[k] = keys[k].data();
+          kl[k] = keys[k].size();
+        }
+        e = ws_encode_bucket_frames_dev(d_payload, total, B, kp.data(), kl.data(), (int)nb,
+                                        d_frames, max_payload + max_buckets * (12 + kKeyRoom),
+                                        frame_off.data(), reinterpret_cast<ws_stream_t>(s_push));
+        if (e != WS_OK) {
+          fail(e, std::string("sync_relay: frames: ") + ws_last_error());
+          return;
+        }
+      }
       auto issue = [&](uint64_t k) {
-        const uint64_t n = std::min(B, total - std::min(total, k * B));
-        cudaMemcpyAsync(stage[k % depth], static_cast<char*>(d_payload) + k * B, n,
-                        cudaMemcpyDeviceToHost, s_push);
+        if (framed) {
+          cudaMemcpyAsync(stage[k % depth], static_cast<char*>(d_frames) + frame_off[k],
+                          frame_off[k + 1] - frame_off[k], cudaMemcpyDeviceToHost, s_push);
+        } else {
+          const uint64_t n = std::min(B, total - std::min(total, k * B));
+          cudaMemcpyAsync(stage[k % depth], static_cast<char*>(d_payload) + k * B, n,
+                          cudaMemcpyDeviceToHost, s_push);
+        }
         cudaEventRecord(ev[k % depth], s_push);
       };
       for (uint64_t k = 0; k < std::min<uint64_t>(nb, depth - 1); ++k) issue(k);
@@ -267,9 +301,15 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         cudaEventSynchronize(ev[k % depth]);
         const uint64_t n = std::min(B, total - std::min(total, k * B));
         push_pacer.acquire(n);
-        const std::string key = key_of(step, name, segs[i].shard, info.codec, info.index_width,
-                                       (uint32_t)k);
-        if (relay.put(relay.ctx, key.data(), key.size(), stage[k % depth], n) != 0) {
+        const std::string& key = keys[k];
+        if (framed) {
+          const int rc = relay.put_frame(relay.ctx, stage[k % depth], frame_off[k + 1] - frame_off[k]);
+          if (rc != 0) {  // 3: the receiver's CRC check failed (tcp_relay.hpp status 3)
+            fail(rc == 3 ? WS_INTEGRITY : WS_TRANSFER_ERROR,
+                 (rc == 3 ? "relay rejected the frame of '" : "relay put failed for '") + key + "'");
+            return;
+          }
+        } else if (relay.put(relay.ctx, key.data(), key.size(), stage[k % depth], n) != 0) {
           fail(WS_TRANSFER_ERROR, "relay put failed for '" + key + "'");
           return;
         }
@@ -281,8 +321,10 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   };
 
   // ---- puller --------------------------------------------------------------
-  uint8_t* h_payload = host_alloc(max_payload);
+  uint8_t* h_payload = host_alloc(framed ? frame_cap : max_payload);
   void* d_in = dev_alloc(max_payload);
+  void* d_frame = framed ? dev_alloc(frame_cap) : nullptr;
+  uint32_t* d_one = framed ? static_cast<uint32_t*>(dev_alloc(8)) : nullptr;
   uint32_t* d_idx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
   void* d_val = dev_alloc(max_cap * 4);
   uint32_t* d_ridx = static_cast<uint32_t*>(dev_alloc(max_cap * 4));
@@ -292,7 +334,7 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   uint32_t* d_rerr = d_err ? d_err + 1 : nullptr;  // reslice's own error word
   size_t ws_bytes = ws_diff_workspace_bytes(max_cap);
   void* d_ws = dev_alloc(ws_bytes);
-  staged = staged && h_payload && d_in && d_idx && d_val && d_ridx && d_rval && d_rnnz && d_err &&
+  staged = staged && (!framed || (d_frame && d_one)) && h_payload && d_in && d_idx && d_val && d_ridx && d_rval && d_rnnz && d_err &&
            d_ws;
   if (!staged) {
     for (auto& e : ev) cudaEventDestroy(e);
@@ -334,6 +376,49 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
   };
   const bool dbg = getenv("WSYNC_RELAY_DEBUG") != nullptr;
   double dt[5] = {0, 0, 0, 0, 0};  // debug: h2d, peek, decode, reslice, apply
+  // Framed pull of one bucket: the frame (in h_payload) is checked on the
+  // GPU -- its CRC-32 over every preceding byte (wire.cpp:45, IntegrityError
+  // on mismatch) and its key -- and its bucket lands at d_in + at.  Returns
+  // the bucket length, or -1 after fail().
+  auto take_frame = [&](int64_t n, const std::string& want_key, uint64_t at,
+                        uint64_t room) -> int64_t {
+    if (n < 12 || (uint64_t)n > frame_cap) {
+      fail(WS_PAYLOAD_FORMAT, "relay frame of '" + want_key + "' is truncated or oversized");
+      return -1;
+    }
+    uint32_t klen = 0, plen = 0, crc = 0;
+    std::memcpy(&klen, h_payload, 4);
+    if ((uint64_t)klen + 12 > (uint64_t)n) {
+      fail(WS_PAYLOAD_FORMAT, "relay frame of '" + want_key + "': key length");
+      return -1;
+    }
+    std::memcpy(&plen, h_payload + 4 + klen, 4);
+    if ((uint64_t)klen + plen + 12 != (uint64_t)n || plen > room) {
+      fail(WS_PAYLOAD_FORMAT, "relay frame of '" + want_key + "': payload length");
+      return -1;
+    }
+    if (std::string(reinterpret_cast<const char*>(h_payload) + 4, klen) != want_key) {
+      fail(WS_PAYLOAD_FORMAT, "relay frame carries another key than '" + want_key + "'");
+      return -1;
+    }
+    std::memcpy(&crc, h_payload + 8 + klen + plen, 4);
+    cudaMemcpyAsync(d_frame, h_payload, (uint64_t)n, cudaMemcpyHostToDevice, s_pull);
+    const void* fp = d_frame;
+    const uint64_t covered = 8 + (uint64_t)klen + plen;
+    uint32_t got = 0;
+    ws_status e = ws_crc32_dev(&fp, &covered, 1, &got, reinterpret_cast<ws_stream_t>(s_pull));
+    if (e != WS_OK) {
+      fail(e, std::string("sync_relay: frame crc: ") + ws_last_error());
+      return -1;
+    }
+    if (got != crc) {
+      fail(WS_INTEGRITY, "frame CRC mismatch for '" + want_key + "'");
+      return -1;
+    }
+    cudaMemcpyAsync(static_cast<char*>(d_in) + at, static_cast<const char*>(d_frame) + 8 + klen,
+                    plen, cudaMemcpyDeviceToDevice, s_pull);
+    return plen;
+  };
   auto puller = [&] {
     const auto t0 = Clock::now();
     double apply_acc = 0;
@@ -348,15 +433,26 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
       const char* kp[3] = {cand[0].data(), cand[1].data(), cand[2].data()};
       const uint64_t kl[3] = {cand[0].size(), cand[1].size(), cand[2].size()};
       int hit = -1;
-      int64_t n0 = relay.get_any(relay.ctx, kp, kl, 3, timeout, &hit, h_payload, max_payload);
-      if (n0 < 0 || hit < 0) {
+      int64_t n0 = framed ? relay.get_any_frame(relay.ctx, kp, kl, 3, timeout, &hit, h_payload,
+                                                frame_cap)
+                          : relay.get_any(relay.ctx, kp, kl, 3, timeout, &hit, h_payload,
+                                          max_payload);
+      if (n0 < 0 || hit < 0 || hit > 2) {
         fail(n0 == -1 ? WS_RELAY_TIMEOUT : WS_TRANSFER_ERROR,
              "relay get_any for '" + cand[1] + "' failed");
         return;
       }
+      const uint8_t* head0 = h_payload;
+      if (framed) {  // bucket 0 to d_in; its payload header read from the host copy
+        uint32_t klen0 = 0;
+        if (n0 >= 12) std::memcpy(&klen0, h_payload, 4);
+        head0 = h_payload + 8 + klen0;
+        n0 = take_frame(n0, cand[hit], 0, max_payload);
+        if (n0 < 0) return;
+      }
       pull_pacer.acquire((uint64_t)n0);
       uint64_t total = 0;
-      if (!payload_total(h_payload, (uint64_t)n0, &total) || total > max_payload) {
+      if (!payload_total(head0, (uint64_t)n0, &total) || total > max_payload) {
         fail(WS_PAYLOAD_FORMAT, "bad first bucket for '" + cand[hit] + "'");
         return;
       }
@@ -375,8 +471,14 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         const char* kkp = kk.data();
         const uint64_t kkl = kk.size();
         int h = -1;
-        const int64_t nk = relay.get_any(relay.ctx, &kkp, &kkl, 1, timeout, &h, h_payload + have,
-                                         max_payload - have);
+        int64_t nk = framed ? relay.get_any_frame(relay.ctx, &kkp, &kkl, 1, timeout, &h,
+                                                  h_payload, frame_cap)
+                            : relay.get_any(relay.ctx, &kkp, &kkl, 1, timeout, &h,
+                                            h_payload + have, max_payload - have);
+        if (framed && nk >= 0) {
+          nk = take_frame(nk, kk, have, total - have);
+          if (nk < 0) return;
+        }
         if (nk < 0 || have + (uint64_t)nk > total) {
           fail(nk == -1 ? WS_RELAY_TIMEOUT : WS_PAYLOAD_FORMAT, "relay get for '" + kk + "' failed");
           return;
@@ -391,7 +493,7 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
         return;
       }
       const auto ta = Clock::now();
-      cudaMemcpyAsync(d_in, h_payload, total, cudaMemcpyHostToDevice, s_pull);
+      if (!framed) cudaMemcpyAsync(d_in, h_payload, total, cudaMemcpyHostToDevice, s_pull);
       cudaStreamSynchronize(s_pull);
       auto tk = Clock::now();
       auto lap = [&](int q) {

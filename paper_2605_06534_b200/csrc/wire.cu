@@ -276,6 +276,9 @@ ws_status wire_cuda(cudaError_t e, const char* what) { return cuda_status(e, wha
 // threshold of 0, every synchronisation handed the memory back to the driver,
 // so each call paid a full allocation (~4 ms per decode on the relay path).
 // The process's default pool is left untouched.
+}  // namespace
+
+namespace wsync {
 std::mutex g_scratch_mu;
 cudaMemPool_t g_scratch_pools[64] = {};
 
@@ -306,6 +309,9 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   }
   return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
+}  // namespace wsync
+
+namespace {
 
 }  // namespace
 

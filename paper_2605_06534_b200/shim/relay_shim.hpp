@@ -46,7 +46,7 @@ inline int64_t relay_get_any(void* ctx, const char* const* keys, const uint64_t*
 }
 
 inline ws_relay bind_relay(coserve::transfer::Relay& relay) {
-  ws_relay r;
+  ws_relay r{};  // no framed transport: the Relay frames (or not) itself
   r.ctx = &relay;
   r.put = &relay_put;
   r.get_any = &relay_get_any;

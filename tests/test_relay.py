@@ -103,3 +103,45 @@ def test_missing_buckets_time_out(reference):
     cb = (relay.ctx, C.cast(drop, C.c_void_p).value, relay.callbacks[2])
     with pytest.raises(ws.RelayTimeout):
         eng.sync_relay(cb, step=1, timeout_ms=200)
+
+
+@pytest.mark.parametrize("mode,density", [("async", 0.01), ("batch", 0.4)])
+def test_gpu_frames_through_reference_tcp_relay(restatement, reference, mode, density):
+    """SURVEY §8(f) rank 3 on a real transport: every bucket travels as the
+    reference's frame (wire.cpp:35-47) built and CRC-32'd on the GPU, written
+    after the PUT op byte to the reference's own TcpRelayServer, which checks
+    the CRC and stores the bucket; the puller gets frames back over GET_ANY
+    and checks key and CRC on the GPU.  The stored buckets equal the
+    reference encoding of the oracle delta; serving == next."""
+    ws, plan, eng = _engine()
+    eng.generate(seed=4, density=density)
+    tcp = reference.tcp_relay()
+    bucket = 512
+    rep = eng.sync_relay(tcp.callbacks, step=3, mode=mode, bucket_bytes=bucket)
+    nb = 0
+    for i, (p, desc, off, n) in enumerate(plan.segments):
+        meta = plan.manifest[p]
+        payload, codec, iw, nxt = _expected_payload(restatement, ws, meta, desc, n, 4, density)
+        r, size, stage = plan.segment_key_fields(i)
+        for q in range(ws.wire.num_buckets(len(payload), bucket)):
+            k = reference.bucket_key(3, meta.name, r, size, stage, desc, codec, iw, q).decode()
+            assert tcp.get(k) == payload[q * bucket:(q + 1) * bucket], k
+            nb += 1
+        assert _bits(eng.serve_view(i)).tobytes() == nxt.tobytes(), meta.name
+    assert tcp.buckets() == nb == rep["push_buckets"] == rep["pull_buckets"]
+    tcp.close()
+
+
+@pytest.mark.parametrize("flip", ["put", "get"])
+def test_corrupted_frames_raise_integrity_error(reference, flip):
+    """A bit flipped in transit: on PUT the reference server's CRC check
+    rejects the GPU-built frame (status 3); on GET the engine's GPU CRC check
+    catches it.  Either way the sync fails with IntegrityError
+    (relay.hpp:20-22)."""
+    ws, plan, eng = _engine()
+    eng.generate(seed=5, density=0.01)
+    tcp = reference.tcp_relay(flip_put=5 if flip == "put" else 0,
+                              flip_get=5 if flip == "get" else 0)
+    with pytest.raises(ws.IntegrityError):
+        eng.sync_relay(tcp.callbacks, step=1, bucket_bytes=512, timeout_ms=2000)
+    tcp.close()
