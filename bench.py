@@ -384,6 +384,16 @@ def run_ours(args):
                  "peak_gbs": 900.0, "measured_peer_copy_gbs": 770.0,
                  "frac_of_900": round(sent / win / 1e9 / 900.0, 4) if win > 0 else None,
                  "frac_of_770": round(sent / win / 1e9 / 770.0, 4) if win > 0 else None}
+        try:  # the pack kernel's NVLink counters from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "route_ncu.json")) as f:
+                rn = json.load(f).get(str(n))
+            if rn and args.config == 2:
+                route["ncu_pack_nvltx_gbs"] = round(rn["pack_nvltx_gbs_mean"], 1)
+                route["ncu_pack_frac_of_900"] = round(rn["pack_frac_of_900_mean"], 4)
+                route["ncu_pack_user_gbs"] = round(rn["pack_user_gbs_mean"], 1)
+                route["ncu_source"] = "profiles/" + rn["source"]
+        except Exception:
+            pass
         if nvl0 is not None and nvl1 is not None:
             tx = (nvl1[0] - nvl0[0]) * 1024 / args.steps
             rx = (nvl1[1] - nvl0[1]) * 1024 / args.steps
