@@ -115,7 +115,7 @@ struct RelayError {
 ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
                                 const ws_relay_options& ro, const ws_relay& relay,
                                 ws_relay_report* rep) {
-  if (!relay.put || !relay.get_any)
+  if (!(relay.put && relay.get_any) && !(relay.put_frame && relay.get_any_frame))
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_sync_relay: relay callbacks missing");
   if (ro.bucket_bytes == 0) return set_error(WS_INVALID_ARGUMENT, "bucket_bytes must be > 0");
   if (cudaSetDevice(device_) != cudaSuccess) return set_error(WS_CUDA, "cudaSetDevice");
