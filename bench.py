@@ -347,8 +347,9 @@ def run_ours(args):
     train_elems = plan.info.train_elems
     nnz = probe["nnz"]
     # K1 reads prev+next (2 B each) and writes idx u32 + val u16 per change;
-    # with the fused apply it also read-modify-writes the 2-B serving element
-    # of every change routed to this GPU's own serving shard (4 B).
+    # with the fused apply (always on in the product build) it also
+    # read-modify-writes the 2-B serving element of every change routed to
+    # this GPU's own serving shard (4 B).
     my_coord = plan.info.serve_coord
     local_frac = (sum(ov for (_, c, _, ov) in plan.routes if c == my_coord) /
                   max(1, train_elems))

@@ -364,3 +364,20 @@ __device__ __forceinline__ void gen_elem_bf16(uint64_t key, uint64_t g, uint64_t
 }
 
 }  // namespace wsync
+
+// ---- ablation switches --------------------------------------------------------
+// The measurements DESIGN.md quotes turned individual mechanisms off through
+// environment variables.  They are read only by the ablation build (make
+// ABLATIONS=1 -> lib/libwsync_ablate.so, loaded with WSYNC_LIB); the
+// product library always runs the measured-best configuration.
+#include <cstdlib>
+namespace wsync {
+inline const char* ablation_env(const char* name) {
+#ifdef WSYNC_ABLATIONS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+}  // namespace wsync

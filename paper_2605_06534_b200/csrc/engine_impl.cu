@@ -100,7 +100,7 @@ ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
   WS_CUDA_TRY(cudaMalloc(&d_fill_, ns * 8), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_fix_list_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
   WS_CUDA_TRY(cudaMalloc(&d_fix_n_, 4), "cudaMalloc");
-  if (const char* f = getenv("WSYNC_COUNT_ONLY")) count_only_ = atoi(f) != 0;
+  if (const char* f = ablation_env("WSYNC_COUNT_ONLY")) count_only_ = atoi(f) != 0;
   spill_blocks_ = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(), ntiles_));
   WS_CUDA_TRY(cudaMalloc(&d_spill_, encode_spill_bytes(dtype_, spill_blocks_)), "cudaMalloc spill");
   WS_CUDA_TRY(cudaMalloc(&d_tile_cnt_, std::max<size_t>(1, ntiles_) * 4), "cudaMalloc");
@@ -158,9 +158,9 @@ ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
   }
   WS_CUDA_TRY(cudaMemcpy(d_fuse_, fuse.data(), fuse.size() * sizeof(FuseEntry),
                          cudaMemcpyHostToDevice), "H2D");
-  if (const char* f = getenv("WSYNC_NO_FUSED_APPLY")) fuse_apply_ = atoi(f) == 0;
+  if (const char* f = ablation_env("WSYNC_NO_FUSED_APPLY")) fuse_apply_ = atoi(f) == 0;
   sa_div_ = dtype_ == WS_BF16 ? 250u : 0u;  // K1 streamed apply from 0.4% density
-  if (const char* f = getenv("WSYNC_SA_DIV")) {
+  if (const char* f = ablation_env("WSYNC_SA_DIV")) {
     sa_div_ = dtype_ == WS_BF16 ? (uint32_t)atoi(f) : 0u;
     sa_env_ = true;
   }
@@ -168,7 +168,7 @@ ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
     WS_CUDA_TRY(cudaHostAlloc(&h_sa_, 16, cudaHostAllocMapped), "cudaHostAlloc");
     h_sa_[0] = h_sa_[1] = 0;
     WS_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sa_), h_sa_, 0), "mapped");
-    if (const char* f = getenv("WSYNC_SA_FORCE")) sa_force_ = atoi(f) != 0;
+    if (const char* f = ablation_env("WSYNC_SA_FORCE")) sa_force_ = atoi(f) != 0;
   }
   WS_CUDA_TRY(cudaMalloc(&d_local_, std::max<size_t>(1, local.size()) * sizeof(LocalEntry)),
               "cudaMalloc");

@@ -435,7 +435,7 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id, GroupShared* group) {
   std::vector<uint64_t> send_full, recv_full;
   exchange_caps(plan_, me, &send_full, &recv_full);
   double frac = 0.25;
-  if (const char* f = getenv("WSYNC_EXCHANGE_FRACTION")) frac = atof(f);
+  if (const char* f = ablation_env("WSYNC_EXCHANGE_FRACTION")) frac = atof(f);
   std::vector<uint64_t> region_cap(c->coords);
   for (int k = 0; k < c->coords; ++k)
     region_cap[k] = send_full[k] ? std::max<uint64_t>(4096, (uint64_t)(frac * send_full[k])) : 0;
@@ -595,9 +595,7 @@ ws_status ws_engine::init_p2p() {
   P.ent_cnt = c->d_ent_cnt;
   P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_head) + kMailboxBytes);
   P.err = c->d_err;
-#ifdef WSYNC_ABLATIONS
-  if (const char* d = getenv("WSYNC_P2P_DEBUG")) P.debug = atoi(d);
-#endif
+  if (const char* d = ablation_env("WSYNC_P2P_DEBUG")) P.debug = atoi(d);
   c->nsend_entries = (int)mine.size();
   WS_CUDA_TRY(cudaMemset(c->d_err, 0, 4), "memset");
   c->p2p = true;
@@ -702,7 +700,7 @@ ws_status ws_engine::map_serve() {
   P.dense_direct = 0;
   std::vector<void*> ps;
   const bool ok = c->fab->share(serve, &ps) == WS_OK;
-  const char* env = getenv("WSYNC_DENSE_DIRECT");
+  const char* env = ablation_env("WSYNC_DENSE_DIRECT");
   if (ok) {
     c->peer_serve = ps;
     if (!(env && env[0] == '0')) {
@@ -796,7 +794,7 @@ ws_status ws_engine::exchange_fuse_k1(EncodeArgs& a, cudaStream_t s) {
   // waiting for the previous step's acks inside K1 couples the ranks' start
   // times; the pack it replaces costs 0.2-0.5 ms.  See DESIGN.md §6.
   static const bool enabled = [] {
-    const char* e = getenv("WSYNC_FUSED_REMOTE");
+    const char* e = ablation_env("WSYNC_FUSED_REMOTE");
     return e && e[0] == '1';
   }();
   // Only with direct dense boxes: a segment that comes out dense after K1
@@ -916,11 +914,11 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
   Comm* c = comm_;
   const int R = c->R;
   static const int overlap_sms = [] {
-    const char* e = getenv("WSYNC_OVERLAP_SMS");
+    const char* e = ablation_env("WSYNC_OVERLAP_SMS");
     return e ? std::max(0, atoi(e)) : 28;
   }();
   static const bool overlap = [] {
-    const char* e = getenv("WSYNC_OVERLAP");
+    const char* e = ablation_env("WSYNC_OVERLAP");
     return !(e && e[0] == '0');
   }();
   cudaStream_t ks = c->s_enc, xs = overlap ? c->s_xchg : c->s_enc;

@@ -1056,13 +1056,13 @@ cudaError_t launch_encode(int dtype, const EncodeArgs& a, cudaStream_t s, int* g
   // one persistent block per SM; the producer warp claims super-tiles in order
   int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)sm_count(),
                                                            std::max(a.ntiles, 1u)));
-  if (const char* g = getenv("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
+  if (const char* g = ablation_env("WSYNC_ENCODE_GRID")) grid = std::max(1, atoi(g));
   if (a.max_grid) grid = std::min<int>(grid, (int)a.max_grid);
   if (!a.spill || a.spill_blocks == 0) return cudaErrorInvalidValue;
   grid = std::min<int>(grid, (int)a.spill_blocks);
   if (grid_out) *grid_out = grid;
   EncodeArgs a2 = a;
-  if (const char* d = getenv("WSYNC_ENCODE_DEBUG")) a2.debug = (uint32_t)atoi(d);
+  if (const char* d = ablation_env("WSYNC_ENCODE_DEBUG")) a2.debug = (uint32_t)atoi(d);
   cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   switch (dtype) {

@@ -374,7 +374,7 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
     ws_bytes = ws_diff_workspace_bytes(grown.cap);
     return true;
   };
-  const bool dbg = getenv("WSYNC_RELAY_DEBUG") != nullptr;
+  const bool dbg = ablation_env("WSYNC_RELAY_DEBUG") != nullptr;
   double dt[5] = {0, 0, 0, 0, 0};  // debug: h2d, peek, decode, reslice, apply
   // Framed pull of one bucket: the frame (in h_payload) is checked on the
   // GPU -- its CRC-32 over every preceding byte (wire.cpp:45, IntegrityError
