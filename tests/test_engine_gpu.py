@@ -251,7 +251,7 @@ def test_predicted_dense_segments_fixup(restatement, first):
         assert rep["nnz"] == total
 
 
-@pytest.mark.parametrize("density", [0.006, 0.03, 0.15])
+@pytest.mark.parametrize("density", [0.006, 0.012, 0.03, 0.15])
 def test_streamed_apply_adds_delta(density):
     """K1's streamed apply (fuse_on = 2): from the second sync
     on, fused segments denser than 1/sa_div get serve + (next - prev) stored
@@ -273,6 +273,7 @@ def test_streamed_apply_adds_delta(density):
         before.append(v.to(torch.int32) & 0xFFFF)
     rep = eng.sync_step()
     torch.cuda.synchronize()
+    assert rep["streamed_apply"] == 1, rep
     dense = 0
     for i in range(len(plan.segments)):
         p = eng.segment_view(i, 0).view(torch.int16).to(torch.int32) & 0xFFFF
