@@ -282,7 +282,11 @@ typedef struct ws_plan ws_plan;
  * shards it encodes (plan_pushes), which serving shards it holds
  * (ServeState::init, engine.cpp:34-49), and the route from every trainer
  * shard to every serving shard that intersects it (plan_pulls,
- * plan.cpp:89-121, extended with box intersection across dims).  Errors:
+ * plan.cpp:89-121, extended with box intersection across dims).
+ * world == 1 with a multi-rank layout is a one-GPU plan of that layout: the
+ * one GPU encodes every trainer rank's shards and holds every serving
+ * coordinate's shards (one replica), all routes local -- the whole
+ * TransferEngine::sync_step of engine.cpp:66-254 on one device.  Errors:
  * WS_INDIVISIBLE_SHAPE, WS_UNKNOWN_MODULE_KIND, WS_INCOMPLETE_COVERAGE,
  * WS_INVALID_ARGUMENT (world != layout sizes). */
 ws_status ws_plan_create(const ws_param* params, int nparams, ws_dtype dtype,
@@ -295,7 +299,8 @@ typedef struct ws_plan_info {
   int32_t num_segments;       /* trainer shards encoded on this rank */
   int32_t num_serve_shards;   /* serving shards resident on this rank */
   int32_t num_routes;         /* (segment, serving coordinate) pairs */
-  int32_t serve_coord;        /* this rank's serving coordinate, -1 if none */
+  int32_t serve_coord;        /* this rank's serving coordinate; -1 if none, or all of
+                                 them (one-GPU plan of a multi-rank layout) */
   uint64_t train_arena_elems; /* prev/next arena sizes (elements) */
   uint64_t serve_arena_elems;
   uint64_t train_elems;       /* sum of segment sizes (dense-equivalent) */
@@ -310,6 +315,9 @@ ws_status ws_plan_segment(const ws_plan* plan, int i, int32_t* param,
 /* Serving shard i of this rank. */
 ws_status ws_plan_serve_shard(const ws_plan* plan, int i, int32_t* param,
                               ws_shard* desc, uint64_t* offset, uint64_t* n);
+/* Serving coordinate (stage * tp + tp rank, plan.hpp:44) of serving shard i. */
+ws_status ws_plan_serve_shard_coord(const ws_plan* plan, int i, int32_t* coord);
+
 /* The ShardDescriptor fields of segment i that its bucket keys carry
  * (BucketKey::for_shard, key.hpp:55-67). */
 ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_rank,
@@ -508,6 +516,10 @@ ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out);
  * sent / received.  Zero at world 1.  Synchronises. */
 ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records, uint64_t* sent_dense,
                                    uint64_t* recv_records);
+
+/* Every segment's change count and codec ('S' sparse, 'D' dense) from the
+ * last sync (num_segments entries each; either may be NULL).  Synchronises. */
+ws_status ws_engine_segment_counts(ws_engine* eng, uint64_t* nnz, char* codec);
 
 /* Segment i's delta stream from the last sync: device pointers into the
  * engine's record buffer, its record count (host, needs a synchronised

@@ -228,6 +228,8 @@ _SIGS = {
     "ws_engine_exchange_bytes": ([_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)],
                                  C.c_int),
     "ws_engine_release_staging": ([_vp], C.c_int),
+    "ws_plan_serve_shard_coord": ([_vp, C.c_int, C.POINTER(_i32)], C.c_int),
+    "ws_engine_segment_counts": ([_vp, C.POINTER(_u64), C.c_char_p], C.c_int),
     "ws_group_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
     "ws_group_destroy": ([_vp], None),
     "ws_engine_create_grouped": ([_vp, C.c_int, _vp, C.POINTER(_vp)], C.c_int),

@@ -112,6 +112,13 @@ ws_status ws_plan_segment(const ws_plan* plan, int i, int32_t* param, ws_shard* 
   return WS_OK;
 }
 
+ws_status ws_plan_serve_shard_coord(const ws_plan* plan, int i, int32_t* coord) {
+  if (!plan || !coord || i < 0 || i >= (int)plan->p->serve_shards().size())
+    return set_error(WS_INVALID_ARGUMENT, "ws_plan_serve_shard_coord: index out of range");
+  *coord = plan->p->serve_shard_coord(i);
+  return WS_OK;
+}
+
 ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_rank,
                                      int32_t* tp_size, int32_t* pp_stage) {
   if (!plan || i < 0 || i >= (int)plan->p->segments().size())
@@ -237,6 +244,12 @@ ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out) {
   DeviceGuard device_guard;
   if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_timing: null engine");
   return eng->timing(reset, out);
+}
+
+ws_status ws_engine_segment_counts(ws_engine* eng, uint64_t* nnz, char* codec) {
+  DeviceGuard device_guard;
+  if (!eng) return set_error(WS_INVALID_ARGUMENT, "ws_engine_segment_counts: null engine");
+  return eng->segment_counts(nnz, codec);
 }
 
 ws_status ws_engine_segment_delta(ws_engine* eng, int i, const uint32_t** idx, const void** val,

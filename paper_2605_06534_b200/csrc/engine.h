@@ -27,6 +27,7 @@ struct ws_engine {
                       uint64_t* nnz_host, ws_report* report);
   ws_status segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
                           char* codec);
+  ws_status segment_counts(uint64_t* nnz, char* codec);
   ws_status timing(int reset, ws_timing* out);
   ws_status payload(int i, bool wide, void* out_dev, ws_payload_info* info, cudaStream_t s);
   // payload of segment i from its ascending stream (idx, val, nnz, codec);

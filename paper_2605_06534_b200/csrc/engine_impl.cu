@@ -129,19 +129,24 @@ ws_status ws_engine::init(const uint8_t* unique_id, bool grouped) {
 
   // Local routes: destinations on this GPU's serving coordinate.
   std::vector<LocalEntry> local;
-  const int me = plan_.my_coord();
+  std::vector<int> local_per_seg(std::max(1, nseg_), 0);
   for (const Route& r : plan_.routes()) {
-    if (r.coord != me) continue;
+    if (!plan_.route_is_local(r)) continue;
     const ParamMeta& p = plan_.manifest()[r.dst.param];
     local.push_back(make_local_entry(dtype_, p.shape.data(), (int)p.shape.size(), r.seg,
                                      segs[r.seg].shard.d, r.dst.d, r.dst_offset));
+    ++local_per_seg[r.seg];
   }
   nlocal_ = (int)local.size();
-  // Per-segment fused-apply entries for K1 (a segment feeds at most one
-  // serving shard of this GPU: one shard per parameter per coordinate).
+  // Per-segment fused-apply entries for K1: a segment feeding exactly one
+  // serving shard of this GPU (one shard per parameter per coordinate; a
+  // one-GPU plan of a multi-rank layout can hold several) has it applied by
+  // K1; the others go through the local route.
   std::vector<FuseEntry> fuse(std::max(1, nseg_));
   for (auto& f : fuse) f = FuseEntry{};
-  for (const LocalEntry& e : local) {
+  for (LocalEntry& e : local) {
+    if (local_per_seg[e.seg] != 1) continue;
+    e.fused_ok = 1;
     FuseEntry& f = fuse[e.seg];
     f.mode = e.identity ? 1 : 2;
     f.keep_lo = e.keep_lo;
@@ -508,6 +513,18 @@ ws_status ws_engine::sync_step_impl(const ws_sync_options& o, cudaStream_t s,
     }
   }
   return sync_finish(x, s, nnz_host, report);
+}
+
+ws_status ws_engine::segment_counts(uint64_t* nnz, char* codec) {
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  std::vector<uint64_t> n(std::max(1, nseg_), 0);
+  if (nseg_) WS_CUDA_TRY(cudaMemcpy(n.data(), d_nnz_, nseg_ * 8, cudaMemcpyDeviceToHost), "D2H");
+  for (int i = 0; i < nseg_; ++i) {
+    if (nnz) nnz[i] = n[i];
+    if (codec) codec[i] = (last_sparse_ && (!ntiles_ || n[i] <= segs_[i].cap)) ? 'S' : 'D';
+  }
+  return WS_OK;
 }
 
 ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,

@@ -23,10 +23,16 @@ __device__ __forceinline__ bool seg_dense(const RouteSideArgs& a, int seg) {
   return !a.sparse || a.seg_nnz[seg] > a.seg_cap[seg];
 }
 
+// K1 applied entry e's records as it wrote them (the segment's only local
+// route, fused this sync)
+__device__ __forceinline__ bool entry_fused(const RouteSideArgs& a, const LocalEntry& e) {
+  return a.fused && e.fused_ok && a.fuse_on[e.seg];
+}
+
 // sparse, not fused, and dense enough to apply by streaming (local routes)
-__device__ __forceinline__ bool seg_stream(const RouteSideArgs& a, int seg) {
-  return a.stream_apply && !(a.fused && a.fuse_on[seg]) &&
-         a.seg_nnz[seg] * kStreamDiv > a.segs[seg].n;
+__device__ __forceinline__ bool entry_stream(const RouteSideArgs& a, const LocalEntry& e) {
+  return a.stream_apply && !entry_fused(a, e) &&
+         a.seg_nnz[e.seg] * kStreamDiv > a.segs[e.seg].n;
 }
 
 // Super-tiles [*ta, *tb) of an entry's segment that can hold records for it:
@@ -48,11 +54,11 @@ __device__ __forceinline__ void entry_tiles(const RouteSideArgs& a, const LocalE
 // Units of one entry: groups of kTilesPerUnit super-tiles of records
 // (sparse) or row-run chunks (dense).
 __device__ __forceinline__ uint64_t entry_units(const RouteSideArgs& a, const LocalEntry& e) {
-  if (seg_dense(a, e.seg) || seg_stream(a, e.seg)) {
+  if (seg_dense(a, e.seg) || entry_stream(a, e)) {
     const uint64_t per_row = (e.box.run + kCopyChunk - 1) / kCopyChunk;
     return e.box.rows * per_row;
   }
-  if (a.fused && a.fuse_on[e.seg]) return 0;  // K1 applied the sparse records as it wrote them
+  if (entry_fused(a, e)) return 0;  // K1 applied the sparse records as it wrote them
   if (a.k1_emitted) return 0;                  // K1 stored them into the receivers' regions
   if (a.seg_nnz[e.seg] == 0) return 0;
   uint32_t ta, tb;
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
   for (int base = 0; base < a.nentries; base += kWlThreads) {
     const int e = base + tid;
     const uint64_t u = e < a.nentries ? entry_units(a, a.entries[e]) : 0;
-    if (e < a.nentries && a.fused) {
+    if (e < a.nentries && a.fused && a.entries[e].fused_ok) {
       // Next sync: fuse the apply into K1 only for segments that stayed well
       // below the dense threshold; the others skip the scattered
       // read-modify-writes of records a dense copy would overwrite anyway.
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
     const LocalEntry& E = a.entries[s_entry];
     const uint64_t lu = u - s_u0;
     __syncthreads();
-    const bool stream = !seg_dense(a, E.seg) && seg_stream(a, E.seg);
+    const bool stream = !seg_dense(a, E.seg) && entry_stream(a, E);
     if (!seg_dense(a, E.seg) && !stream) {
       uint64_t k0, k1;
       warp_tile_records(a, E, lu, threadIdx.x >> 5, &k0, &k1);

@@ -123,8 +123,15 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
   if (world <= 0 || rank < 0 || rank >= world)
     throw PlanError{WS_INVALID_ARGUMENT, "rank " + std::to_string(rank) + " of " +
                                              std::to_string(world)};
-  if (serve.tp <= 0 || serve.pp <= 0 || serve.replicas <= 0 ||
-      serve.tp * serve.pp * serve.replicas != world)
+  if (serve.tp <= 0 || serve.pp <= 0 || serve.replicas <= 0)
+    throw PlanError{WS_INVALID_ARGUMENT, "serve tp, pp and replicas must be positive"};
+  const int train_ranks =
+      train.scheme == WS_TRAIN_TP ? train.tp * train.pp * train.dp : world;
+  // world 1 with a multi-rank layout: one GPU hosts every rank
+  collapsed_ = world == 1 && (train_ranks > 1 || serve.tp * serve.pp > 1);
+  if (collapsed_ && serve.replicas != 1)
+    throw PlanError{WS_INVALID_ARGUMENT, "a one-GPU plan of a multi-rank layout has one replica"};
+  if (!collapsed_ && serve.tp * serve.pp * serve.replicas != world)
     throw PlanError{WS_INVALID_ARGUMENT, "serve tp*pp*replicas must equal the world size"};
   if (manifest_.empty()) throw PlanError{WS_INVALID_ARGUMENT, "empty manifest"};
   for (const auto& p : manifest_) {
@@ -147,9 +154,9 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
   segments_.assign(world, {});
   if (train.scheme == WS_TRAIN_TP) {
     // plan.cpp:8-21: every shard dealt round-robin over dp; the dealt rank's
-    // GPU at (stage, tp_rank) encodes it.
+    // GPU at (stage, tp_rank) encodes it (rank 0 when collapsed).
     if (train.tp <= 0 || train.pp <= 0 || train.dp <= 0 ||
-        train.tp * train.pp * train.dp != world)
+        (!collapsed_ && train.tp * train.pp * train.dp != world))
       throw PlanError{WS_INVALID_ARGUMENT, "train tp*pp*dp must equal the world size"};
     size_t next = 0;
     for (int p = 0; p < P; ++p) {
@@ -158,7 +165,7 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
         const int g = dp_rank * train.pp * train.tp + d.pp_stage * train.tp + d.tp_rank;
         Segment s;
         s.shard = d;
-        segments_[g].push_back(s);
+        segments_[collapsed_ ? 0 : g].push_back(s);
       }
     }
   } else if (train.scheme == WS_TRAIN_FSDP) {
@@ -210,9 +217,21 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
     }
     serve_arena_by_coord_[c] = off;
   }
+  if (collapsed_) {  // every coordinate's arena, one after the other
+    for (int c = 0; c < C; ++c) {
+      for (ServeShard ss : serve_by_coord_[c]) {
+        ss.offset += serve_all_elems_;
+        serve_all_.push_back(ss);
+        serve_all_coord_.push_back(c);
+      }
+      serve_all_elems_ += serve_arena_by_coord_[c];
+    }
+  }
 
   // ---- routes: box intersections (plan_pulls, plan.cpp:89-121, extended) ---
   routes_.assign(world, {});
+  std::vector<uint64_t> coord_base(C, 0);  // collapsed: coordinate c's arena offset
+  for (int c = 1; c < C; ++c) coord_base[c] = coord_base[c - 1] + serve_arena_by_coord_[c - 1];
   std::map<std::pair<int, int>, uint64_t> covered;  // (coord, param) -> elements
   for (int r = 0; r < world; ++r) {
     const auto& segs = segments_[r];
@@ -227,7 +246,7 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
           rt.seg = si;
           rt.coord = c;
           rt.dst = ss.shard;
-          rt.dst_offset = ss.offset;
+          rt.dst_offset = ss.offset + (collapsed_ ? coord_base[c] : 0);
           rt.overlap = ov;
           routes_[r].push_back(rt);
           covered[{c, src.param}] += ov;
@@ -251,7 +270,9 @@ int Plan::coord_of_rank(int r) const {
   return r % coords();
 }
 
-uint64_t Plan::serve_arena_elems() const { return serve_arena_by_coord_[my_coord()]; }
+uint64_t Plan::serve_arena_elems() const {
+  return collapsed_ ? serve_all_elems_ : serve_arena_by_coord_[my_coord()];
+}
 
 uint64_t Plan::train_elems() const {
   uint64_t n = 0;

@@ -77,12 +77,22 @@ class Plan {
   int replicas() const { return serve_.replicas; }
   int coord_of_rank(int r) const;            // -1 when rank r holds no serving shard
   int rank_of(int replica, int coord) const { return replica * coords() + coord; }
+  // One GPU hosts every rank of a multi-rank layout (world 1 with trainer
+  // ranks or serving coordinates > 1): all logical trainer ranks' shards are
+  // its segments, all coordinates' serving shards its serving arena, and
+  // every route is local.
+  bool collapsed() const { return collapsed_; }
+  bool route_is_local(const Route& r) const { return collapsed_ || r.coord == my_coord(); }
 
   // This rank's view.
   const std::vector<Segment>& segments() const { return segments_[rank_]; }
-  const std::vector<ServeShard>& serve_shards() const { return serve_by_coord_[my_coord()]; }
+  const std::vector<ServeShard>& serve_shards() const {
+    return collapsed_ ? serve_all_ : serve_by_coord_[my_coord()];
+  }
+  // serving coordinate of serve_shards()[i]
+  int serve_shard_coord(int i) const { return collapsed_ ? serve_all_coord_[i] : my_coord(); }
   const std::vector<Route>& routes() const { return routes_[rank_]; }
-  int my_coord() const { return coord_of_rank(rank_); }
+  int my_coord() const { return collapsed_ ? -1 : coord_of_rank(rank_); }
   uint64_t train_arena_elems() const { return train_arena_[rank_]; }
   uint64_t serve_arena_elems() const;
 
@@ -99,6 +109,10 @@ class Plan {
   ws_train_layout train_;
   ws_serve_layout serve_;
   int world_, rank_;
+  bool collapsed_ = false;
+  std::vector<ServeShard> serve_all_;      // collapsed: every coordinate's shards
+  std::vector<int> serve_all_coord_;
+  uint64_t serve_all_elems_ = 0;
   uint64_t model_elems_ = 0;
   std::vector<std::vector<Segment>> segments_;        // per rank
   std::vector<uint64_t> train_arena_;                 // per rank

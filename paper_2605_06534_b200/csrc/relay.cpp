@@ -186,10 +186,10 @@ ws_status ws_engine::sync_relay(uint64_t step, const ws_sync_options& o,
     const Route* route;
   };
   std::vector<Pull> pulls;
-  const int my_coord = plan_.my_coord();
   for (int g = 0; g < plan_.world(); ++g)
     for (const Route& r : plan_.routes_of(g))
-      if (r.coord == my_coord) pulls.push_back(Pull{&plan_.segments_of(g)[r.seg], &r});
+      if (g == plan_.rank() ? plan_.route_is_local(r) : r.coord == plan_.my_coord())
+        pulls.push_back(Pull{&plan_.segments_of(g)[r.seg], &r});
   // sizes: the largest payload (dense bound) and record count of a shard
   // pushed or pulled here (a sparse payload holds at most threshold x n + 1)
   uint64_t max_payload = 64, max_n = 1, max_cap = 1;

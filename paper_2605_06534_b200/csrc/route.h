@@ -39,7 +39,7 @@ struct LocalEntry {
   int32_t seg;
   int32_t identity;
   int32_t coord;              // destination serving coordinate (pack region)
-  int32_t pad_;
+  int32_t fused_ok;           // the segment's only local route: K1 may apply it (fuse_on)
   uint32_t keep_lo, keep_hi;  // identity: keep src-local i in [keep_lo, keep_hi)
   int64_t shift;              // identity: dst-local = i + shift
   uint64_t dst_base;          // serving shard offset (elements)

@@ -81,6 +81,13 @@ class Plan:
             check(lib.ws_plan_serve_shard(h, i, C.byref(p), C.byref(d), C.byref(off),
                                           C.byref(n)))
             self.serve_shards.append((p.value, (d.slice_dim, d.start, d.end), off.value, n.value))
+        # serving coordinate of every serving shard (all coordinates on a
+        # one-GPU plan of a multi-rank layout)
+        self.serve_coords = []
+        for i in range(info.num_serve_shards):
+            c = C.c_int32()
+            check(lib.ws_plan_serve_shard_coord(h, i, C.byref(c)))
+            self.serve_coords.append(c.value)
         self.routes = []
         for i in range(info.num_routes):
             s, c, r, ov = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()

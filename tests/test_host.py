@@ -148,9 +148,40 @@ def test_plan_errors():
     with pytest.raises(ws.UnknownModuleKind):
         ws.Plan([ws.ParamMeta("w", 99, (8, 4), 0)], ws.BF16, ws.TrainConfig("fsdp"),
                 ws.ServeConfig(1, 1, 1))
-    with pytest.raises(ws.InvalidArgument):
+    with pytest.raises(ws.InvalidArgument):  # 2 trainer ranks on 4 GPUs
         ws.Plan([ws.ParamMeta("w", K.NORM, (8,), 0)], ws.BF16, ws.TrainConfig("tp", 2, 1, 1),
-                ws.ServeConfig(1, 1, 1), world=1, rank=0)
+                ws.ServeConfig(2, 1, 2), world=4, rank=0)
+    with pytest.raises(ws.InvalidArgument):  # a one-GPU plan holds one replica
+        ws.Plan([ws.ParamMeta("w", K.NORM, (8,), 0)], ws.BF16, ws.TrainConfig("tp", 2, 1, 1),
+                ws.ServeConfig(1, 1, 2), world=1, rank=0)
+
+
+@pytest.mark.parametrize("train,serve", [((2, 2, 2), (4, 2)), ((1, 2, 3), (2, 1)),
+                                         ((4, 1, 1), (2, 2))])
+def test_one_gpu_plan_is_the_union_of_the_ranks(train, serve):
+    """world 1 with a multi-rank layout: the segments are every trainer
+    rank's shards (plan_pushes, plan.cpp:8-21), the serving shards every
+    coordinate's (ServeState::init, engine.cpp:34-49), each route local."""
+    import paper_2605_06534_b200 as ws
+    m = ws.toy_transformer_manifest(layers=4, hidden=64, vocab=128)
+    W = train[0] * train[1] * train[2]
+    one = ws.Plan(m, ws.I32, ws.TrainConfig("tp", *train), ws.ServeConfig(serve[0], serve[1], 1),
+                  world=1, rank=0)
+    reps = max(1, W // (serve[0] * serve[1]))
+    segs, routes = [], 0
+    if W % (serve[0] * serve[1]) == 0:
+        for r in range(W):
+            pr = ws.Plan(m, ws.I32, ws.TrainConfig("tp", *train),
+                         ws.ServeConfig(serve[0], serve[1], reps), world=W, rank=r)
+            segs += [(p, d, n) for (p, d, off, n) in pr.segments]
+            routes += len(pr.routes)
+        assert sorted(segs) == sorted((p, d, n) for (p, d, off, n) in one.segments)
+        assert routes == one.info.num_routes
+    # every coordinate's serving shards, laid out one coordinate after the other
+    assert set(one.serve_coords) == set(range(serve[0] * serve[1]))
+    offs = [off for (_, _, off, _) in one.serve_shards]
+    assert offs == sorted(offs) and one.info.serve_arena_elems >= offs[-1] + one.serve_shards[-1][3]
+    assert one.info.serve_coord == -1
 
 
 def test_arena_alignment():

@@ -7,7 +7,10 @@ oracle), compiled unmodified by oracle/Makefile with tests/ref/doctest.h:
 * transfer_test_dropin -- linked with paper_2605_06534_b200/shim/codec_shim.cpp
                           instead of codec.cpp, so the reference engine's
                           diff / reslice / apply run on the B200 kernels through
-                          the C-ABI (the drop-in proof; GPU).
+                          the C-ABI (the drop-in proof, INTEGRATION.md; GPU);
+* transfer_test_dropin_engine -- also engine_shim.cpp instead of engine.cpp:
+                          TransferEngine::sync_step itself runs on libwsync's
+                          resident-arena engine (GPU).
 """
 import os
 import subprocess
@@ -35,5 +38,18 @@ def test_reference_suite_on_reference_codec():
 @pytest.mark.gpu
 def test_reference_suite_on_b200_kernels():
     rc, log = _run("transfer_test_dropin")
+    assert rc == 0, log[-4000:]
+    assert "test cases: 21 | failed: 0" in log
+
+
+@pytest.mark.gpu
+def test_reference_suite_on_b200_engine():
+    """The sync-level drop-in: engine_shim.cpp replaces engine.cpp (and
+    codec_shim.cpp codec.cpp), so every TransferEngine::sync_step of the
+    reference's suite -- 8 modes x exactness, the dense fallback, the byte
+    accounting of shard-aware and naive pulls, 12 randomized layouts checked
+    by the element-level oracle (transfer_cases.hpp) -- runs on libwsync's
+    one-GPU engine (ws_plan_create with world 1 hosting every rank)."""
+    rc, log = _run("transfer_test_dropin_engine")
     assert rc == 0, log[-4000:]
     assert "test cases: 21 | failed: 0" in log
