@@ -305,6 +305,29 @@ struct Box {
   uint32_t ext[WS_MAX_DIMS];
 };
 
+// Unsigned 32-bit division by a run-time constant as a multiply-high and
+// shifts (round-up method): q = (t + ((n - t) >> 1)) >> (l - 1), t =
+// mulhi(m, n), l = ceil(log2 d), m = 2^32 (2^l - d) / d + 1; exact for every
+// 32-bit n.  The reslice's per-record coordinate split would otherwise pay
+// two hardware-less integer divisions per dimension.
+struct FastDiv {
+  uint32_t d, m, l;  // l == 0: d == 1
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d <= 1) return f;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.l = l;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  return f;
+}
+__device__ __forceinline__ uint32_t fastdiv(const FastDiv& f, uint32_t n) {
+  if (f.l == 0) return n;
+  const uint32_t t = __umulhi(f.m, n);
+  return (t + ((n - t) >> 1)) >> (f.l - 1);
+}
+
 // Source-local flat index -> destination-local flat index, or ~0ull when the
 // element lies outside the destination box (codec.cpp:125-131 generalised).
 struct Remap {
@@ -312,6 +335,7 @@ struct Remap {
   uint32_t src_ext[WS_MAX_DIMS];
   int64_t shift[WS_MAX_DIMS];   // src.lo - dst.lo
   uint32_t dst_ext[WS_MAX_DIMS];
+  FastDiv div[WS_MAX_DIMS];     // by src_ext[d]
 };
 
 __device__ __forceinline__ unsigned long long remap_index(const Remap& m, uint32_t i) {
@@ -320,8 +344,9 @@ __device__ __forceinline__ unsigned long long remap_index(const Remap& m, uint32
 #pragma unroll
   for (int d = WS_MAX_DIMS - 1; d >= 0; --d) {
     if (d < m.nd) {
-      c[d] = rem % m.src_ext[d];
-      rem /= m.src_ext[d];
+      const uint32_t q = fastdiv(m.div[d], rem);
+      c[d] = rem - q * m.src_ext[d];
+      rem = q;
     }
   }
   unsigned long long di = 0;

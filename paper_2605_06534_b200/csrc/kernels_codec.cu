@@ -1174,6 +1174,7 @@ Remap make_remap(const int64_t* full, int nd, const ws_shard& src, const ws_shar
     m.src_ext[i] = S.ext[i];
     m.dst_ext[i] = D.ext[i];
     m.shift[i] = (int64_t)S.lo[i] - (int64_t)D.lo[i];
+    m.div[i] = make_fastdiv(S.ext[i]);
   }
   return m;
 }

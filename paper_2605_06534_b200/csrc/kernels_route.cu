@@ -141,6 +141,15 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(RouteSideArgs a) {
   }
 }
 
+// Block-cooperative copy of one route entry into shared memory (the caller
+// synchronises before use).
+__device__ __forceinline__ void load_entry(LocalEntry* dst, const LocalEntry* src) {
+  static_assert(sizeof(LocalEntry) % 4 == 0, "word copy");
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (uint32_t w = threadIdx.x; w < sizeof(LocalEntry) / 4; w += blockDim.x) d[w] = __ldg(s + w);
+}
+
 __device__ __forceinline__ int find_entry(const uint64_t* off, int n, uint64_t u) {
   int lo = 0, hi = n;  // off[lo] <= u < off[hi]
   while (hi - lo > 1) {
@@ -156,6 +165,8 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
   using T = typename Tr::T;
   __shared__ int s_entry;
   __shared__ uint64_t s_u0;
+  __shared__ LocalEntry s_E;  // the unit's entry (read per record: kept on chip)
+  int cur = -1;
   const uint64_t total = a.unit_off[a.nentries];
   T* serve = reinterpret_cast<T*>(a.serve);
   const T* val = reinterpret_cast<const T*>(a.rec_val);
@@ -167,9 +178,11 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
       s_u0 = a.unit_off[e];
     }
     __syncthreads();
-    const LocalEntry& E = a.entries[s_entry];
+    const int ei = s_entry;
     const uint64_t lu = u - s_u0;
+    if (ei != cur) load_entry(&s_E, a.entries + ei), cur = ei;
     __syncthreads();
+    const LocalEntry& E = s_E;
     const bool stream = !seg_dense(a, E.seg) && entry_stream(a, E);
     if (!seg_dense(a, E.seg) && !stream) {
       uint64_t k0, k1;
@@ -248,6 +261,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
   const RouteSideArgs& a = pa.r;
   __shared__ int s_entry;
   __shared__ uint64_t s_u0;
+  __shared__ LocalEntry s_E;  // the unit's entry (read per record: kept on chip)
+  int cur = -1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint64_t total = a.unit_off[a.nentries];
   const T* val = reinterpret_cast<const T*>(a.rec_val);
@@ -272,9 +287,10 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     }
     __syncthreads();
     const int ei = s_entry;  // s_entry is rewritten for the next unit after the barrier
-    const LocalEntry& E = a.entries[ei];
     const uint64_t lu = u - s_u0;
+    if (ei != cur) load_entry(&s_E, a.entries + ei), cur = ei;
     __syncthreads();
+    const LocalEntry& E = s_E;
     const int c = E.coord;
     // P2P: this entry's own region at every replica; NCCL: the coordinate's send region
     const EntryDest* ED = P.on ? P.edest + ei : nullptr;
