@@ -325,9 +325,11 @@ std::vector<int> segment_rounds(const Plan& plan, int g, int R, uint32_t tile) {
 }
 struct RecvLayout {
   std::vector<std::pair<int, int>> entries;  // (source rank, its remote-entry index)
-  std::vector<uint64_t> off, cap;            // records
+  std::vector<uint64_t> off, cap;            // bytes (p2p_region_bytes), records
+  std::vector<uint64_t> dst_base;            // the route's destination shard offset
   std::vector<int> round;
   uint64_t records = 0;
+  uint64_t bytes = 0;                        // receive area
   size_t head = 0;                           // mailbox + count slots, bytes
 };
 // Records one remote entry (route r of rank g) can carry in a sync whose
@@ -352,10 +354,12 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile, double t) 
       if (r.coord != k) continue;
       const uint64_t cap = entry_capacity(plan, g, r, t);
       L.entries.emplace_back(g, e);
-      L.off.push_back(L.records);
+      L.off.push_back(L.bytes);
       L.cap.push_back(cap);
+      L.dst_base.push_back(r.dst_offset);
       L.round.push_back(sr[r.seg]);
       L.records += cap;
+      L.bytes += p2p_region_bytes(plan.dtype(), cap);
     }
   }
   L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
@@ -609,7 +613,6 @@ ws_status ws_engine::init_p2p() {
 ws_status ws_engine::p2p_size(double t) {
   Comm* c = comm_;
   const int me = c->rank, W = c->world, R = c->R;
-  const size_t wb = wire_bytes(dtype_);
   const uint32_t tile = encode_tile_elems(dtype_);
   int ok = cudaDeviceSynchronize() == cudaSuccess;
   ws_status st = c->fab->all_min(&ok);  // every rank's syncs so far are done
@@ -621,7 +624,7 @@ ws_status ws_engine::p2p_size(double t) {
   c->sized_t = -1.0;
   std::vector<RecvLayout> lay(W);
   for (int q = 0; q < W; ++q) lay[q] = recv_layout(plan_, q, R, tile, t);
-  const size_t bytes = std::max<uint64_t>(1, lay[me].records) * wb;
+  const size_t bytes = std::max<uint64_t>(16, lay[me].bytes);
   ok = cudaMalloc(&c->d_rec, bytes) == cudaSuccess;
   cudaGetLastError();
   st = c->fab->all_min(&ok);
@@ -651,7 +654,7 @@ ws_status ws_engine::p2p_size(double t) {
       for (int j = 0; j < (int)Lq.entries.size(); ++j)
         if (Lq.entries[j].first == me && Lq.entries[j].second == e) pos = j;
       if (pos < 0) return set_error(WS_TRANSFER_ERROR, "p2p: entry missing from a receiver layout");
-      D.rec[r] = static_cast<char*>(c->peer_rec[q]) + Lq.off[pos] * wb;
+      D.rec[r] = static_cast<char*>(c->peer_rec[q]) + Lq.off[pos];
       D.cnt[r] = reinterpret_cast<uint32_t*>(static_cast<char*>(c->peer_head[q]) + kMailboxBytes) +
                  pos;
       ++r;
@@ -674,7 +677,8 @@ ws_status ws_engine::p2p_size(double t) {
     std::vector<RecvEntry> re;
     for (int j = 0; j < (int)L.entries.size(); ++j)
       if (L.round[j] == r)
-        re.push_back(RecvEntry{L.off[j], (uint32_t)j, (uint32_t)L.entries[j].first});
+        re.push_back(RecvEntry{L.off[j], L.cap[j], L.dst_base[j], (uint32_t)j,
+                               (uint32_t)L.entries[j].first});
     if (!re.empty())
       WS_CUDA_TRY(cudaMemcpy(c->rr[r].d_rentries, re.data(), re.size() * sizeof(RecvEntry),
                              cudaMemcpyHostToDevice), "H2D");
@@ -1167,7 +1171,7 @@ ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense
     *recv_records = pulled_bytes_;
     return WS_OK;
   }
-  const size_t wb = wire_bytes(dtype_), esz = dtype_size(dtype_);
+  const size_t wb = p2p_record_bytes(dtype_), esz = dtype_size(dtype_);
   const int ne = (int)c->mine.size();
   std::vector<uint32_t> cnt(std::max(1, ne));
   std::vector<uint64_t> nnz(std::max(1, nseg_)), cap(std::max(1, nseg_));
@@ -1191,7 +1195,8 @@ ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense
   if (!L.entries.empty())
     WS_CUDA_TRY(cudaMemcpy(rc.data(), static_cast<char*>(c->d_head) + kMailboxBytes,
                            L.entries.size() * 4, cudaMemcpyDeviceToHost), "D2H");
-  for (size_t j = 0; j < L.entries.size(); ++j) *recv_records += (uint64_t)rc[j] * wb;
+  for (size_t j = 0; j < L.entries.size(); ++j)
+    *recv_records += (uint64_t)(rc[j] & ~kCountSet) * wb;
   return WS_OK;
 }
 

@@ -254,8 +254,8 @@ __device__ __forceinline__ typename Traits<DT>::T* fuse_target(const FuseEntry* 
 #endif
 
 // Fused remote emission (bf16): the record (segment-local i, value v) of a
-// lane with `valid`, re-indexed into route M's destination shard, stored as a
-// wire record (serving index << 16 | value) into every replica's region.
+// lane with `valid`, re-indexed into route M's destination shard, stored
+// (shard-local index, value) into every replica's region.
 // Warp-collective: every lane calls it.
 __device__ __forceinline__ void emit_remote(const RemoteMap& M, bool valid, uint32_t i,
                                             uint16_t v) {
@@ -277,10 +277,12 @@ __device__ __forceinline__ void emit_remote(const RemoteMap& M, bool valid, uint
   base = __shfl_sync(kFullMask, base, 0);
   if (!valid) return;
   const uint64_t slot = (uint64_t)base + __popc(bal & ((1u << lane) - 1u));
-  if (slot >= M.cap) return;  // cannot happen: the capacity is the route's overlap
-  const uint64_t w = ((M.dst_base + d) << 16) | (uint64_t)v;
+  if (slot >= M.cap) return;  // cannot happen: a sparse segment fits its regions
 #pragma unroll 1
-  for (int r = 0; r < 8 && M.rec[r]; ++r) reinterpret_cast<uint64_t*>(M.rec[r])[slot] = w;
+  for (int r = 0; r < 8 && M.rec[r]; ++r) {  // SoA region: shard-local index | value
+    reinterpret_cast<uint32_t*>(M.rec[r])[slot] = (uint32_t)d;
+    reinterpret_cast<uint16_t*>(reinterpret_cast<uint32_t*>(M.rec[r]) + M.cap)[slot] = v;
+  }
 }
 
 // Ascending rank of in-tile element li among the super-tile's changes.

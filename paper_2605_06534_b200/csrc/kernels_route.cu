@@ -295,6 +295,30 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
     // P2P: this entry's own region at every replica; NCCL: the coordinate's send region
     const EntryDest* ED = P.on ? P.edest + ei : nullptr;
     const uint64_t roff = P.on ? 0 : pa.region_off[c], rcap = P.on ? ED->cap : pa.region_cap[c];
+    // stores one record at `slot` of the entry's region
+    auto put = [&](uint64_t slot, uint64_t idx, T v, bool set) {
+      if (slot >= rcap) {
+        atomicOr(pa.err, WS_ERRBIT_CAPACITY);
+        return;
+      }
+      if (P.on) {
+        // straight into every replica's receive region over NVLink: the
+        // shard-local index and the value (SoA, p2p_record_bytes)
+        const uint32_t li = (uint32_t)(idx - E.dst_base);
+        for (int r = 0; r < kMaxReplicas && ED->rec[r]; ++r) {
+          reinterpret_cast<uint32_t*>(ED->rec[r])[slot] = li;
+          reinterpret_cast<T*>(reinterpret_cast<uint32_t*>(ED->rec[r]) + rcap)[slot] = v;
+        }
+      } else if constexpr (DT == WS_BF16) {
+        const uint64_t w = (set ? kWireSet : 0ull) | (idx << 16) | (uint64_t)v;
+        reinterpret_cast<uint64_t*>(pa.send)[roff + slot] = w;
+      } else {
+        ulonglong2 w;
+        w.x = (set ? kWireSet : 0ull) | idx;
+        w.y = (unsigned long long)v;
+        reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
+      }
+    };
     // emits one record per lane with `valid`, reserving slots warp-wide
     auto emit = [&](bool valid, uint64_t idx, T v, bool set) {
       const unsigned bal = __ballot_sync(kFullMask, valid);
@@ -304,54 +328,54 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
         base = P.on ? atomicAdd(P.ent_cnt + ei, (unsigned)__popc(bal))
                     : atomicAdd(pa.region_cnt + c, (unsigned long long)__popc(bal));
       base = __shfl_sync(kFullMask, base, 0);
-      if (!valid) return;
-      const uint64_t slot = base + __popc(bal & ((1u << lane) - 1u));
-      if (slot >= rcap) {
-        atomicOr(pa.err, WS_ERRBIT_CAPACITY);
-        return;
-      }
-      if constexpr (DT == WS_BF16) {
-        const uint64_t w = (set ? kWireSet : 0ull) | (idx << 16) | (uint64_t)v;
-        if (!P.on) {
-          reinterpret_cast<uint64_t*>(pa.send)[roff + slot] = w;
-        } else {  // straight into every replica's receive buffer over NVLink
-          for (int r = 0; r < kMaxReplicas && ED->rec[r]; ++r)
-            reinterpret_cast<uint64_t*>(ED->rec[r])[slot] = w;
-        }
-      } else {
-        ulonglong2 w;
-        w.x = (set ? kWireSet : 0ull) | idx;
-        w.y = (unsigned long long)v;
-        if (!P.on) {
-          reinterpret_cast<ulonglong2*>(pa.send)[roff + slot] = w;
-        } else {
-          for (int r = 0; r < kMaxReplicas && ED->rec[r]; ++r)
-            reinterpret_cast<ulonglong2*>(ED->rec[r])[slot] = w;
-        }
-      }
+      if (valid) put(base + __popc(bal & ((1u << lane) - 1u)), idx, v, set);
     };
     if (!seg_dense(a, E.seg)) {
       uint64_t k0, k1;
       warp_tile_records(a, E, lu, warp, &k0, &k1);
       if (P.debug & 2) k1 = k0;
       const uint64_t rec = a.seg_rec[E.seg];
-      for (uint64_t kb = k0; kb < k1; kb += 32) {
-        const uint64_t k = kb + lane;
-        bool valid = k < k1;
-        uint64_t d = 0;
-        T v = 0;
-        if (valid) {
-          const uint32_t i = __ldg(a.rec_idx + rec + k);
-          if (E.identity) {
-            valid = i >= E.keep_lo && i < E.keep_hi;
-            d = (uint64_t)((int64_t)i + E.shift);
-          } else {
-            d = remap_index(E.map, i);
-            valid = d != ~0ull;
-          }
-          v = __ldg(val + rec + k);
+      // kPackBatch x 32 records per pass: their loads are all in flight
+      // before the first is used, and one atomic reserves all their slots
+      constexpr int kPackBatch = 4;
+      for (uint64_t kb = k0; kb < k1; kb += 32 * kPackBatch) {
+        uint32_t ix[kPackBatch];
+        T v[kPackBatch];
+#pragma unroll
+        for (int b = 0; b < kPackBatch; ++b) {
+          const uint64_t k = kb + b * 32 + lane;
+          ix[b] = k < k1 ? __ldg(a.rec_idx + rec + k) : 0u;
+          v[b] = k < k1 ? __ldg(val + rec + k) : T(0);
         }
-        emit(valid, E.dst_base + d, v, false);
+        uint64_t d[kPackBatch];
+        unsigned bal[kPackBatch];
+        uint32_t total = 0;
+#pragma unroll
+        for (int b = 0; b < kPackBatch; ++b) {
+          const uint64_t k = kb + b * 32 + lane;
+          bool valid = k < k1;
+          if (E.identity) {
+            valid = valid && ix[b] >= E.keep_lo && ix[b] < E.keep_hi;
+            d[b] = (uint64_t)((int64_t)ix[b] + E.shift);
+          } else {
+            d[b] = valid ? remap_index(E.map, ix[b]) : ~0ull;
+            valid = d[b] != ~0ull;
+          }
+          bal[b] = __ballot_sync(kFullMask, valid);
+          total += __popc(bal[b]);
+        }
+        if (!total) continue;
+        unsigned long long base = 0;
+        if (lane == 0)
+          base = P.on ? atomicAdd(P.ent_cnt + ei, total)
+                      : atomicAdd(pa.region_cnt + c, (unsigned long long)total);
+        base = __shfl_sync(kFullMask, base, 0);
+#pragma unroll
+        for (int b = 0; b < kPackBatch; ++b) {
+          if ((bal[b] >> lane) & 1u) put(base + __popc(bal[b] & ((1u << lane) - 1u)),
+                                         E.dst_base + d[b], v[b], false);
+          base += __popc(bal[b]);
+        }
       }
     } else {
       const BoxCopyArgs& B = E.box;
@@ -420,8 +444,12 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
       for (int e = threadIdx.x; e < a.nentries; e += blockDim.x) {
         const EntryDest& D = P.edest[e];
         const unsigned c0 = *reinterpret_cast<volatile unsigned*>(P.ent_cnt + e);
-        const uint32_t n = (P.dense_direct && seg_dense(a, a.entries[e].seg))
-                               ? 0u : (uint32_t)(c0 < D.cap ? c0 : D.cap);
+        const bool dense = seg_dense(a, a.entries[e].seg);
+        // a dense box that went direct sends no records; one that did not
+        // sent set records (count flagged)
+        const uint32_t n = (P.dense_direct && dense)
+                               ? 0u
+                               : ((uint32_t)(c0 < D.cap ? c0 : D.cap) | (dense ? kCountSet : 0u));
         for (int r = 0; r < kMaxReplicas && D.rec[r]; ++r) st_relaxed_sys_u32(D.cnt[r], n);
       }
       __threadfence_system();
@@ -518,8 +546,8 @@ __global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
   for (int base = 0; base < P.nrecv; base += 1024) {
     const int e = base + tid;
     const uint64_t u = e < P.nrecv
-        ? ((uint64_t)ld_acquire_sys_u32(P.recv_cnt + P.rentries[e].cnt_idx) + kApplyUnit - 1) /
-              kApplyUnit
+        ? ((uint64_t)(ld_acquire_sys_u32(P.recv_cnt + P.rentries[e].cnt_idx) & ~kCountSet) +
+           kApplyUnit - 1) / kApplyUnit
         : 0;
     uint64_t inc = u;
 #pragma unroll
@@ -554,41 +582,59 @@ __global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
 template <int DT>
 __global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
   const int W = P.world;
-  __shared__ int s_e;
-  __shared__ uint64_t s_k0, s_k1;
+  using Tr = Traits<DT>;
+  using T = typename Tr::T;
+  __shared__ const uint32_t* s_idx;
+  __shared__ const T* s_val;
+  __shared__ T* s_dst;
+  __shared__ uint32_t s_k0, s_k1, s_set;
   const uint64_t total = (P.debug & 1) ? 0 : P.recv_units[P.nrecv];
   for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
     if (threadIdx.x == 0) {
       const int e = find_entry(P.recv_units, P.nrecv, u);
       const RecvEntry R = P.rentries[e];
-      const uint64_t n = P.recv_cnt[R.cnt_idx];
+      const uint32_t c = P.recv_cnt[R.cnt_idx];
+      const uint64_t n = c & ~kCountSet;
       const uint64_t lo = (u - P.recv_units[e]) * kApplyUnit;
-      s_e = e;
-      s_k0 = R.off + lo;
-      s_k1 = R.off + (n < lo + kApplyUnit ? n : lo + kApplyUnit);
+      const uint32_t* region =
+          reinterpret_cast<const uint32_t*>(static_cast<const char*>(P.recv) + R.off);
+      s_idx = region;
+      s_val = reinterpret_cast<const T*>(region + R.cap);
+      s_dst = serve + R.dst_base;
+      s_set = (c & kCountSet) ? 1u : 0u;
+      s_k0 = (uint32_t)lo;
+      s_k1 = (uint32_t)(n < lo + kApplyUnit ? n : lo + kApplyUnit);
     }
     __syncthreads();
-    const uint64_t k0 = s_k0, k1 = s_k1;
+    const uint32_t* idx = s_idx;
+    const T* val = s_val;
+    T* dst = s_dst;
+    const uint32_t k0 = s_k0, k1 = s_k1;
+    const bool set = s_set != 0;
     __syncthreads();
-    // block-local strided apply of [k0, k1)
-    using Tr = Traits<DT>;
-    using T = typename Tr::T;
-    for (uint64_t kb = k0 + threadIdx.x; kb < k1; kb += (uint64_t)blockDim.x * kApplyBatch) {
-      uint64_t ix[kApplyBatch];
+    // block-local strided apply of [k0, k1): every serving-word load of a
+    // batch is issued before any store
+    for (uint32_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x * kApplyBatch) {
+      uint32_t ix[kApplyBatch];
       T v[kApplyBatch], o[kApplyBatch];
-      bool ok[kApplyBatch], st[kApplyBatch];
+      bool ok[kApplyBatch];
 #pragma unroll
       for (int j = 0; j < kApplyBatch; ++j) {
-        const uint64_t k = kb + (uint64_t)j * blockDim.x;
+        const uint32_t k = kb + j * blockDim.x;
         ok[j] = k < k1;
-        if (ok[j]) decode_wire<DT>(P.recv, k, &ix[j], &v[j], &st[j]);
+        if (ok[j]) {
+          ix[j] = __ldg(idx + k);
+          v[j] = __ldg(val + k);
+        }
+      }
+      if (!set) {
+#pragma unroll
+        for (int j = 0; j < kApplyBatch; ++j)
+          if (ok[j]) o[j] = dst[ix[j]];
       }
 #pragma unroll
       for (int j = 0; j < kApplyBatch; ++j)
-        if (ok[j] && !st[j]) o[j] = serve[ix[j]];
-#pragma unroll
-      for (int j = 0; j < kApplyBatch; ++j)
-        if (ok[j]) serve[ix[j]] = st[j] ? v[j] : Tr::add(o[j], v[j]);
+        if (ok[j]) dst[ix[j]] = set ? v[j] : Tr::add(o[j], v[j]);
     }
   }
   __syncthreads();

@@ -79,13 +79,26 @@ struct RouteSideArgs {
 // Work list + fused reslice/apply/dense-copy for the local routes.
 cudaError_t launch_local_route(int dtype, const RouteSideArgs& a, int grid, cudaStream_t s);
 
-// Wire records for the NVLink exchange: self-describing (serving-arena
+// Wire records of the NCCL-fallback exchange: self-describing (serving-arena
 // index, value), so a receiver needs no route table and arrival order does
 // not matter.  bf16: one u64 = set:1 | index:47 | value:16.  4-byte dtypes:
 // {u64 set:1 | index:63, u32 value, u32 pad}.  "set" records carry dense-
 // fallback values (overwrite, copy_overlap semantics); the others are deltas.
 constexpr uint64_t kWireSet = 1ull << 63;
 inline size_t wire_bytes(int dtype) { return dtype == WS_BF16 ? 8 : 16; }
+
+// Records of the peer-memory exchange: every receive region belongs to one
+// (source, route), so a record carries only its index local to the
+// destination shard (u32: a shard has < 2^32 elements) and its value, as two
+// arrays -- u32 idx[cap] | value[cap] -- 6 bytes per bf16 record, the
+// algorithmic 4 + 2 of SURVEY §8(d).  The receiver adds the route's shard
+// offset.  A region whose source segment went dense without direct box
+// stores carries "set" records: its published count has bit 31 set.
+inline size_t p2p_record_bytes(int dtype) { return 4 + (dtype == WS_BF16 ? 2 : 4); }
+inline uint64_t p2p_region_bytes(int dtype, uint64_t cap) {
+  return (cap * p2p_record_bytes(dtype) + 15) / 16 * 16;  // next region 16-byte aligned
+}
+constexpr uint32_t kCountSet = 0x80000000u;
 
 // Packs the records of the routes to other GPUs into one region per serving
 // coordinate (warp-aggregated atomic reservation; order inside a region is
@@ -150,12 +163,14 @@ struct P2PArgs {
 struct EntryDest {
   void* rec[kMaxReplicas];      // record region at replica r (null-terminated)
   uint32_t* cnt[kMaxReplicas];  // its count slot at replica r
-  uint64_t cap;                 // region capacity, records (the route's overlap)
+  uint64_t cap;                 // region capacity, records
 };
-// A region of this rank's receive area: records [off, off + count) where
-// count is the source's published count for it.
+// A region of this rank's receive area: `count` records (the source's
+// published count) in the SoA layout of p2p_record_bytes at byte `off`.
 struct RecvEntry {
-  uint64_t off;                 // records from the start of the record area
+  uint64_t off;                 // bytes from the start of the receive area
+  uint64_t cap;                 // region capacity, records (the value array follows idx[cap])
+  uint64_t dst_base;            // the destination shard's offset in the serving arena
   uint32_t cnt_idx;
   uint32_t src;
 };
