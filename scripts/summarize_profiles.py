@@ -11,6 +11,7 @@ launch, read by bench.py's roofline `traffic`).
 """
 import argparse
 import csv
+import re
 import json
 import os
 import shutil
@@ -70,15 +71,22 @@ def main():
         rows = list(csv.reader(lines))
         hdr = rows[0]
         ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+        # the sync's kernels (libwsync's), not the setup's (torch arena
+        # initialisation, the generator) or the verification's
+        setup = ("gen_kernel", "vectorized_elementwise_kernel", "elementwise_kernel",
+                 "reduce_kernel", "nccl")
         tot = {}
         for r in rows[1:]:
-            name = r[ik].split("<")[0].split("::")[-1].split("(")[0]
+            m = re.search(r"(\w+_kernel)", r[ik])
+            name = m.group(1) if m else r[ik][:40]
+            if any(x in r[ik] for x in setup):
+                continue
             tot[name] = tot.get(name, 0) + float(r[iv].replace(",", ""))
         s = sum(tot.values())
         with open(os.path.join(prof, f"{tag}_launch_shares.txt"), "w") as f:
-            f.write("kernel, total ns over the captured launches, share\n")
+            f.write("kernel (libwsync sync kernels of the captured launches), total ns, share\n")
             for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-                f.write(f"{k}, {v:.0f}, {v / s:.3f}\n")
+                f.write(f"{k}, {v:.0f}, {v / s:.4f}\n")
     if os.path.exists(args.rep):
         ms = raw_metrics(args.rep)
         with open(os.path.join(prof, f"{tag}_encode_ncu.txt"), "w") as f:
