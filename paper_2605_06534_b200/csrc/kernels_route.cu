@@ -18,6 +18,7 @@ namespace wsync {
 namespace {
 
 constexpr int kWlThreads = 1024;
+constexpr int kCopyIlp = 4;  // dense box copies: 16-byte vectors per thread in flight
 
 __device__ __forceinline__ bool seg_dense(const RouteSideArgs& a, int seg) {
   return !a.sparse || a.seg_nnz[seg] > a.seg_cap[seg];
@@ -246,7 +247,20 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
         constexpr int VE = Tr::kVE;
         const uint4* s4 = reinterpret_cast<const uint4*>(src + c0);
         uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
-        for (uint64_t j = threadIdx.x; j < (c1 - c0) / VE; j += blockDim.x) d4[j] = ld_stream(s4 + j);
+        const uint64_t nv = (c1 - c0) / VE;
+        for (uint64_t j0 = threadIdx.x; j0 < nv; j0 += (uint64_t)blockDim.x * kCopyIlp) {
+          uint4 v[kCopyIlp];
+#pragma unroll
+          for (int q = 0; q < kCopyIlp; ++q) {
+            const uint64_t j = j0 + (uint64_t)q * blockDim.x;
+            if (j < nv) v[q] = ld_stream(s4 + j);
+          }
+#pragma unroll
+          for (int q = 0; q < kCopyIlp; ++q) {
+            const uint64_t j = j0 + (uint64_t)q * blockDim.x;
+            if (j < nv) d4[j] = v[q];
+          }
+        }
       } else {
         for (uint64_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) dst[j] = src[j];
       }
@@ -411,10 +425,23 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
           for (int r = 0; r < nrep; ++r)
             reinterpret_cast<T*>(P.serve_dst[c][r])[dofs + c0 + j] = s0[j];
         const uint4* sv = reinterpret_cast<const uint4*>(s0 + head);
-        for (uint64_t j = threadIdx.x; j < body; j += blockDim.x) {
-          const uint4 v = ld_stream(sv + j);
-          for (int r = 0; r < nrep; ++r)
-            reinterpret_cast<uint4*>(reinterpret_cast<T*>(P.serve_dst[c][r]) + dofs + c0 + head)[j] = v;
+        // kCopyIlp vectors per thread in flight before they are stored
+        for (uint64_t j0 = threadIdx.x; j0 < body; j0 += (uint64_t)blockDim.x * kCopyIlp) {
+          uint4 v[kCopyIlp];
+#pragma unroll
+          for (int q = 0; q < kCopyIlp; ++q) {
+            const uint64_t j = j0 + (uint64_t)q * blockDim.x;
+            if (j < body) v[q] = ld_stream(sv + j);
+          }
+          for (int r = 0; r < nrep; ++r) {
+            uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<T*>(P.serve_dst[c][r]) + dofs + c0 +
+                                                head);
+#pragma unroll
+            for (int q = 0; q < kCopyIlp; ++q) {
+              const uint64_t j = j0 + (uint64_t)q * blockDim.x;
+              if (j < body) d[j] = v[q];
+            }
+          }
         }
         for (uint64_t j = head + body * V + threadIdx.x; j < n; j += blockDim.x)
           for (int r = 0; r < nrep; ++r)
