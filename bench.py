@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1,
                     help="Qwen layers per CPU thread in the reference sample")
+    ap.add_argument("--placement", default="overlap", choices=["rank", "overlap"],
+                    help="which serving rank each GPU hosts (ws_placement): 'overlap' keeps "
+                         "the most trainer->serving elements on their own GPU")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
                     help="BASELINE.json config: 2 Qwen3-8B FSDP-N -> TP2 x N/2 at 1%% (default), "
                          "3 Qwen3-32B TP-N -> TP-N/2 x 2 at 0.5%%, 4 Qwen3-30B-A3B expert-sharded "
@@ -293,7 +296,8 @@ def run_ours(args):
     manifest = ws.MODELS[args.model]()
     (scheme, _), tp, replicas, layout_desc = layouts(n, args.config)
     train = ws.TrainConfig("fsdp") if scheme == "fsdp" else ws.TrainConfig("tp", n, 1, 1)
-    plan = ws.Plan(manifest, ws.BF16, train, ws.ServeConfig(tp, 1, replicas), world=n, rank=rank)
+    plan = ws.Plan(manifest, ws.BF16, train, ws.ServeConfig(tp, 1, replicas, args.placement),
+                   world=n, rank=rank)
     eng = ws.TransferEngine(plan, device=local, unique_id=uid)
     zipf = CONFIGS[args.config].get("zipf")
     eng.generate(seed=args.seed, density=args.density, expert_zipf=zipf, perm_seed=11)
@@ -368,16 +372,18 @@ def run_ours(args):
     # ---- route stage on NVLink (N > 1) ----
     route = None
     if n > 1:
-        sent = xbytes["sent_records"] + xbytes["sent_dense"]
-        # 6 B per record (u32 index + u16 value) per remote replica
-        remote_recs = xbytes["sent_records"] // 8
+        sent = xbytes["sent_record_bytes"] + xbytes["sent_dense_bytes"]
+        # 6 B per record (u32 index + u16 value) per remote
+        # replica -- also the wire format (SoA u32 shard-local index + u16)
+        wire_b = 6
+        remote_recs = xbytes["sent_record_bytes"] // wire_b
         pack_s = tim["pack_s"] / tim["pack_steps"] if tim.get("pack_steps") else None
         # the NVLink kernel's window: the pack (single-round exchange), else
         # the whole route stage (pack + receiver scatter)
         win = pack_s or route_s
-        route = {"bytes_per_sync": sent, "wire_bytes_per_record": 8,
-                 "alg_bytes_per_sync": 6 * remote_recs + xbytes["sent_dense"],
-                 "recv_bytes_per_sync": xbytes["recv_records"],
+        route = {"bytes_per_sync": sent, "wire_bytes_per_record": wire_b,
+                 "alg_bytes_per_sync": 6 * remote_recs + xbytes["sent_dense_bytes"],
+                 "recv_bytes_per_sync": xbytes["recv_record_bytes"],
                  "stage_ms": round(route_s * 1e3, 4),
                  "pack_ms": round(pack_s * 1e3, 4) if pack_s else None,
                  "window": "pack_kernel (NVLink stores)" if pack_s else "route stage",
@@ -440,6 +446,7 @@ def run_ours(args):
                        "config": args.config, "model": args.model, "density": args.density,
                        "density_threshold": args.threshold,
                        "train": f"{scheme}{n}", "serve": f"tp{tp}x{replicas}",
+                       "placement": args.placement,
                        "model_elems": model_elems,
                        "l2": "inputs larger than L2 (prev+next %.1f GB per GPU per step)"
                              % (4 * train_elems / 1e9)},

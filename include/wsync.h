@@ -268,12 +268,24 @@ typedef struct ws_train_layout {
   int32_t tp, pp, dp;
 } ws_train_layout;
 
+/* Which serving rank each GPU of the world hosts (trainer rank g and one
+ * serving rank share GPU g). */
+typedef enum ws_placement {
+  WS_PLACE_RANK = 0,    /* serving rank g on GPU g (the reference's numbering) */
+  WS_PLACE_OVERLAP = 1  /* serving ranks assigned to GPUs so that the elements each
+                           GPU's trainer shards route to its own serving shards are
+                           maximal in sum: fewest bytes over NVLink (FSDP-N -> TP2 x
+                           N/2 puts coordinate 0 on GPUs 0..N/2-1) */
+} ws_placement;
+
 /* ServeConfig{tp,pp} (plan.hpp:17-21) times `replicas` identical copies.
  * Serving rank of (replica r, stage s, tp rank k) is r*tp*pp + s*tp + k.
  * WS_EXPERT parameters are split along dim 0 over the tp ranks (EP = TP
- * for experts, e.g. tp 8 gives EP8). */
+ * for experts, e.g. tp 8 gives EP8).  `placement` (ws_placement; 0 when
+ * zero-initialised) maps serving ranks to GPUs. */
 typedef struct ws_serve_layout {
   int32_t tp, pp, replicas;
+  int32_t placement;
 } ws_serve_layout;
 
 typedef struct ws_plan ws_plan;
@@ -305,6 +317,9 @@ typedef struct ws_plan_info {
   uint64_t serve_arena_elems;
   uint64_t train_elems;       /* sum of segment sizes (dense-equivalent) */
   uint64_t model_elems;       /* whole model */
+  int32_t serve_rank;         /* serving rank hosted on this GPU (replica * tp * pp +
+                                 serve_coord; -1 when serve_coord is -1) */
+  int32_t serve_replica;      /* its replica index, or -1 */
 } ws_plan_info;
 ws_status ws_plan_get_info(const ws_plan* plan, ws_plan_info* info);
 
@@ -514,8 +529,8 @@ ws_status ws_engine_timing(ws_engine* eng, int reset, ws_timing* out);
  * boxes stored straight into their serving arenas, and the records other
  * ranks published into this rank's regions.  NCCL-fallback exchange: bytes
  * sent / received.  Zero at world 1.  Synchronises. */
-ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records, uint64_t* sent_dense,
-                                   uint64_t* recv_records);
+ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_record_bytes,
+                                   uint64_t* sent_dense_bytes, uint64_t* recv_record_bytes);
 
 /* Every segment's change count and codec ('S' sparse, 'D' dense) from the
  * last sync (num_segments entries each; either may be NULL).  Synchronises. */

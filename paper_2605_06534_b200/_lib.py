@@ -96,14 +96,16 @@ class TrainLayout(C.Structure):  # ws_train_layout
 
 
 class ServeLayout(C.Structure):  # ws_serve_layout
-    _fields_ = [("tp", C.c_int32), ("pp", C.c_int32), ("replicas", C.c_int32)]
+    _fields_ = [("tp", C.c_int32), ("pp", C.c_int32), ("replicas", C.c_int32),
+                ("placement", C.c_int32)]
 
 
 class PlanInfo(C.Structure):  # ws_plan_info
     _fields_ = [("num_segments", C.c_int32), ("num_serve_shards", C.c_int32),
                 ("num_routes", C.c_int32), ("serve_coord", C.c_int32),
                 ("train_arena_elems", C.c_uint64), ("serve_arena_elems", C.c_uint64),
-                ("train_elems", C.c_uint64), ("model_elems", C.c_uint64)]
+                ("train_elems", C.c_uint64), ("model_elems", C.c_uint64),
+                ("serve_rank", C.c_int32), ("serve_replica", C.c_int32)]
 
 
 class SyncOptions(C.Structure):  # ws_sync_options

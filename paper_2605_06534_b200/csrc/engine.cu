@@ -97,6 +97,8 @@ ws_status ws_plan_get_info(const ws_plan* plan, ws_plan_info* info) {
   info->serve_arena_elems = p.serve_arena_elems();
   info->train_elems = p.train_elems();
   info->model_elems = p.model_elems();
+  info->serve_rank = p.serve_rank_of(p.rank());
+  info->serve_replica = info->serve_rank < 0 ? -1 : info->serve_rank / p.coords();
   return WS_OK;
 }
 

@@ -77,7 +77,8 @@ struct ws_engine {
   ws_status exchange_apply(int round, cudaStream_t s, uint32_t* launches);
   ws_status exchange_end(cudaStream_t s);
   ws_status exchange_mark_pack(cudaStream_t s);
-  ws_status exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense, uint64_t* recv_records);
+  ws_status exchange_bytes(uint64_t* sent_record_bytes, uint64_t* sent_dense_bytes,
+                           uint64_t* recv_record_bytes);
   bool exchange_needs_resize(const ws_sync_options& o) const;
   // grows the P2P receive regions for o.density_threshold (collective)
   ws_status exchange_prepare(const ws_sync_options& o);

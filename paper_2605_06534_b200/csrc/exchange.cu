@@ -1159,16 +1159,16 @@ static ws_status check_exchange(const Plan& plan, int rounds, double t) {
 // records stored into the replicas' receive regions (one copy per replica),
 // dense boxes stored straight into their serving arenas, and the records
 // the sources published into this rank's regions.  Synchronises.
-ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense,
-                                    uint64_t* recv_records) {
-  *sent_records = *sent_dense = *recv_records = 0;
+ws_status ws_engine::exchange_bytes(uint64_t* sent_record_bytes, uint64_t* sent_dense_bytes,
+                                    uint64_t* recv_record_bytes) {
+  *sent_record_bytes = *sent_dense_bytes = *recv_record_bytes = 0;
   Comm* c = comm_;
   if (!c) return WS_OK;
   WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
   WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
   if (!c->p2p) {
-    *sent_records = pushed_wire_bytes_;
-    *recv_records = pulled_bytes_;
+    *sent_record_bytes = pushed_wire_bytes_;
+    *recv_record_bytes = pulled_bytes_;
     return WS_OK;
   }
   const size_t wb = p2p_record_bytes(dtype_), esz = dtype_size(dtype_);
@@ -1186,9 +1186,9 @@ ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense
     while (nrep < kMaxReplicas && c->edest[e].rec[nrep]) ++nrep;
     const bool dense = !last_sparse_ || nnz[rt.seg] > cap[rt.seg];
     if (dense && c->pargs.dense_direct)
-      *sent_dense += rt.overlap * esz * nrep;
+      *sent_dense_bytes += rt.overlap * esz * nrep;
     else
-      *sent_records += (uint64_t)std::min<uint64_t>(cnt[e], c->edest[e].cap) * wb * nrep;
+      *sent_record_bytes += (uint64_t)std::min<uint64_t>(cnt[e], c->edest[e].cap) * wb * nrep;
   }
   const RecvLayout L = recv_layout(plan_, c->rank, c->R, encode_tile_elems(dtype_), c->sized_t);
   std::vector<uint32_t> rc(std::max<size_t>(1, L.entries.size()));
@@ -1196,16 +1196,16 @@ ws_status ws_engine::exchange_bytes(uint64_t* sent_records, uint64_t* sent_dense
     WS_CUDA_TRY(cudaMemcpy(rc.data(), static_cast<char*>(c->d_head) + kMailboxBytes,
                            L.entries.size() * 4, cudaMemcpyDeviceToHost), "D2H");
   for (size_t j = 0; j < L.entries.size(); ++j)
-    *recv_records += (uint64_t)(rc[j] & ~kCountSet) * wb;
+    *recv_record_bytes += (uint64_t)(rc[j] & ~kCountSet) * wb;
   return WS_OK;
 }
 
-extern "C" ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_records,
-                                              uint64_t* sent_dense, uint64_t* recv_records) {
+extern "C" ws_status ws_engine_exchange_bytes(ws_engine* eng, uint64_t* sent_record_bytes,
+                                              uint64_t* sent_dense_bytes, uint64_t* recv_record_bytes) {
   DeviceGuard device_guard;
-  if (!eng || !sent_records || !sent_dense || !recv_records)
+  if (!eng || !sent_record_bytes || !sent_dense_bytes || !recv_record_bytes)
     return set_error(WS_INVALID_ARGUMENT, "ws_engine_exchange_bytes: null argument");
-  return eng->exchange_bytes(sent_records, sent_dense, recv_records);
+  return eng->exchange_bytes(sent_record_bytes, sent_dense_bytes, recv_record_bytes);
 }
 
 extern "C" ws_status ws_nccl_unique_id(uint8_t out[128]) {

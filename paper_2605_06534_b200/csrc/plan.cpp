@@ -9,6 +9,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <limits>
 #include <map>
 
 namespace wsync {
@@ -125,6 +126,8 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
                                              std::to_string(world)};
   if (serve.tp <= 0 || serve.pp <= 0 || serve.replicas <= 0)
     throw PlanError{WS_INVALID_ARGUMENT, "serve tp, pp and replicas must be positive"};
+  if (serve.placement != WS_PLACE_RANK && serve.placement != WS_PLACE_OVERLAP)
+    throw PlanError{WS_INVALID_ARGUMENT, "unknown serve placement"};
   const int train_ranks =
       train.scheme == WS_TRAIN_TP ? train.tp * train.pp * train.dp : world;
   // world 1 with a multi-rank layout: one GPU hosts every rank
@@ -254,6 +257,7 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
       }
     }
   }
+  place();
   for (int c = 0; c < C; ++c)
     for (const auto& ss : serve_by_coord_[c]) {
       const uint64_t got = covered[{c, ss.shard.param}];
@@ -266,8 +270,66 @@ Plan::Plan(std::vector<ParamMeta> manifest, int dtype, const ws_train_layout& tr
 }
 
 int Plan::coord_of_rank(int r) const {
-  if (r < 0 || r >= world_) return -1;
-  return r % coords();
+  if (collapsed_ || r < 0 || r >= world_) return -1;
+  return serve_rank_[r] % coords();
+}
+
+std::vector<int> assign_min_cost(const std::vector<int64_t>& cost, int n) {
+  // rows are added one at a time; each grows a shortest-path tree over the
+  // columns (reduced costs stay >= 0 thanks to the potentials u, v)
+  const int64_t INF = std::numeric_limits<int64_t>::max() / 4;
+  std::vector<int64_t> u(n + 1, 0), v(n + 1, 0);
+  std::vector<int> row_of(n + 1, 0), way(n + 1, 0);  // column j (1-based) -> row (1-based)
+  for (int i = 1; i <= n; ++i) {
+    row_of[0] = i;
+    int j0 = 0;
+    std::vector<int64_t> minv(n + 1, INF);
+    std::vector<char> used(n + 1, 0);
+    do {
+      used[j0] = 1;
+      const int i0 = row_of[j0];
+      int64_t delta = INF;
+      int j1 = 0;
+      for (int j = 1; j <= n; ++j) {
+        if (used[j]) continue;
+        const int64_t cur = cost[(size_t)(i0 - 1) * n + (j - 1)] - u[i0] - v[j];
+        if (cur < minv[j]) minv[j] = cur, way[j] = j0;
+        if (minv[j] < delta) delta = minv[j], j1 = j;
+      }
+      for (int j = 0; j <= n; ++j) {
+        if (used[j]) u[row_of[j]] += delta, v[j] -= delta;
+        else minv[j] -= delta;
+      }
+      j0 = j1;
+    } while (row_of[j0] != 0);
+    do {  // flip the augmenting path
+      const int j1 = way[j0];
+      row_of[j0] = row_of[j1];
+      j0 = j1;
+    } while (j0);
+  }
+  std::vector<int> col(n, -1);
+  for (int j = 1; j <= n; ++j) col[row_of[j] - 1] = j - 1;
+  return col;
+}
+
+// Serving rank of every GPU.  WS_PLACE_OVERLAP: GPU g hosting serving rank j
+// (coordinate j % C) keeps local the elements its trainer shards route to
+// that coordinate; the assignment maximises their sum (ties: rank order).
+void Plan::place() {
+  const int W = world_, C = coords();
+  serve_rank_.resize(W);
+  for (int g = 0; g < W; ++g) serve_rank_[g] = g;
+  if (collapsed_ || serve_.placement == WS_PLACE_RANK) return;
+  std::vector<uint64_t> w((size_t)W * C, 0);  // elements GPU g's shards route to coord c
+  for (int g = 0; g < W; ++g)
+    for (const Route& r : routes_[g]) w[(size_t)g * C + r.coord] += r.overlap;
+  const int64_t tie = W + 1;  // any weight difference outranks every tie-break
+  std::vector<int64_t> cost((size_t)W * W);
+  for (int g = 0; g < W; ++g)
+    for (int j = 0; j < W; ++j)
+      cost[(size_t)g * W + j] = -(int64_t)w[(size_t)g * C + j % C] * tie + (j != g ? 1 : 0);
+  serve_rank_ = assign_min_cost(cost, W);
 }
 
 uint64_t Plan::serve_arena_elems() const {

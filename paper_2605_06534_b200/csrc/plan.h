@@ -76,7 +76,8 @@ class Plan {
   int coords() const { return serve_.tp * serve_.pp; }
   int replicas() const { return serve_.replicas; }
   int coord_of_rank(int r) const;            // -1 when rank r holds no serving shard
-  int rank_of(int replica, int coord) const { return replica * coords() + coord; }
+  // serving rank (replica * coords + coord) hosted on GPU r (ws_placement)
+  int serve_rank_of(int r) const { return collapsed_ || r < 0 || r >= world_ ? -1 : serve_rank_[r]; }
   // One GPU hosts every rank of a multi-rank layout (world 1 with trainer
   // ranks or serving coordinates > 1): all logical trainer ranks' shards are
   // its segments, all coordinates' serving shards its serving arena, and
@@ -119,7 +120,14 @@ class Plan {
   std::vector<std::vector<ServeShard>> serve_by_coord_;
   std::vector<uint64_t> serve_arena_by_coord_;
   std::vector<std::vector<Route>> routes_;            // per source rank
+  std::vector<int> serve_rank_;                       // per GPU: hosted serving rank
+
+  void place();
 };
+
+// Minimum-cost perfect assignment of n rows to n columns (cost row-major,
+// n x n): col[row].  O(n^3) shortest augmenting paths with potentials.
+std::vector<int> assign_min_cost(const std::vector<int64_t>& cost, int n);
 
 constexpr uint64_t kArenaAlign = 64;  // elements; keeps 16-B vectors aligned for every dtype
 

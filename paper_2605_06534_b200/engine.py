@@ -38,13 +38,19 @@ class TrainConfig:
 
 @dataclass
 class ServeConfig:
-    """ServeConfig{tp,pp} (plan.hpp:17-21) x ``replicas``."""
+    """ServeConfig{tp,pp} (plan.hpp:17-21) x ``replicas``; ``placement``
+    "rank" hosts serving rank g on GPU g, "overlap" assigns serving ranks to
+    GPUs for the fewest NVLink bytes (ws_placement)."""
     tp: int = 1
     pp: int = 1
     replicas: int = 1
+    placement: str = "rank"
 
     def c(self):
-        return _lib.ServeLayout(self.tp, self.pp, self.replicas)
+        codes = {"rank": 0, "overlap": 1}
+        if self.placement not in codes:
+            raise ValueError(f"unknown placement {self.placement!r}")
+        return _lib.ServeLayout(self.tp, self.pp, self.replicas, codes[self.placement])
 
 
 class Plan:
@@ -205,12 +211,14 @@ class TransferEngine:
         return t.as_dict()
 
     def exchange_bytes(self):
-        """NVLink bytes of the last sync on this rank: (records sent, dense
-        boxes sent, records received) -- ws_engine_exchange_bytes."""
+        """NVLink bytes of the last sync on this rank: wire records sent (one
+        copy per replica), dense boxes sent, wire records received --
+        ws_engine_exchange_bytes."""
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
         with torch.cuda.device(self.device):
             check(lib.ws_engine_exchange_bytes(self.h, C.byref(a), C.byref(b), C.byref(c)))
-        return {"sent_records": a.value, "sent_dense": b.value, "recv_records": c.value}
+        return {"sent_record_bytes": a.value, "sent_dense_bytes": b.value,
+                "recv_record_bytes": c.value}
 
     def segment_payload(self, i, force_wide_index=False):
         """Segment i's payload from the last sync in the reference wire format

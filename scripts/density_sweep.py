@@ -57,6 +57,7 @@ def main():
     ap.add_argument("--model", default="qwen3-8b")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--densities", default=None, help="comma-separated subset")
+    ap.add_argument("--placement", default="overlap", choices=["rank", "overlap"])
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -70,7 +71,7 @@ def main():
         uid = obj[0]
     tp = 1 if world == 1 else 2
     plan = ws.Plan(ws.MODELS[args.model](), ws.BF16, ws.TrainConfig("fsdp"),
-                   ws.ServeConfig(tp, 1, world // tp), world=world, rank=rank)
+                   ws.ServeConfig(tp, 1, world // tp, args.placement), world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=local, unique_id=uid)
     dense_eq = 2 * plan.info.model_elems
     for d in ([float(x) for x in args.densities.split(',')] if args.densities else DENSITIES):
@@ -83,6 +84,7 @@ def main():
         if rank == 0:
             print(json.dumps({
                 "config": 5, "model": args.model, "n_gpus": world, "density": d,
+                "placement": args.placement,
                 "sparse_ms": round(ms_sparse, 3), "dense_ms": round(ms_dense, 3),
                 "sparse_gbs": round(dense_eq / ms_sparse / 1e6, 1),
                 "dense_gbs": round(dense_eq / ms_dense / 1e6, 1),

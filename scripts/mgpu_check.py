@@ -34,6 +34,15 @@ import torch.distributed as dist  # noqa: E402
 import paper_2605_06534_b200 as ws  # noqa: E402
 
 
+
+# serving-rank placement of every layout (ws_placement); WSYNC_CHECK_PLACEMENT=rank
+# checks the reference's rank order instead
+PLACEMENT = os.environ.get("WSYNC_CHECK_PLACEMENT", "overlap")
+
+
+def serve_cfg(tp, pp, replicas):
+    return ws.ServeConfig(tp, pp, replicas, PLACEMENT)
+
 def serve_equals_gen(eng, plan, seed, density, which, tabs=None):
     bad = []
     for i, (p, desc, off, n) in enumerate(plan.serve_shards):
@@ -93,7 +102,7 @@ def relay_case(rank, world, uid_fn, manifest, density, seed, mode):
     each rank pushes its trainer shards and pulls every shard routed to its
     serving coordinate (engine.cpp:109-238, one puller per serving rank)."""
     tp = 1 if world == 1 else 2
-    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), serve_cfg(tp, 1, world // tp),
                    world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
     eng.generate(seed=seed, density=density)
@@ -115,7 +124,7 @@ def relay_case(rank, world, uid_fn, manifest, density, seed, mode):
 
 def bf16_case(rank, world, uid_fn, manifest, density, seed):
     tp = 1 if world == 1 else 2
-    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), serve_cfg(tp, 1, world // tp),
                    world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
     eng.generate(seed=seed, density=density)
@@ -152,7 +161,7 @@ def ref_case(rank, world, uid_fn, dtype, density, sparse):
     st = ref.toy_state(3, 64, 128, dtype, (world, 1, 1), (world, 1), density, 7)
     st.run(mode_async=True, shard_aware=True, sparse=sparse, threshold=0.20, bucket_bytes=8192)
     manifest = [ws.ParamMeta(n, k, tuple(s), l) for (n, k, s, l) in st.params]
-    plan = ws.Plan(manifest, dtype, ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1),
+    plan = ws.Plan(manifest, dtype, ws.TrainConfig("tp", world, 1, 1), serve_cfg(world, 1, 1),
                    world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid_fn())
     td = {ws.I32: torch.int32, ws.F32: torch.float32}[dtype]
@@ -199,7 +208,7 @@ def main():
     # through several steps: an even count must leave serving == prev
     manifest = ws.MODELS["qwen2.5-0.5b"]([0, 23])
     tp = 1 if world == 1 else 2
-    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp),
+    plan = ws.Plan(manifest, ws.BF16, ws.TrainConfig("fsdp"), serve_cfg(tp, 1, world // tp),
                    world=world, rank=rank)
     eng = ws.TransferEngine(plan, device=rank % torch.cuda.device_count(), unique_id=uid())
     eng.generate(seed=8, density=0.02)
@@ -229,10 +238,10 @@ def main():
     half = max(1, world // 2)
     for name, manifest, train, serve, density, zipf in (
             ("config3 qwen3-32b[0,63]", ws.MODELS["qwen3-32b"]([0, 63]),
-             ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(half, 1, world // half), 0.005,
+             ws.TrainConfig("tp", world, 1, 1), serve_cfg(half, 1, world // half), 0.005,
              None),
             ("config4 qwen3-30b-a3b[0,47]", ws.MODELS["qwen3-30b-a3b"]([0, 47]),
-             ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1), 0.01, 1.1)):
+             ws.TrainConfig("tp", world, 1, 1), serve_cfg(world, 1, 1), 0.01, 1.1)):
         bad, rep = layout_case(rank, world, uid, manifest, train, serve, density, 5, zipf)
         results[name] = bad or "ok"
         results[name + " shards dense/sparse"] = (rep["dense_shards"], rep["sparse_shards"])
@@ -242,7 +251,7 @@ def main():
     if world > 1:
         for density in (0.01, 0.45):
             bad, rep = layout_case(rank, world, uid, ws.MODELS["qwen2.5-0.5b"]([0, 23]),
-                                   ws.TrainConfig("fsdp"), ws.ServeConfig(1, 1, world), density, 7)
+                                   ws.TrainConfig("fsdp"), serve_cfg(1, 1, world), density, 7)
             results[f"fan-out tp1x{world} d={density}"] = bad or "ok"
             ok &= not bad
     for dtype in (ws.I32, ws.F32):

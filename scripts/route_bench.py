@@ -31,20 +31,23 @@ def main():
     ap.add_argument("--model", default="qwen3-8b")
     ap.add_argument("--density", type=float, default=0.01)
     ap.add_argument("--serve-tp", type=int, default=2)
+    ap.add_argument("--dense", action="store_true", help="sparse=False syncs (dense box copies)")
+    ap.add_argument("--placement", default="overlap", choices=["rank", "overlap"])
     args = ap.parse_args()
     n = args.gpus
     tp = min(args.serve_tp, n)
     g = ws.EngineGroup(ws.MODELS[args.model](), ws.BF16, ws.TrainConfig("fsdp"),
-                       ws.ServeConfig(tp, 1, n // tp), n, device=list(range(n)))
+                       ws.ServeConfig(tp, 1, n // tp, args.placement), n,
+                       device=list(range(n)))
     g.generate(seed=1, density=args.density)
     rev = False
     for _ in range(args.warmup):
-        g.sync_step(reverse=rev, report=False)
+        g.sync_step(sparse=not args.dense, reverse=rev, report=False)
         rev = not rev
     for e in g.engines:
         e.timing(reset=True)
     for _ in range(args.steps):
-        g.sync_step(reverse=rev, report=False)
+        g.sync_step(sparse=not args.dense, reverse=rev, report=False)
         rev = not rev
     ranks = []
     for e in g.engines:
@@ -52,7 +55,7 @@ def main():
         xb = e.exchange_bytes()
         k = max(1, t["steps"])
         pack = t["pack_s"] / t["pack_steps"] if t["pack_steps"] else None
-        sent = xb["sent_records"] + xb["sent_dense"]
+        sent = xb["sent_record_bytes"] + xb["sent_dense_bytes"]
         ranks.append({"device": e.device.index, "encode_ms": t["encode_s"] / k * 1e3,
                       "route_ms": t["route_s"] / k * 1e3,
                       "pack_ms": pack * 1e3 if pack else None, **xb,
@@ -65,7 +68,8 @@ def main():
                                       device=e.device)
             want = nx if rev else pv
             ok &= bool(torch.equal(e.serve_view(i).view(torch.int16), want.view(torch.int16)))
-    print(json.dumps({"gpus": n, "model": args.model, "density": args.density,
+    print(json.dumps({"gpus": n, "model": args.model, "density": args.density, "dense": args.dense,
+                      "placement": args.placement,
                       "layout": f"FSDP{n} -> TP{tp} x {n // tp}", "steps": args.steps,
                       "verified": ok, "ranks": ranks}), flush=True)
     g.close()

@@ -56,12 +56,21 @@ def _layouts(ws):
         "tp2pp2dp2-tp4pp2": (ws.TrainConfig("tp", 2, 2, 2), ws.ServeConfig(4, 2, 1), 8),
         # BASELINE config 3's layout (TP8 -> TP4 x 2)
         "tp8-tp4x2": (ws.TrainConfig("tp", 8, 1, 1), ws.ServeConfig(4, 1, 2), 8),
+        # serving ranks placed for the fewest NVLink bytes (WS_PLACE_OVERLAP)
+        "fsdp4-tp2x2-overlap": (ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, 2, "overlap"), 4),
+        "fsdp8-tp2x4-overlap": (ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, 4, "overlap"), 8),
+        "tp8-tp4x2-overlap": (ws.TrainConfig("tp", 8, 1, 1), ws.ServeConfig(4, 1, 2, "overlap"),
+                              8),
+        "tp2pp2dp2-tp4pp2-overlap": (ws.TrainConfig("tp", 2, 2, 2),
+                                     ws.ServeConfig(4, 2, 1, "overlap"), 8),
     }
 
 
 @pytest.mark.parametrize("layout", ["fsdp2-tp2", "fsdp4-tp2x2", "fsdp8-tp2x4", "fsdp4-tp1x4",
                                     "tp2pp2-tp1pp2x2", "tp2dp2-tp2x2", "tp1pp2dp2-tp2pp2",
-                                    "tp2pp2dp2-tp4pp2", "tp8-tp4x2"])
+                                    "tp2pp2dp2-tp4pp2", "tp8-tp4x2", "fsdp4-tp2x2-overlap",
+                                    "fsdp8-tp2x4-overlap", "tp8-tp4x2-overlap",
+                                    "tp2pp2dp2-tp4pp2-overlap"])
 def test_group_bf16_layouts(layout):
     """bf16 sparse sync (1%), reverse sync, dense fallback (45%), sparse=False
     on the toy transformer (4 layers, so PP=2 has two stages)."""
@@ -88,10 +97,12 @@ def test_group_config2_layout_qwen():
     """BASELINE config 2's layout, FSDP8 -> TP2 x 4, on Qwen2.5-0.5B-shaped
     weights (cross-dim FSDP -> TP routes for every RowLinear), 1% density,
     10 alternating syncs (epochs and acks through several steps): an even
-    count leaves every replica at `prev`, then one more at `next`."""
+    count leaves every replica at `prev`, then one more at `next`.  Serving
+    ranks placed as the bench places them (overlap placement)."""
     import paper_2605_06534_b200 as ws
     g = ws.EngineGroup(ws.MODELS["qwen2.5-0.5b"](), ws.BF16, ws.TrainConfig("fsdp"),
-                       ws.ServeConfig(2, 1, 4), 8, device=0)
+                       ws.ServeConfig(2, 1, 4, "overlap"), 8, device=0)
+    assert [e.plan.info.serve_coord for e in g.engines] == [0, 0, 0, 0, 1, 1, 1, 1]
     g.generate(seed=8, density=0.01)
     for k in range(10):
         g.sync_step(reverse=bool(k % 2), report=False)
@@ -174,7 +185,8 @@ REF_LAYOUTS = [((2, 1, 1), (2, 1)), ((2, 1, 1), (1, 1)), ((1, 2, 1), (1, 2)),
 
 @pytest.mark.parametrize("train,serve", REF_LAYOUTS)
 @pytest.mark.parametrize("dtype", [I32, F32])
-def test_group_matches_reference_engine(reference, dtype, train, serve):
+@pytest.mark.parametrize("placement", ["rank", "overlap"])
+def test_group_matches_reference_engine(reference, dtype, train, serve, placement):
     """Same weights through the reference's sync_step (MemoryRelay, Async,
     shard-aware, sparse, 0.20) and through the group; 5% density so most
     shards are sparse and the small ones go dense."""
@@ -188,7 +200,8 @@ def test_group_matches_reference_engine(reference, dtype, train, serve):
                      bucket_bytes=8192)
     manifest = [ws.ParamMeta(n, k, tuple(s), l) for (n, k, s, l) in st.params]
     g = ws.EngineGroup(manifest, dtype, ws.TrainConfig("tp", *train),
-                       ws.ServeConfig(serve[0], serve[1], world // coords), world, device=0)
+                       ws.ServeConfig(serve[0], serve[1], world // coords, placement), world,
+                       device=0)
     for eng in g.engines:
         _load_reference_state(ws, eng, st, dtype)
     reps = g.sync_step()
@@ -207,7 +220,8 @@ def test_group_matches_reference_engine(reference, dtype, train, serve):
     g.close()
 
 
-def test_group_one_rank_per_gpu():
+@pytest.mark.parametrize("placement", ["rank", "overlap"])
+def test_group_one_rank_per_gpu(placement):
     """The same group with one rank per GPU of the process (peer memory over
     NVLink, every rank's sync concurrent on its GPU): FSDP-N -> TP2 x N/2 on
     the GPUs present (skipped on a one-GPU box)."""
@@ -217,8 +231,8 @@ def test_group_one_rank_per_gpu():
         pytest.skip("needs 2+ GPUs")
     n = 4 if n >= 4 else 2
     manifest = ws.MODELS["qwen2.5-0.5b"]([0, 1, 23])
-    g = ws.EngineGroup(manifest, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, n // 2),
-                       n, device=list(range(n)))
+    g = ws.EngineGroup(manifest, ws.BF16, ws.TrainConfig("fsdp"),
+                       ws.ServeConfig(2, 1, n // 2, placement), n, device=list(range(n)))
     g.generate(seed=2, density=0.01)
     for k in range(4):
         g.sync_step(reverse=bool(k % 2), report=False)

@@ -211,19 +211,71 @@ def test_expert_thresholds_match_restatement():
     assert sorted(zipf) == sorted(ws.expert_thresholds(128, 0.01, 1.1, 8))
 
 
+def _remote_elems(plan, replicas):
+    """Elements GPU `plan.rank` stores into peers per dense sync: every
+    route once per replica, minus the one its own serving shard holds."""
+    return sum(ov * replicas - (ov if c == plan.info.serve_coord else 0)
+               for (_, c, _, ov) in plan.routes)
+
+
+@pytest.mark.parametrize("world,tp", [(4, 2), (8, 2), (8, 4)])
+def test_overlap_placement(world, tp):
+    """WS_PLACE_OVERLAP: serving ranks are a permutation of the GPUs, every
+    coordinate has its replicas, routes are unchanged, and the heaviest
+    GPU stores fewer bytes into its peers than under rank placement (FSDP-N
+    -> TP2: coordinate 0 on the GPUs whose trainer rows it serves)."""
+    import paper_2605_06534_b200 as ws
+    m = ws.MODELS["qwen3-8b"]()
+    got = {}
+    for placement in ("rank", "overlap"):
+        plans = [ws.Plan(m, ws.BF16, ws.TrainConfig("fsdp"),
+                         ws.ServeConfig(tp, 1, world // tp, placement), world=world, rank=r)
+                 for r in range(world)]
+        ranks = [p.info.serve_rank for p in plans]
+        assert sorted(ranks) == list(range(world))
+        for p in plans:
+            assert p.info.serve_coord == p.info.serve_rank % tp
+            assert p.info.serve_replica == p.info.serve_rank // tp
+        got[placement] = (plans, [p.info.serve_coord for p in plans],
+                          max(_remote_elems(p, world // tp) for p in plans))
+    assert got["rank"][1] == [r % tp for r in range(world)]
+    if tp == 2:
+        assert got["overlap"][1] == [r * tp // world for r in range(world)]
+    assert got["overlap"][2] < got["rank"][2]
+    for a, b in zip(got["rank"][0], got["overlap"][0]):
+        assert a.routes == b.routes and a.segments == b.segments
+    with pytest.raises(ValueError):
+        ws.ServeConfig(2, 1, 2, "nearest").c()
+
+
+def test_overlap_placement_keeps_rank_order_on_ties():
+    """When every placement moves the same bytes (replicated parameters
+    only), serving rank g stays on GPU g."""
+    import paper_2605_06534_b200 as ws
+    K = ws.ModuleKind
+    m = [ws.ParamMeta("n", K.NORM, (64,), 0)]
+    for r in range(4):
+        p = ws.Plan(m, ws.BF16, ws.TrainConfig("fsdp"), ws.ServeConfig(2, 1, 2, "overlap"),
+                    world=4, rank=r)
+        assert p.info.serve_rank == r
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("rounds", [1, 3, 4])
-def test_exchange_layouts_consistent(world, rounds):
+@pytest.mark.parametrize("placement", ["rank", "overlap"])
+def test_exchange_layouts_consistent(world, rounds, placement):
     """The P2P exchange every rank builds (receive regions, rounds, who
     expects whom) is consistent for the bench layout up to 8 GPUs -- the
     N = 8 path the pool cannot run is checked here on the host."""
     import paper_2605_06534_b200 as ws
     from paper_2605_06534_b200._lib import check, lib
     tp = 1 if world == 1 else 2
-    layouts = [(ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp), ws.MODELS["qwen3-8b"]()),
-               (ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(max(1, world // 2), 1, min(2, world)),
+    layouts = [(ws.TrainConfig("fsdp"), ws.ServeConfig(tp, 1, world // tp, placement),
+                ws.MODELS["qwen3-8b"]()),
+               (ws.TrainConfig("tp", world, 1, 1),
+                ws.ServeConfig(max(1, world // 2), 1, min(2, world), placement),
                 ws.MODELS["qwen3-32b"]([0, 63])),
-               (ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1),
+               (ws.TrainConfig("tp", world, 1, 1), ws.ServeConfig(world, 1, 1, placement),
                 ws.MODELS["qwen3-30b-a3b"]([0, 47]))]
     for train, serve, manifest in layouts:
         plan = ws.Plan(manifest, ws.BF16, train, serve, world=world, rank=0)

@@ -1,7 +1,8 @@
 """Multi-GPU parity (one process per GPU through torchrun): runs
 scripts/mgpu_check.py on every visible GPU (at most 4) for both exchange
-paths -- the fused peer-memory (P2P) path and the NCCL baseline -- and
-the P2P path with bounded receive regions.  Skipped on
+paths -- the fused peer-memory (P2P) path and the NCCL baseline -- with
+serving ranks placed by overlap (the bench's placement), and the P2P path
+with the reference's rank order.  Skipped on
 a single-GPU box; the CPU side of the N>1 logic is covered by
 tests/test_multirank_cpu.py."""
 import json
@@ -25,15 +26,15 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p_bounded"])
+@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p_rank"])
 def test_mgpu_check(mode):
-    """p2p_bounded: receive regions sized by WSYNC_MAX_THRESHOLD=0.2."""
+    """p2p_rank: serving rank g on GPU g (WS_PLACE_RANK)."""
     n = min(torch.cuda.device_count(), 4)
     if n < 2:
         pytest.skip("needs at least 2 GPUs")
     env = dict(os.environ, WSYNC_EXCHANGE=mode.split("_")[0])
-    if mode == "p2p_bounded":
-        env["WSYNC_MAX_THRESHOLD"] = "0.2"
+    if mode == "p2p_rank":
+        env["WSYNC_CHECK_PLACEMENT"] = "rank"
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
                         "--master-port", str(_port()), os.path.join(ROOT, "scripts", "mgpu_check.py")],
