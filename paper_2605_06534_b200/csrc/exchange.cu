@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -926,6 +927,22 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
     return !(e && e[0] == '0');
   }();
   cudaStream_t ks = c->s_enc, xs = overlap ? c->s_xchg : c->s_enc;
+  // ablation build: WSYNC_TIMELINE=1 prints each sync's stage timeline (ms from
+  // the start: every K1 round, pack and receive-side apply, the local route)
+  static const bool timeline = ablation_env("WSYNC_TIMELINE") != nullptr;
+  thread_local std::map<int, std::vector<cudaEvent_t>> tl_events;  // per device
+  std::vector<cudaEvent_t>& tl_ev = tl_events[device_];
+  std::vector<std::string> tl_name;
+  auto mark = [&](const std::string& name, cudaStream_t st) -> ws_status {
+    if (!timeline) return WS_OK;
+    if (tl_name.size() == tl_ev.size()) {
+      tl_ev.emplace_back();
+      WS_CUDA_TRY(cudaEventCreate(&tl_ev.back()), "event");
+    }
+    WS_CUDA_TRY(cudaEventRecord(tl_ev[tl_name.size()], st), "event");
+    tl_name.push_back(name);
+    return WS_OK;
+  };
   WS_CUDA_TRY(cudaEventRecord(c->ev_start, s), "event");
   WS_CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_start, 0), "wait");
   if (xs != ks) WS_CUDA_TRY(cudaStreamWaitEvent(xs, c->ev_start, 0), "wait");
@@ -933,6 +950,8 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
   if (count_only_) WS_CUDA_TRY(cudaMemsetAsync(d_fill_, 0, nseg_ * 8, ks), "memset fill");
   const EncodeArgs a = encode_args(pa, na);
   const int sms = sm_count();
+  ws_status st0 = mark("start", ks);
+  if (st0 != WS_OK) return st0;
   for (int r = 0; r < R; ++r) {
     EncodeArgs ar = a;
     ar.tile_offset = c->tile_first[r];
@@ -946,10 +965,15 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
       ws_status st = launch_fixup(a, c->seg_first[r], c->seg_first[r + 1], ks, launches);
       if (st != WS_OK) return st;
     }
+    ws_status st = mark("k1." + std::to_string(r), ks);
+    if (st != WS_OK) return st;
     if (r < R - 1) {
       WS_CUDA_TRY(cudaEventRecord(c->ev_round[r], ks), "event");
       if (xs != ks) WS_CUDA_TRY(cudaStreamWaitEvent(xs, c->ev_round[r], 0), "wait");
-      ws_status st = exchange_round(o, na, r, xs, launches);
+      st = exchange_pack(o, na, r, xs, launches);
+      if (st == WS_OK) st = mark("pack." + std::to_string(r), xs);
+      if (st == WS_OK) st = exchange_apply(r, xs, launches);
+      if (st == WS_OK) st = mark("apply." + std::to_string(r), xs);
       if (st != WS_OK) return st;
     }
   }
@@ -957,7 +981,11 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
   ws_status st = local_route(o, pa, na, ks, launches);
   if (st != WS_OK) return st;
   WS_CUDA_TRY(cudaEventRecord(ev[3], ks), "event");
-  st = exchange_round(o, na, R - 1, ks, launches);
+  st = mark("local", ks);
+  if (st == WS_OK) st = exchange_pack(o, na, R - 1, ks, launches);
+  if (st == WS_OK) st = mark("pack." + std::to_string(R - 1), ks);
+  if (st == WS_OK) st = exchange_apply(R - 1, ks, launches);
+  if (st == WS_OK) st = mark("apply." + std::to_string(R - 1), ks);
   if (st != WS_OK) return st;
   if (xs != ks) {
     WS_CUDA_TRY(cudaEventRecord(c->ev_xdone, xs), "event");
@@ -965,6 +993,18 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
   }
   st = exchange_end(ks);
   if (st != WS_OK) return st;
+  if (timeline) {
+    st = mark("end", ks);
+    if (st != WS_OK) return st;
+    WS_CUDA_TRY(cudaEventSynchronize(tl_ev[tl_name.size() - 1]), "sync");
+    std::string line = "{\"rank\": " + std::to_string(c->rank);
+    for (size_t i = 1; i < tl_name.size(); ++i) {
+      float ms = 0;
+      WS_CUDA_TRY(cudaEventElapsedTime(&ms, tl_ev[0], tl_ev[i]), "elapsed");
+      line += ", \"" + tl_name[i] + "\": " + std::to_string(ms);
+    }
+    fprintf(stderr, "%s}\n", line.c_str());
+  }
   WS_CUDA_TRY(cudaEventRecord(c->ev_encdone, ks), "event");
   WS_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_encdone, 0), "wait");
   return WS_OK;
