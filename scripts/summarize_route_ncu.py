@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Summarise an ncu CSV of the route kernels (scripts/gpu_r2_n*.sh: ncu over
+"""Summarise an ncu CSV of the route kernels (scripts/gpu_route_ncu.sh: ncu over
 scripts/route_bench.py, one process, one rank per GPU) into per-launch
 NVLink / DRAM rates: prints a table and writes profiles/route_ncu.json."""
 import csv
@@ -26,10 +26,21 @@ def load(path):
 
 def main():
     summary = {}
+    # key -> capture: the bench reads str(N) (its placement, overlap, when
+    # captured); "4_rank" / "4_dense" are the rank-order and sparse=False runs
+    caps = []
     for n in (2, 4, 8):
-        path = os.path.join(ROOT, "profiles", f"r02_route_ncu_n{n}.csv")
-        if not os.path.exists(path):
-            continue
+        for suffix in ("_overlap", ""):
+            path = os.path.join(ROOT, "profiles", f"r02_route_ncu_n{n}{suffix}.csv")
+            if os.path.exists(path):
+                caps.append((str(n), path))
+                break
+    for key, name in (("4_rank", "r02_route_ncu_n4.csv"),
+                      ("4_dense", "r02_route_ncu_dense_n4_overlap.csv")):
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path) and all(path != p for _, p in caps):
+            caps.append((key, path))
+    for n, path in caps:
         launches = []
         print(f"== N={n} ({os.path.basename(path)})")
         print(f"{'launch':>6} {'dev':>3} {'kernel':28} {'us':>8} {'nvltx MB':>9} {'user MB':>8} "
@@ -53,7 +64,7 @@ def main():
             mean = sum(r["nvltx_gbs"] for r in packs) / len(packs)
             print(f"pack_kernel: mean {mean:.0f} GB/s nvltx ({mean / 900:.2f} of 900), "
                   f"max {best['nvltx_gbs']:.0f}")
-            summary[str(n)] = {"pack_nvltx_gbs_mean": mean, "pack_frac_of_900_mean": mean / 900,
+            summary[n] = {"pack_nvltx_gbs_mean": mean, "pack_frac_of_900_mean": mean / 900,
                                "pack_user_gbs_mean": sum(r["user_gbs"] for r in packs) / len(packs),
                                "launches": launches, "source": os.path.basename(path)}
     with open(os.path.join(ROOT, "profiles", "route_ncu.json"), "w") as f:
