@@ -542,6 +542,14 @@ ws_status ws_engine_segment_counts(ws_engine* eng, uint64_t* nnz, char* codec);
 ws_status ws_engine_segment_delta(ws_engine* eng, int i, const uint32_t** idx,
                                   const void** val, uint64_t* nnz, char* codec);
 
+/* Segment i's record stream as K1 wrote it in the last sync (engine mode,
+ * before any compaction): one run per super-tile of `*tile_elems` elements,
+ * the runs in reservation order, ascending inside each; `*nrec` records
+ * (min(count, capacity); 0 when the segment went dense).  Device pointers
+ * into the engine's record buffer.  Synchronises. */
+ws_status ws_engine_segment_stream(ws_engine* eng, int i, const uint32_t** idx,
+                                   const void** val, uint64_t* nrec, uint64_t* tile_elems);
+
 #ifdef __cplusplus
 }
 #endif

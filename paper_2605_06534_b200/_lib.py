@@ -239,6 +239,8 @@ _SIGS = {
     "ws_group_sync_step": ([_vp, C.POINTER(SyncOptions), _vp, _vp], C.c_int),
     "ws_engine_segment_delta": ([_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_u64),
                                  C.c_char_p], C.c_int),
+    "ws_engine_segment_stream": ([_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_u64),
+                                  C.POINTER(_u64)], C.c_int),
 }
 
 SYMBOLS = tuple(_SIGS)

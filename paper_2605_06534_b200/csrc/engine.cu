@@ -254,6 +254,14 @@ ws_status ws_engine_segment_counts(ws_engine* eng, uint64_t* nnz, char* codec) {
   return eng->segment_counts(nnz, codec);
 }
 
+ws_status ws_engine_segment_stream(ws_engine* eng, int i, const uint32_t** idx, const void** val,
+                                   uint64_t* nrec, uint64_t* tile_elems) {
+  DeviceGuard device_guard;
+  if (!eng || !idx || !val || !nrec || !tile_elems)
+    return set_error(WS_INVALID_ARGUMENT, "ws_engine_segment_stream: null argument");
+  return eng->segment_stream(i, idx, val, nrec, tile_elems);
+}
+
 ws_status ws_engine_segment_delta(ws_engine* eng, int i, const uint32_t** idx, const void** val,
                                   uint64_t* nnz, char* codec) {
   DeviceGuard device_guard;

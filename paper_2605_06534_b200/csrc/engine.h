@@ -25,6 +25,8 @@ struct ws_engine {
                      uint64_t perm_seed = 0);
   ws_status sync_step(const ws_sync_options& o, cudaStream_t s, const void* next_host,
                       uint64_t* nnz_host, ws_report* report);
+  ws_status segment_stream(int i, const uint32_t** idx, const void** val, uint64_t* nrec,
+                           uint64_t* tile_elems);
   ws_status segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
                           char* codec);
   ws_status segment_counts(uint64_t* nnz, char* codec);

@@ -527,6 +527,21 @@ ws_status ws_engine::segment_counts(uint64_t* nnz, char* codec) {
   return WS_OK;
 }
 
+ws_status ws_engine::segment_stream(int i, const uint32_t** idx, const void** val,
+                                    uint64_t* nrec, uint64_t* tile_elems) {
+  if (i < 0 || i >= nseg_) return set_error(WS_INVALID_ARGUMENT, "segment index out of range");
+  WS_CUDA_TRY(cudaSetDevice(device_), "cudaSetDevice");
+  WS_CUDA_TRY(cudaDeviceSynchronize(), "sync");
+  uint64_t n = 0;
+  WS_CUDA_TRY(cudaMemcpy(&n, d_nnz_ + i, 8, cudaMemcpyDeviceToHost), "D2H nnz");
+  const bool sparse = last_sparse_ && n <= segs_[i].cap;
+  *idx = d_idx_ + segs_[i].rec;
+  *val = static_cast<const char*>(d_val_) + segs_[i].rec * dtype_size(dtype_);
+  *nrec = sparse ? n : 0;
+  *tile_elems = encode_tile_elems(dtype_);
+  return WS_OK;
+}
+
 ws_status ws_engine::segment_delta(int i, const uint32_t** idx, const void** val, uint64_t* nnz,
                                    char* codec) {
   if (i < 0 || i >= nseg_) return set_error(WS_INVALID_ARGUMENT, "segment index out of range");

@@ -291,6 +291,20 @@ class TransferEngine:
                            _wrap(val.value, k, VAL_DTYPE[self.plan.dtype], self.device)), c, nnz.value
 
 
+    def segment_stream(self, i):
+        """Segment i's records as K1 wrote them in the last sync (one run per
+        super-tile, runs in reservation order, ascending inside each):
+        (idx int32 tensor, val tensor, super-tile elements) --
+        ws_engine_segment_stream."""
+        idx, val, n, te = C.c_void_p(), C.c_void_p(), C.c_uint64(), C.c_uint64()
+        with torch.cuda.device(self.device):
+            check(lib.ws_engine_segment_stream(self.h, i, C.byref(idx), C.byref(val), C.byref(n),
+                                               C.byref(te)))
+        k = n.value
+        return (_wrap(idx.value, k, torch.int32, self.device),
+                _wrap(val.value, k, VAL_DTYPE[self.plan.dtype], self.device), te.value)
+
+
 class EngineGroup:
     """Every rank of a multi-GPU layout as an engine of THIS process on one
     GPU (ws_group, include/wsync.h): the ranks share mailboxes, receive

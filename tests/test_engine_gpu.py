@@ -177,6 +177,52 @@ def _check_segment_on_device(eng, i, reverse=False):
     return nnz
 
 
+def _check_stream_as_written(eng, i):
+    """Segment i's records exactly as K1 left them in the engine (before any
+    compaction; what the local route and the NVLink pack read): every
+    super-tile's records are one contiguous run, strictly ascending inside
+    it, and the stream sorted is the compacted ascending stream, values
+    attached (codec.cpp:48-49 order restored)."""
+    idx, val, tile_elems = eng.segment_stream(i)
+    delta, codec, nnz = eng.segment_delta(i)
+    if codec != "S":
+        assert idx.numel() == 0
+        return
+    assert idx.numel() == nnz
+    if nnz == 0:
+        return
+    ii = idx.to(torch.int64) & 0xFFFFFFFF
+    tile = ii // tile_elems
+    starts = torch.cat([torch.zeros(1, dtype=torch.int64, device=ii.device),
+                        torch.nonzero(tile[1:] != tile[:-1]).flatten() + 1])
+    run_tiles = tile[starts]
+    assert run_tiles.unique().numel() == run_tiles.numel(), i  # one run per super-tile
+    same = tile[1:] == tile[:-1]
+    assert bool((ii[1:][same] > ii[:-1][same]).all()), i
+    order = torch.argsort(ii)
+    assert torch.equal(ii[order], delta.indices.to(torch.int64) & 0xFFFFFFFF), i
+    assert torch.equal(val[order].view(torch.int16), delta.values.view(torch.int16)), i
+
+
+@pytest.mark.parametrize("density", [0.01, 0.05, 0.15])
+def test_k1_stream_as_written(density):
+    """The engine's unordered record stream itself (ws_engine_segment_stream),
+    both K1 instantiations: the first sync runs the per-record one, later
+    syncs the streamed-apply one (4 staging slots per thread, so 5% and 15%
+    push many records through the spill path)."""
+    import paper_2605_06534_b200 as ws
+    _, plan, eng = _engine(ws.MODELS["qwen2.5-0.5b"]([0, 1, 23]))
+    eng.generate(seed=5, density=density)
+    variants = []
+    for k in range(3):
+        rep = eng.sync_step(reverse=bool(k % 2))
+        variants.append(rep["streamed_apply"])
+        for i in range(len(plan.segments)):
+            _check_stream_as_written(eng, i)
+            _check_segment_on_device(eng, i, reverse=bool(k % 2))
+    assert variants[0] == 0 and variants[-1] == 1, variants
+
+
 @pytest.mark.parametrize("model,density", [("qwen2.5-0.5b", 0.01), ("qwen2.5-0.5b", 0.1)])
 def test_full_model_bf16(restatement, model, density):
     """A whole model through the engine (many super-tiles per block, so warp
@@ -293,8 +339,8 @@ def test_qwen3_8b_whole_model_bench_config(restatement):
     FSDP1 -> TP1, 1% density, four alternating syncs.  From the second sync
     on K1 runs its streamed-apply instantiation (the first sync's density,
     1% >= 1/250, selects it) -- the one the bench times.  After the first
-    and the last sync every segment's compacted record stream and every
-    serving shard is checked on the device; the largest segment (the
+    and the last sync every segment's record stream (as K1 wrote it and
+    compacted) and every serving shard is checked on the device; the largest segment (the
     622 M-element embedding) and the smallest against the C oracle."""
     import paper_2605_06534_b200 as ws
     _, plan, eng = _engine(ws.MODELS["qwen3-8b"]())
@@ -313,6 +359,7 @@ def test_qwen3_8b_whole_model_bench_config(restatement):
         total = 0
         for i in range(len(plan.segments)):
             total += _check_segment_on_device(eng, i, reverse=rev)
+            _check_stream_as_written(eng, i)
             want = eng.segment_view(i, 0 if rev else 1).view(torch.int16)
             assert torch.equal(eng.serve_view(i).view(torch.int16), want), i
         assert rep["nnz"] == total
