@@ -9,6 +9,8 @@ exists; the fixture is committed so parity stays pinned on hosts without it
 
 Contents (every array produced by the reference's own functions):
   diff/<dtype>/<k>     codec.cpp:34-63 diff_shards + codec.cpp:65-92 apply_delta
+  bf16/<k>             the same on 16-bit words (the reference's I32 path on
+                       zero-extended words, low 16 bits)
   reslice/<k>          codec.cpp:94-138 reslice_delta (same-dim, randomized)
   wire/<dtype>/<iw>    codec.cpp:145-183 encode_sparse / encode_dense payloads
   key/<k>, frame/<k>   key.cpp:47-69 BucketKey::encode, wire.cpp:35-47 frames
@@ -64,6 +66,25 @@ def generate(ref):
             g.update({p + "shape": np.array(shape, np.int64), p + "prev": prev, p + "next": nxt,
                       p + "idx": idx.astype(np.uint64), p + "val": val, p + "target": tgt,
                       p + "applied": applied})
+    # bf16 has no reference code: the reference's I32 path on zero-extended
+    # 16-bit words (the low 16 bits of its u32 wrap-around delta / sum are the
+    # u16 wrap-around delta / sum)
+    for k, (n, dens) in enumerate(((4099, 0.01), (777, 0.3), (64, 1.0))):
+        prev = rng.integers(0, 1 << 16, n).astype(np.uint16)
+        nxt = prev.copy()
+        m = rng.random(n) < dens
+        nxt[m] += rng.integers(1, 1 << 16, m.sum()).astype(np.uint16)
+        prev[:4] = [0x7FC1, 0x0000, 0x8000, 0xFF80]  # NaN payload, +0, -0, -inf by bits
+        nxt[:4] = [0x7FC2, 0x8000, 0x8000, 0x7F80]
+        idx, val = ref.diff_shards(I32, [n], prev.astype(np.int32), nxt.astype(np.int32))
+        tgt = rng.integers(0, 1 << 16, n).astype(np.uint16)
+        applied, rc = ref.apply_delta(I32, [n], tgt.astype(np.int32), [n], idx, val)
+        assert rc == 0
+        p = f"bf16/{k}/"
+        g.update({p + "prev": prev, p + "next": nxt, p + "idx": idx.astype(np.uint64),
+                  p + "val": (val.astype(np.int64) & 0xFFFF).astype(np.uint16),
+                  p + "target": tgt, p + "applied": (applied.astype(np.int64) & 0xFFFF).astype(
+                      np.uint16)})
     for k in range(10):
         nd = int(rng.integers(1, 4))
         full = [int(rng.integers(1, 5)) * 4 for _ in range(nd)]

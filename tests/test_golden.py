@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle.oracle import F32, I32
+from oracle.oracle import BF16, F32, I32
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
                       "reference_vectors.npz")
@@ -62,6 +62,14 @@ def test_restatement_reproduces_golden(golden, restatement):
             pay = restatement.encode_sparse(dt, list(golden[p + "shape"]), golden[p + "idx"],
                                             golden[p + "val"], iw)
             assert bytes(pay) == golden[p + f"sparse{iw}"].tobytes(), (p, iw)
+    for k in _cases(golden, "bf16/"):
+        p = f"bf16/{k}/"
+        idx, val = restatement.diff_shards(BF16, golden[p + "prev"], golden[p + "next"])
+        assert idx.astype(np.uint64).tobytes() == golden[p + "idx"].tobytes(), p
+        assert val.view(np.uint16).tobytes() == golden[p + "val"].tobytes(), p
+        got, rc = restatement.apply_delta(BF16, golden[p + "target"], golden[p + "idx"],
+                                          golden[p + "val"])
+        assert rc == 0 and got.view(np.uint16).tobytes() == golden[p + "applied"].tobytes(), p
     for k in _cases(golden, "reslice/"):
         p = f"reslice/{k}/"
         oi, ov = restatement.reslice_delta(I32, list(golden[p + "full"]), _desc(golden[p + "src"]),
@@ -93,6 +101,19 @@ def test_cuda_codec_reproduces_golden(golden):
             tgt = _dev(golden[p + "target"], dt).view(shape)
             ws.apply_delta(tgt, d)
             assert tgt.cpu().numpy().tobytes() == golden[p + "applied"].tobytes(), p
+    for k in _cases(golden, "bf16/"):
+        p = f"bf16/{k}/"
+        prev = torch.from_numpy(golden[p + "prev"].view(np.int16).copy()).cuda().view(torch.bfloat16)
+        nxt = torch.from_numpy(golden[p + "next"].view(np.int16).copy()).cuda().view(torch.bfloat16)
+        d = ws.diff_shards(prev, nxt)
+        idx = d.indices.cpu().numpy().view(np.uint32).astype(np.uint64)
+        assert idx.tobytes() == golden[p + "idx"].tobytes(), p
+        assert d.values.cpu().numpy().view(np.uint16).tobytes() == golden[p + "val"].tobytes(), p
+        tgt = torch.from_numpy(golden[p + "target"].view(np.int16).copy()).cuda().view(
+            torch.bfloat16)
+        ws.apply_delta(tgt, d)
+        assert tgt.view(torch.int16).cpu().numpy().view(np.uint16).tobytes() == \
+            golden[p + "applied"].tobytes(), p
     for k in _cases(golden, "reslice/"):
         p = f"reslice/{k}/"
         full = tuple(int(x) for x in golden[p + "full"])
