@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256) local_apply_kernel(RouteSideArgs a) {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256) pack_kernel(PackArgs pa) {
+__global__ void __launch_bounds__(256, 4) pack_kernel(PackArgs pa) {
   using Tr = Traits<DT>;
   using T = typename Tr::T;
   const RouteSideArgs& a = pa.r;
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
 // Step 2: the grid applies unit after unit (one region slice each), then the
 // last block acks the sources so they may refill their regions next step.
 template <int DT>
-__global__ void __launch_bounds__(256) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
+__global__ void __launch_bounds__(256, 8) apply_p2p_kernel(P2PArgs P, typename Traits<DT>::T* serve) {
   const int W = P.world;
   using Tr = Traits<DT>;
   using T = typename Tr::T;
