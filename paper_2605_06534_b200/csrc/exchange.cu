@@ -868,7 +868,7 @@ ws_status ws_engine::exchange_mark_pack(cudaStream_t s) {
 ws_status ws_engine::exchange_apply(int round, cudaStream_t s, uint32_t* launches) {
   Comm* c = comm_;
   if (!c->rr[round].mask) return WS_OK;
-  WS_CUDA_TRY(launch_apply_p2p(dtype_, round_args(round), serve, sm_count() * 4, s),
+  WS_CUDA_TRY(launch_apply_p2p(dtype_, round_args(round), serve, sm_count() * 8, s),
               "apply (p2p)");
   *launches += 2;
   return WS_OK;

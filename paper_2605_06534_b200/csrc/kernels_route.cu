@@ -560,7 +560,7 @@ __global__ void p2p_ready_kernel(P2PArgs P) {
 // P2P receiver, step 1 (one block): wait (acquire) for the step flag of
 // every expected source, then turn the published per-entry counts into a
 // prefix of apply units (kApplyUnit records each).
-constexpr uint64_t kApplyUnit = 8192;
+constexpr uint64_t kApplyUnit = 2048;
 __global__ void __launch_bounds__(1024) p2p_recv_plan_kernel(P2PArgs P) {
   __shared__ uint64_t s_warp[32];
   __shared__ uint64_t s_carry;
