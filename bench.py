@@ -18,6 +18,7 @@ Value = 2 B x model elements / (max over ranks of device time per step).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -323,6 +324,10 @@ def run_ours(args):
 
     # ---- timed region: K syncs, no host synchronisation inside ----
     nvl = NvlinkCounters(local) if n > 1 else None
+    # no collector pause while the syncs are enqueued: at N > 1 a stalled
+    # rank stalls every peer's exchange
+    gc.collect()
+    gc.disable()
     barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -335,6 +340,7 @@ def run_ours(args):
             rev = not rev
         end.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     nvl1 = nvl.read() if nvl else None
     barrier()
     ms = start.elapsed_time(end) / args.steps
@@ -529,6 +535,8 @@ def run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev):
                        reverse=rev, report=False)
     rev = not rev
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()
     barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -538,6 +546,7 @@ def run_e2e(args, eng, plan, world, local, dense_eq_bytes, barrier, rev):
         rev = not rev
     torch.cuda.synchronize()
     barrier()
+    gc.enable()
     wall = (time.perf_counter() - t0) / steps
     t = torch.tensor([wall], device=eng.device, dtype=torch.float64)
     if world > 1:
