@@ -328,19 +328,39 @@ def run_ours(args):
     # rank stalls every peer's exchange
     gc.collect()
     gc.disable()
-    barrier()
-    torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nvl0 = nvl.read() if nvl else None
+    align = torch.zeros(1, device=dev)
+    # BENCH_STEP_TRACE=1: per-step device times and host enqueue times of
+    # every rank on stderr (diagnostics; the line's numbers are unchanged)
+    trace = os.environ.get("BENCH_STEP_TRACE") == "1"
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if trace else []
+    host_t = []
     with ClockSampler(local) as clocks:
+        # the sampler and counter reads start before the barrier, so no rank
+        # enters the timed region late; at N > 1 every GPU's start event
+        # follows the same collective, so the ranks' regions begin together
+        # (otherwise the first sync of an early rank waits for the others)
+        nvl0 = nvl.read() if nvl else None
+        barrier()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.all_reduce(align)
         start.record(stream)
-        for _ in range(args.steps):
+        h0 = time.perf_counter()
+        for k in range(args.steps):
             eng.sync_step(sparse=True, density_threshold=args.threshold, reverse=rev,
                           report=False)
             rev = not rev
+            if trace:
+                marks[k].record(stream)
+                host_t.append(round((time.perf_counter() - h0) * 1e3, 3))
         end.record(stream)
         torch.cuda.synchronize()
     gc.enable()
+    if trace:
+        print(json.dumps({"rank": rank, "step_end_ms": [round(start.elapsed_time(m), 3)
+                                                        for m in marks],
+                          "host_enqueued_ms": host_t}), file=sys.stderr, flush=True)
     nvl1 = nvl.read() if nvl else None
     barrier()
     ms = start.elapsed_time(end) / args.steps
