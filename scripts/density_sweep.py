@@ -29,10 +29,12 @@ def timed(eng, steps, **kw):
         eng.sync_step(reverse=rev, report=False, **kw)
         rev = not rev
     torch.cuda.synchronize()
-    if dist.is_initialized():
-        dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     eng.timing(reset=True)
+    if dist.is_initialized():
+        dist.barrier()
+        # every GPU's start event follows the same collective (bench.py)
+        dist.all_reduce(torch.zeros(1, device="cuda"))
     s.record()
     for _ in range(steps):
         eng.sync_step(reverse=rev, report=False, **kw)
