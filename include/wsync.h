@@ -343,6 +343,12 @@ ws_status ws_plan_segment_key_fields(const ws_plan* plan, int i, int32_t* tp_ran
  * destinations vs expectations, mailbox size): WS_OK when consistent. */
 ws_status ws_plan_check_exchange(const ws_plan* plan, int rounds);
 
+/* Exchange rounds an engine of this plan uses (K1 overlapped with the
+ * exchange when the layout's exchange is heavy: 3 when some rank stores at
+ * least half an element into peers per element it encodes, else 1;
+ * WSYNC_ROUNDS overrides). */
+ws_status ws_plan_exchange_rounds(const ws_plan* plan, int32_t* rounds);
+
 /* Route i: source segment, destination serving coordinate, number of
  * destination ranks (replicas of that coordinate) and the elements of the
  * box intersection. */

@@ -201,6 +201,7 @@ _SIGS = {
     "ws_bucket_key": ([_u64, C.c_char_p, C.c_int, C.c_int, C.c_int, Shard, C.c_char, C.c_int,
                        C.c_uint32, C.c_char_p, _u64, C.POINTER(_u64)], C.c_int),
     "ws_plan_check_exchange": ([_vp, C.c_int], C.c_int),
+    "ws_plan_exchange_rounds": ([_vp, C.POINTER(C.c_int32)], C.c_int),
     "ws_plan_segment_key_fields": ([_vp, C.c_int, C.POINTER(_i32), C.POINTER(_i32),
                                     C.POINTER(_i32)], C.c_int),
     "ws_engine_sync_relay": ([_vp, _u64, C.POINTER(SyncOptions), C.POINTER(RelayOptions),

@@ -366,10 +366,26 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile, double t) 
   L.head = kMailboxBytes + ((L.entries.size() * 4 + 255) / 256) * 256;
   return L;
 }
-int default_rounds(int world) {
-  // Measured (Qwen3-8B, 1%): 3 rounds take N = 4 from 4.10 to 3.74 ms; at
-  // N = 2 the 0.46 ms exchange gains nothing from the split.
-  int R = world >= 4 ? 3 : 1;
+// Exchange rounds of a plan: overlapping the exchange with K1 pays only when
+// the exchange is heavy, because K1 gives up SMs to it in every round after
+// the first.  The measure is the largest "remote share" over the ranks:
+// elements a rank stores into peers per element it encodes (every route once
+// per replica, minus the copy its own serving shard holds).  Measured (1%
+// unless noted): config 2 (share 0.15 at N = 2, 1.15 at N = 4) gains from 3
+// rounds only at N = 4 (4.10 -> 3.74 ms); config 3 (share 1.0, 0.5%) gains
+// at N = 2 too (20.89 -> 20.35 ms); config 4 (expert-sharded, share 0.005
+// at N = 4) loses 18% with them (7.67 vs 9.38 ms).
+int default_rounds(const Plan& plan) {
+  double worst = 0;
+  for (int g = 0; g < plan.world(); ++g) {
+    uint64_t train = 0, remote = 0;
+    for (const Segment& sg : plan.segments_of(g)) train += sg.n;
+    for (const Route& r : plan.routes_of(g))
+      remote += r.overlap * (uint64_t)plan.replicas() -
+                (r.coord == plan.coord_of_rank(g) ? r.overlap : 0);
+    if (train) worst = std::max(worst, (double)remote / (double)train);
+  }
+  int R = worst >= 0.5 ? 3 : 1;
   if (const char* e = getenv("WSYNC_ROUNDS")) R = std::max(1, std::min(kMaxRounds, atoi(e)));
   return R;
 }
@@ -461,7 +477,7 @@ ws_status ws_engine::init_comm(const uint8_t* unique_id, GroupShared* group) {
 ws_status ws_engine::init_p2p() {
   Comm* c = comm_;
   const int me = c->rank, W = c->world;
-  const int R = default_rounds(W);
+  const int R = default_rounds(plan_);
   c->R = R;
   const uint32_t tile = encode_tile_elems(dtype_);
   const RecvLayout L = recv_layout(plan_, me, R, tile, 1.0);
@@ -1136,6 +1152,12 @@ ws_status ws_engine::exchange_status() const {
 // the round of its segment; a receiver expects a source in round r exactly
 // when that source sends it something in round r; the mailbox fits.
 static ws_status check_exchange(const Plan& plan, int rounds, double t);
+
+extern "C" ws_status ws_plan_exchange_rounds(const ws_plan* plan_h, int32_t* rounds) {
+  if (!plan_h || !rounds) return set_error(WS_INVALID_ARGUMENT, "ws_plan_exchange_rounds: null");
+  *rounds = plan_h->p->world() > 1 ? default_rounds(*plan_h->p) : 1;
+  return WS_OK;
+}
 
 extern "C" ws_status ws_plan_check_exchange(const ws_plan* plan_h, int rounds) {
   if (!plan_h || rounds < 1 || rounds > kMaxRounds)

@@ -280,3 +280,31 @@ def test_exchange_layouts_consistent(world, rounds, placement):
     for train, serve, manifest in layouts:
         plan = ws.Plan(manifest, ws.BF16, train, serve, world=world, rank=0)
         check(lib.ws_plan_check_exchange(plan.h, rounds))
+
+
+def test_exchange_rounds_follow_the_remote_share(monkeypatch):
+    """K1 overlaps the exchange (3 rounds) only where the exchange is heavy:
+    config 2 at N >= 4 and config 3, not config 2 at N = 2 nor the
+    expert-sharded config 4 (measured, exchange.cu default_rounds)."""
+    import ctypes as C
+    import paper_2605_06534_b200 as ws
+    from paper_2605_06534_b200._lib import check, lib
+    monkeypatch.delenv("WSYNC_ROUNDS", raising=False)
+
+    def rounds(manifest, train, serve, world):
+        plan = ws.Plan(manifest, ws.BF16, train, serve, world=world, rank=0)
+        r = C.c_int32()
+        check(lib.ws_plan_exchange_rounds(plan.h, C.byref(r)))
+        return r.value
+
+    q8, q32, moe = ws.MODELS["qwen3-8b"](), ws.MODELS["qwen3-32b"]([0, 1]), \
+        ws.MODELS["qwen3-30b-a3b"]([0, 1])
+    fsdp = ws.TrainConfig("fsdp")
+    assert rounds(q8, fsdp, ws.ServeConfig(1, 1, 1), 1) == 1
+    assert rounds(q8, fsdp, ws.ServeConfig(2, 1, 1, "overlap"), 2) == 1
+    assert rounds(q8, fsdp, ws.ServeConfig(2, 1, 2, "overlap"), 4) == 3
+    assert rounds(q8, fsdp, ws.ServeConfig(2, 1, 4, "overlap"), 8) == 3
+    assert rounds(q32, ws.TrainConfig("tp", 2, 1, 1), ws.ServeConfig(1, 1, 2), 2) == 3
+    assert rounds(q32, ws.TrainConfig("tp", 4, 1, 1), ws.ServeConfig(2, 1, 2), 4) == 3
+    assert rounds(moe, ws.TrainConfig("tp", 4, 1, 1), ws.ServeConfig(4, 1, 1), 4) == 1
+    assert rounds(moe, ws.TrainConfig("tp", 8, 1, 1), ws.ServeConfig(8, 1, 1), 8) == 1
