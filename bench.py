@@ -192,7 +192,10 @@ def cpu_reference(args, threads=None, reps=1, warmup=0):
     from oracle.oracle import I32, Reference
     mf = load_manifest_module()
     ref = Reference()
-    nproc = os.cpu_count() or 1
+    try:  # the CPUs this process may run on (cgroup / affinity), not the host's count
+        nproc = len(os.sched_getaffinity(0)) or 1
+    except (AttributeError, OSError):
+        nproc = os.cpu_count() or 1
     layer_elems = sum(p.numel() for p in mf.MODELS[args.model](layer_subset=[1]))
     # 3 copies (prev, next, serving) at 4 B/elem per thread, at most half the free RAM
     try:
