@@ -180,9 +180,10 @@ struct ws_engine {
   uint64_t* d_sa_ = nullptr;
   bool sa_force_ = false;     // ablation: always the streamed-apply instantiation
   bool sa_env_ = false;       // WSYNC_SA_DIV given explicitly
-  // Off by default under overlapped exchange rounds (N >= 4): the serving
-  // stream then competes with the receive scatter for HBM (measured: 3.77 ->
-  // 3.92 ms at N = 4).
+  // Off by default under overlapped exchange rounds: the serving stream then
+  // competes with the receive scatter for HBM (measured at N = 4: 3.77 ->
+  // 3.92 ms in round 1; final build 3.21 -> 3.24 ms config 2, 10.26 -> 10.29
+  // ms config 3, profiles/r02_sa_under_rounds_n4.jsonl).
   uint32_t sa_div() const { return (sa_env_ || exchange_rounds() <= 1) ? sa_div_ : 0u; }
   bool fuse_apply_ = true;  // K1 applies local sparse records (WSYNC_NO_FUSED_APPLY=1 disables)
   int nlocal_ = 0;
