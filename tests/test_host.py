@@ -308,3 +308,30 @@ def test_exchange_rounds_follow_the_remote_share(monkeypatch):
     assert rounds(q32, ws.TrainConfig("tp", 4, 1, 1), ws.ServeConfig(2, 1, 2), 4) == 3
     assert rounds(moe, ws.TrainConfig("tp", 4, 1, 1), ws.ServeConfig(4, 1, 1), 4) == 1
     assert rounds(moe, ws.TrainConfig("tp", 8, 1, 1), ws.ServeConfig(8, 1, 1), 8) == 1
+
+
+@pytest.mark.parametrize("train,serve,world", [
+    (("fsdp",), (2, 1, 2), 4), (("fsdp",), (3, 1, 2), 6), (("fsdp",), (2, 1, 3), 6),
+    (("tp", 4, 1, 1), (2, 1, 2), 4), (("tp", 2, 2, 1), (1, 2, 2), 4),
+    (("tp", 3, 1, 2), (3, 1, 2), 6), (("tp", 6, 1, 1), (2, 1, 3), 6)])
+def test_overlap_placement_is_optimal(train, serve, world):
+    """The min-cost assignment behind WS_PLACE_OVERLAP (plan.cpp
+    assign_min_cost) keeps as many routed elements local as the best of all
+    world! placements (brute force)."""
+    import itertools
+    import paper_2605_06534_b200 as ws
+    m = ws.toy_transformer_manifest(layers=2, hidden=96, vocab=192)
+    tc = ws.TrainConfig(*train)
+    C = serve[0] * serve[1]
+    w = []
+    placed = 0
+    for g in range(world):
+        p = ws.Plan(m, ws.BF16, tc, ws.ServeConfig(*serve, "overlap"), world=world, rank=g)
+        row = [0] * C
+        for (_, c, _, ov) in p.routes:
+            row[c] += ov
+        w.append(row)
+        placed += row[p.info.serve_coord]
+    best = max(sum(w[g][perm[g] % C] for g in range(world))
+               for perm in itertools.permutations(range(world)))
+    assert placed == best
