@@ -88,6 +88,7 @@ struct ws_engine::Comm {
   // exchange rounds (P2P): K1 encodes segment runs round by round and round
   // r's pack/apply overlap the encode of round r + 1
   int R = 1;
+  int overlap_sms = 28;                          // SMs left to the exchange beside K1
   uint64_t step = 0;                             // syncs so far (epochs derive from it)
   std::vector<int> ent_first;                    // R + 1: my remote entries per round
   std::vector<int> seg_first;                    // R + 1: my segments per round
@@ -375,7 +376,7 @@ RecvLayout recv_layout(const Plan& plan, int q, int R, uint32_t tile, double t) 
 // rounds only at N = 4 (4.10 -> 3.74 ms); config 3 (share 1.0, 0.5%) gains
 // at N = 2 too (20.89 -> 20.35 ms); config 4 (expert-sharded, share 0.005
 // at N = 4) loses 18% with them (7.67 vs 9.38 ms).
-int default_rounds(const Plan& plan) {
+double remote_share(const Plan& plan) {
   double worst = 0;
   for (int g = 0; g < plan.world(); ++g) {
     uint64_t train = 0, remote = 0;
@@ -385,9 +386,19 @@ int default_rounds(const Plan& plan) {
                 (r.coord == plan.coord_of_rank(g) ? r.overlap : 0);
     if (train) worst = std::max(worst, (double)remote / (double)train);
   }
-  int R = worst >= 0.5 ? 3 : 1;
+  return worst;
+}
+int default_rounds(const Plan& plan) {
+  int R = remote_share(plan) >= 0.5 ? 3 : 1;
   if (const char* e = getenv("WSYNC_ROUNDS")) R = std::max(1, std::min(kMaxRounds, atoi(e)));
   return R;
+}
+// SMs K1 leaves to the exchange kernels in rounds after the first: 28 at a
+// remote share near 1 (config 2 at N = 4: 16/20/28/36 SMs -> 3.41/3.28/3.20/
+// 3.36 ms), 40 from a share of 2 (FSDP4 -> TP1 x 4, share 3, the stand-in
+// for config 2 at N = 8: 4.61 ms with 28, 4.54 with 40, 4.75 with 56).
+int overlap_sms(const Plan& plan) {
+  return remote_share(plan) >= 2.0 ? 40 : 28;
 }
 }  // namespace
 
@@ -479,6 +490,7 @@ ws_status ws_engine::init_p2p() {
   const int me = c->rank, W = c->world;
   const int R = default_rounds(plan_);
   c->R = R;
+  c->overlap_sms = overlap_sms(plan_);
   const uint32_t tile = encode_tile_elems(dtype_);
   const RecvLayout L = recv_layout(plan_, me, R, tile, 1.0);
   int ok = cudaMalloc(&c->d_head, L.head) == cudaSuccess &&
@@ -934,10 +946,11 @@ ws_status ws_engine::sync_rounds(const ws_sync_options& o, int pa, int na, cudaS
                                  uint32_t* launches, cudaEvent_t* ev) {
   Comm* c = comm_;
   const int R = c->R;
-  static const int overlap_sms = [] {
+  static const int overlap_sms_env = [] {
     const char* e = ablation_env("WSYNC_OVERLAP_SMS");
-    return e ? std::max(0, atoi(e)) : 28;
+    return e ? std::max(0, atoi(e)) : -1;
   }();
+  const int overlap_sms = overlap_sms_env >= 0 ? overlap_sms_env : c->overlap_sms;
   static const bool overlap = [] {
     const char* e = ablation_env("WSYNC_OVERLAP");
     return !(e && e[0] == '0');
