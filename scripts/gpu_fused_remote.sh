@@ -1,6 +1,8 @@
 #!/bin/bash
-# K1-emitted remote records with the streamed apply (ablation build,
-# WSYNC_FUSED_REMOTE=1) vs the pack kernel: parity + same-box A/B at N GPUs
+# K1-emitted remote records (ablation build, WSYNC_FUSED_REMOTE=1) vs the pack
+# kernel: parity + same-box A/B at N GPUs.  r02_fused_remote_sa_ab_n2.jsonl was
+# taken with an encode_kernel<bf16, REMOTE, SA> instantiation that was not kept;
+# the shipped ablation build emits without the streamed apply.
 cd $GRAFT_REPO_ROOT
 N=${N:-2}
 O=gpurun_out/fr_n$N; mkdir -p $O
