@@ -68,12 +68,18 @@ struct ws_engine {
   ws_status sync_begin(SyncCtx& x, const ws_sync_options& o, cudaStream_t s,
                        const void* next_host);
   // K1 (every exchange round's segments back to back) + local route
-  ws_status sync_encode(SyncCtx& x, cudaStream_t s);
+  ws_status sync_encode(SyncCtx& x, cudaStream_t s, bool run_local = true);
   ws_status sync_finish(SyncCtx& x, cudaStream_t s, uint64_t* nnz_host, ws_report* report);
   // sync_step without the grouped-engine check
   ws_status sync_step_impl(const ws_sync_options& o, cudaStream_t s, const void* next_host,
                            uint64_t* nnz_host, ws_report* report);
   int exchange_rounds() const;
+  // P2P syncs without overlapped rounds (one round, or sparse=False): the
+  // stream the local route runs on beside the exchange (null when there is
+  // none), and the fork / join around it
+  cudaStream_t exchange_side_stream() const;
+  ws_status exchange_fork(cudaStream_t s, cudaStream_t side);
+  ws_status exchange_join(cudaStream_t s, cudaStream_t side);
   ws_status exchange_pack(const ws_sync_options& o, int next_arena, int round, cudaStream_t s,
                           uint32_t* launches);
   ws_status exchange_apply(int round, cudaStream_t s, uint32_t* launches);

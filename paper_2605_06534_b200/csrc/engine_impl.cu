@@ -398,7 +398,7 @@ ws_status ws_engine::sync_begin(SyncCtx& x, const ws_sync_options& o, cudaStream
   return WS_OK;
 }
 
-ws_status ws_engine::sync_encode(SyncCtx& x, cudaStream_t s) {
+ws_status ws_engine::sync_encode(SyncCtx& x, cudaStream_t s, bool run_local) {
   const ws_sync_options& o = x.o;
   if (o.sparse && ntiles_) {
     // K1 reserves each super-tile's records with an atomic on its segment's count
@@ -418,6 +418,7 @@ ws_status ws_engine::sync_encode(SyncCtx& x, cudaStream_t s) {
     }
   }
   WS_CUDA_TRY(cudaEventRecord(x.ev[2], s), "event");
+  if (!run_local) return WS_OK;  // the caller runs the local route (and ev[3])
   if (!encode_only_) {  // relay pusher: the serving side applies what it pulls
     ws_status st = local_route(o, x.pa, x.na, s, &x.launches);
     if (st != WS_OK) return st;
@@ -505,10 +506,25 @@ ws_status ws_engine::sync_step_impl(const ws_sync_options& o, cudaStream_t s,
     st = sync_rounds(o, x.pa, x.na, s, &x.launches, x.ev);
     if (st != WS_OK) return st;
   } else {
-    st = sync_encode(x, s);
+    // no overlapped rounds: the local route runs on a side stream beside the
+    // pack and the receive-side apply (disjoint serving boxes; it overlaps
+    // the NVLink transfer with this GPU's own HBM copy / apply)
+    cudaStream_t side = exchange_side_stream();
+    const bool fork = side && plan_.world() > 1 && !encode_only_;
+    st = sync_encode(x, s, !fork);
     if (st != WS_OK) return st;
+    if (fork) {
+      st = exchange_fork(s, side);
+      if (st == WS_OK) st = local_route(o, x.pa, x.na, side, &x.launches);
+      if (st != WS_OK) return st;
+      WS_CUDA_TRY(cudaEventRecord(x.ev[3], side), "event");
+    }
     if (plan_.world() > 1 && !encode_only_) {
       st = exchange(o, x.na, s, &x.launches);
+      if (st != WS_OK) return st;
+    }
+    if (fork) {
+      st = exchange_join(s, side);
       if (st != WS_OK) return st;
     }
   }

@@ -104,6 +104,9 @@ struct ws_engine::Comm {
   cudaStream_t s_enc = nullptr, s_xchg = nullptr;  // high / low priority (R > 1)
   std::vector<cudaEvent_t> ev_round;               // K1 round r done
   cudaEvent_t ev_start = nullptr, ev_xdone = nullptr, ev_encdone = nullptr;
+  // syncs without exchange rounds: the local route's stream beside the exchange
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   void release_peers(std::vector<void*>& v) {
     for (int g = 0; g < (int)v.size(); ++g)
@@ -128,6 +131,9 @@ struct ws_engine::Comm {
     if (ev_start) cudaEventDestroy(ev_start);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
     if (ev_encdone) cudaEventDestroy(ev_encdone);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s_side) cudaStreamDestroy(s_side);
     if (s_enc) cudaStreamDestroy(s_enc);
     if (s_xchg) cudaStreamDestroy(s_xchg);
     cudaFree(d_entries);
@@ -624,6 +630,11 @@ ws_status ws_engine::init_p2p() {
     WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming), "ev");
     WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_encdone, cudaEventDisableTiming), "ev");
   }
+  if (!grouped_) {  // syncs without rounds (one round, or sparse=False)
+    WS_CUDA_TRY(cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking), "stream");
+    WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "ev");
+    WS_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "ev");
+  }
   P.edest = c->d_edest;
   P.ent_cnt = c->d_ent_cnt;
   P.recv_cnt = reinterpret_cast<const uint32_t*>(static_cast<char*>(c->d_head) + kMailboxBytes);
@@ -811,6 +822,26 @@ ws_status ws_engine::exchange_begin(cudaStream_t s, uint32_t* launches) {
   p.epoch = (uint32_t)(c->R * c->step + c->R - 1);  // reached every round of this step
   WS_CUDA_TRY(launch_p2p_ready(p, s), "p2p ready");
   *launches += 1;
+  return WS_OK;
+}
+
+cudaStream_t ws_engine::exchange_side_stream() const {
+  static const bool on = [] {
+    const char* e = ablation_env("WSYNC_SIDE_LOCAL");
+    return !(e && e[0] == '0');
+  }();
+  return on && comm_ && comm_->p2p ? comm_->s_side : nullptr;
+}
+
+ws_status ws_engine::exchange_fork(cudaStream_t s, cudaStream_t side) {
+  WS_CUDA_TRY(cudaEventRecord(comm_->ev_fork, s), "event");
+  WS_CUDA_TRY(cudaStreamWaitEvent(side, comm_->ev_fork, 0), "wait");
+  return WS_OK;
+}
+
+ws_status ws_engine::exchange_join(cudaStream_t s, cudaStream_t side) {
+  WS_CUDA_TRY(cudaEventRecord(comm_->ev_join, side), "event");
+  WS_CUDA_TRY(cudaStreamWaitEvent(s, comm_->ev_join, 0), "wait");
   return WS_OK;
 }
 
